@@ -1,0 +1,158 @@
+/*
+ * rdcnn_cuda.h -- C-ABI of the B200-native FitzHugh-Nagumo RD-CNN stepper.
+ *
+ * Drop-in boundary for the reference's time-stepping path.  Every entry point
+ * names the reference interface it replaces (paths relative to
+ * /root/reference/proj/include/rdcnn/):
+ *
+ *   rdcnn_params_from_gene   make_params<float>(Gene)          model.hpp:24-32
+ *   rdcnn_sim_create         StepBuffers<float>(GridState)     kernels.hpp:22-38
+ *   rdcnn_sim_upload         GridState<float> u/v planes        grid.hpp:31-53
+ *   rdcnn_sim_init           init_center_square / full_random  init.hpp:20-48
+ *   rdcnn_sim_init_image     init_from_image (typ=3)           init.hpp:51-64
+ *   rdcnn_sim_advance        step() x n / run_timed()          kernels.hpp:233-259,
+ *                                                               engine.hpp:98-106
+ *   rdcnn_sim_download       bufs.front readback               engine.hpp:83-92
+ *   rdcnn_checksum_f32       checksum(GridState<float>)        grid.hpp:101-116
+ *   rdcnn_init_*_host        init_* on host buffers            init.hpp:20-48
+ *
+ * Conventions: plain pointers and sizes only; status codes mirror the CLI
+ * exit codes (rdcnn_cli.cpp:28-31): 0 ok, 1 invalid argument, 2 blow-up,
+ * 3 CUDA/device failure.  Every non-zero status leaves a message in the
+ * calling thread's rdcnn_last_error().  A handle owns its device buffers and
+ * its CUDA stream; it may be used by one host thread at a time, distinct
+ * handles are independent (reference SPEC.md:212).  No global mutable state.
+ *
+ * Host layout: row-major planes, index = i*cols + j, batch-major for batched
+ * handles (grid g occupies [g*rows*cols, (g+1)*rows*cols)).
+ */
+#ifndef RDCNN_CUDA_H
+#define RDCNN_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RDCNN_ABI_VERSION 1
+
+enum rdcnn_status {
+  RDCNN_OK = 0,
+  RDCNN_EINVAL = 1,
+  RDCNN_EBLOWUP = 2,
+  RDCNN_ECUDA = 3
+};
+
+enum rdcnn_mode {
+  RDCNN_STRICT = 0, /* default: reference op order, IEEE RN, no FMA, no FTZ */
+  RDCNN_FAST = 1    /* opt-in: FMA-contracted; tolerance-checked, not bit-exact */
+};
+
+/* Gene narrowed to fp32 in kernel order (gene_to_vector, gene.hpp:39-41). */
+typedef struct rdcnn_params_f32 {
+  float dt, a, b, eps, c, du, dv;
+} rdcnn_params_f32;
+
+typedef struct rdcnn_sim* rdcnn_sim_t;
+
+int rdcnn_abi_version(void);
+const char* rdcnn_last_error(void);
+int rdcnn_device_count(int* n);
+
+/* gene7 = {dt, a, b, eps, c, Du, Dv} as doubles; narrows each with T(x). */
+void rdcnn_params_from_gene(const double gene7[7], rdcnn_params_f32* out);
+
+/* rows, cols >= 3 (grid.hpp:49-52); batch >= 1 independent grids of the same
+ * shape; device = CUDA ordinal; mode = rdcnn_mode. */
+int rdcnn_sim_create(int rows, int cols, int batch, int device, int mode,
+                     rdcnn_sim_t* out);
+void rdcnn_sim_destroy(rdcnn_sim_t sim);
+
+/* n = 1 (shared gene) or n = batch (one gene per grid, sweep.hpp:296-309). */
+int rdcnn_sim_set_params(rdcnn_sim_t sim, const rdcnn_params_f32* p, int n);
+
+/* Synchronous host<->device copies of the current state (front buffer).
+ * Pinned host memory gets full link bandwidth; pageable memory also works. */
+int rdcnn_sim_upload(rdcnn_sim_t sim, const float* u, const float* v);
+int rdcnn_sim_download(rdcnn_sim_t sim, float* u, float* v);
+
+/* Device-side initial states, bit-identical to the reference initialisers:
+ * typ 1 = init_center_square, typ 2 = init_full_random (every grid of a
+ * batch from the same seed, sweep.hpp:307 default).  */
+int rdcnn_sim_init(rdcnn_sim_t sim, int typ, uint64_t seed);
+/* typ 3: u = v = float(ka) * float(px/255.0) from an 8-bit rows x cols image
+ * (image.hpp:283, init.hpp:51-64); one image for every grid of a batch. */
+int rdcnn_sim_init_image(rdcnn_sim_t sim, const uint8_t* px, double ka);
+
+/* Advance every grid by `steps` iterations (steps >= 0).  Returns
+ * RDCNN_EBLOWUP if any grid produced a non-finite value; then
+ * first_bad_iter[g] (array of batch entries, may be NULL) holds the 1-based
+ * iteration within this call at which grid g first went non-finite, 0 for
+ * grids that stayed finite.  A blown-up grid stops at that iteration: its
+ * state is the state right after it (reference run_timed leaves bufs.front
+ * there, engine.hpp:103-104); the other grids complete all steps. */
+int rdcnn_sim_advance(rdcnn_sim_t sim, long steps, long* first_bad_iter);
+
+/* Device time of the last advance (CUDA events on the handle's stream). */
+int rdcnn_sim_elapsed_ms(rdcnn_sim_t sim, double* ms);
+/* Kernel launches issued by the last advance (including blow-up replays). */
+int rdcnn_sim_launch_count(rdcnn_sim_t sim, long* n);
+/* Tuning: maximum time levels per launch (1, 2, 4 or 8; default 4) and the
+ * rows per warp segment (0 = automatic). */
+int rdcnn_sim_set_tuning(rdcnn_sim_t sim, int max_levels, int seg_rows);
+/* The handle's CUDA stream (cudaStream_t) for interop with other libraries. */
+int rdcnn_sim_stream(rdcnn_sim_t sim, void** stream);
+/* Device pointers of the current front planes (plane u, plane v), for
+ * zero-copy interop; valid until the next advance/destroy. */
+int rdcnn_sim_device_state(rdcnn_sim_t sim, float** u, float** v);
+
+/* ---- slab mode: one row slab of a larger torus, for multi-GPU runs -------
+ * The slab owns rows [0, rows) of its shard and `ghost` halo rows above and
+ * below.  Device layout per buffer: (rows + 2*ghost) rows, each row = u cols
+ * then v cols (interleaved, so `ghost` rows of both planes are one
+ * contiguous message).  The caller exchanges halos with its ring neighbours
+ * between phases (NCCL send/recv, see paper_2102_10340_b200/slab.py):
+ *   rdcnn_slab_step_boundary(k)   rows [0,ghost) and [rows-ghost,rows) -> back
+ *   ... send back rows [0,ghost) up / [rows-ghost,rows) down, receive ghosts ...
+ *   rdcnn_slab_step_interior(k)   rows [ghost, rows-ghost) -> back
+ *   rdcnn_slab_swap()
+ * k <= ghost levels per block.  `stream` is a cudaStream_t (NULL = the
+ * handle's own stream). */
+int rdcnn_slab_create(int rows, int cols, int ghost, int device, int mode,
+                      rdcnn_sim_t* out);
+/* Initialise the slab as rows [row_offset, row_offset+rows) of a
+ * global_rows x cols lattice built by init typ (1 or 2) from seed. */
+int rdcnn_slab_init(rdcnn_sim_t sim, int typ, uint64_t seed, int global_rows,
+                    int row_offset);
+int rdcnn_slab_step_boundary(rdcnn_sim_t sim, int k, void* stream);
+int rdcnn_slab_step_interior(rdcnn_sim_t sim, int k, void* stream);
+int rdcnn_slab_swap(rdcnn_sim_t sim);
+/* Device pointers (in floats) into the front (which=0) or back (which=1)
+ * buffer: the first owned row and the first top-ghost row; row pitch is
+ * 2*cols floats. */
+int rdcnn_slab_rows_ptr(rdcnn_sim_t sim, int which, float** first_row,
+                        float** first_ghost_row);
+/* Any non-finite value stored so far (1) or not (0); *tag = launch tag. */
+int rdcnn_slab_poll_blowup(rdcnn_sim_t sim, int* bad, unsigned* tag);
+
+/* ---- host helpers (reference-identical, no device needed) --------------- */
+int rdcnn_init_center_square_host(int rows, int cols, uint64_t seed, float* u,
+                                  float* v);
+int rdcnn_init_full_random_host(int rows, int cols, uint64_t seed, float* u,
+                                float* v);
+uint64_t rdcnn_checksum_f32(const float* u, const float* v, size_t cells);
+
+/* ---- self-test of the device arithmetic -------------------------------------
+ * Sweeps all 2^32 fp32 bit patterns x on the device and counts those where
+ * div3_rn(x) differs from IEEE x/3 (finite x) or is finite (non-finite x);
+ * domain 0: every x, domain 1: x = u*u for every u.  */
+int rdcnn_selftest_div3(int device, int domain, uint64_t* mismatches,
+                        uint32_t* first_bad);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RDCNN_CUDA_H */

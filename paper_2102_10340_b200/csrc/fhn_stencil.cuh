@@ -1,0 +1,258 @@
+// fhn_stencil.cuh -- sm_100a register-wavefront stencil for the coupled u/v
+// FitzHugh-Nagumo RD-CNN step (reference proj/include/rdcnn/kernels.hpp:63-72,
+// model.hpp:37-56), advancing K time levels per launch.
+//
+// Mapping:
+//   * one warp owns a column BAND x row SEGMENT of one grid;
+//   * each lane owns W consecutive columns (W=4: one float4 per plane);
+//   * the warp marches down the segment; for each newly loaded level-0 row it
+//     advances every level t=1..K by one row (a skewed wavefront), keeping
+//     only two rows per level in registers;
+//   * left/right neighbours come from the adjacent lanes by warp shuffle;
+//     the outermost `halo_groups` lanes of a band are halo (their values go
+//     stale one column per level and are never stored);
+//   * rows wrap on the torus by index arithmetic (periodic mode) or read
+//     K ghost rows written by the halo exchange (slab mode);
+//   * only level-K rows are stored; their finiteness is folded into one word
+//     per grid (atomicCAS of the launch tag).  Non-finite values are absorbing
+//     and spread one cell per level, so a non-finite value at any level of
+//     the block implies a non-finite stored value; the host replays the block
+//     one level at a time to recover the exact iteration.
+//
+// Arithmetic: in strict mode each operation is one IEEE round-to-nearest op
+// in the reference order (__fadd_rn/__fmul_rn are never contracted), with
+// subnormals preserved (no -ftz).  x/3 uses a three-op corrected reciprocal
+// proven equal to IEEE division on the only domain it sees (x = u*u), see
+// div3_rn below and oracle/div3_check.c.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rdcnn_dev {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// Gene narrowed once to fp32, kernel order {dt,a,b,eps,c,du,dv}
+// (reference model.hpp:24-32, gene.hpp:39-41).
+struct Params {
+  float dt, a, b, eps, c, du, dv;
+};
+
+struct StepArgs {
+  const float* u_in;
+  const float* v_in;
+  float* u_out;
+  float* v_out;
+  long long grid_stride;  // floats between consecutive grids (same for in/out)
+  int rows;               // lattice rows (periodic) or slab rows (ghosted)
+  int cols;               // lattice cols (W divides cols)
+  int pitch;              // floats between consecutive rows
+  int periodic;           // 1: rows wrap mod rows; 0: ghost rows present
+  int ghost;              // ghosted mode: ghost rows above row 0 in the buffer
+  int row_begin, row_end; // output rows computed by this launch
+  int seg_rows;           // H: output rows per warp segment
+  int n_segs;
+  int n_bands;
+  int band_groups;        // useful W-groups per band
+  int halo_groups;        // halo W-groups each side (0 = full-width wrap)
+  int batch;
+  const Params* params;
+  int params_stride;      // 0: one gene for all grids; 1: one per grid
+  unsigned* flags;        // per grid: 0 clean, else tag of the first bad launch
+  unsigned tag;           // this launch's tag (launch index + 1)
+};
+
+// ---------------------------------------------------------------------------
+// Per-cell arithmetic.
+// ---------------------------------------------------------------------------
+
+// RN(x/3) for every x the kernel can present (x = RN(u*u): +0, positive,
+// +inf or NaN).  q0 = RN(x*R), e = x - 3*q0 exactly (FMA), q = RN(q0 + e*R).
+// Exhaustively verified over all 2^32 inputs (CPU: oracle/div3_check.c; GPU:
+// rdcnn_selftest_div3); the single mismatch is x = -0.0, which u*u never
+// produces.  Non-finite x yields a non-finite q, so blow-up is preserved.
+__device__ __forceinline__ float div3_rn(float x) {
+  const float R = __uint_as_float(0x3EAAAAABu);  // RN(1/3)
+  const float q0 = __fmul_rn(x, R);
+  const float e = __fmaf_rn(-q0, 3.0f, x);
+  return __fmaf_rn(e, R, q0);
+}
+
+// kern::stencil_cell (kernels.hpp:63-72) with reaction_u/v (model.hpp:37-46):
+//   lap   = right + left + down + up - 4*c          (down = row i+1)
+//   u+    = u + dt*( u*(c - u*u/3) - v + Du*lap_u )
+//   v+    = v + dt*( -eps*(u - b*v + a) + Dv*lap_v )
+template <bool kFast>
+__device__ __forceinline__ void fhn_cell(float uc, float vc, float ur, float ul,
+                                         float ud, float uu, float vr, float vl,
+                                         float vd, float vu, const Params& p,
+                                         float neg_eps, float& un, float& vn) {
+  if constexpr (!kFast) {
+    const float lap_u =
+        __fsub_rn(__fadd_rn(__fadd_rn(__fadd_rn(ur, ul), ud), uu), __fmul_rn(4.0f, uc));
+    const float lap_v =
+        __fsub_rn(__fadd_rn(__fadd_rn(__fadd_rn(vr, vl), vd), vu), __fmul_rn(4.0f, vc));
+    const float f1 = __fsub_rn(__fmul_rn(uc, __fsub_rn(p.c, div3_rn(__fmul_rn(uc, uc)))), vc);
+    const float f2 = __fmul_rn(neg_eps, __fadd_rn(__fsub_rn(uc, __fmul_rn(p.b, vc)), p.a));
+    un = __fadd_rn(uc, __fmul_rn(p.dt, __fadd_rn(f1, __fmul_rn(p.du, lap_u))));
+    vn = __fadd_rn(vc, __fmul_rn(p.dt, __fadd_rn(f2, __fmul_rn(p.dv, lap_v))));
+  } else {
+    // Opt-in fast mode: same formula, FMA-contracted and reassociated.
+    // Validated statistically, never bit-exact.
+    const float lap_u = __fmaf_rn(-4.0f, uc, (ur + ul) + (ud + uu));
+    const float lap_v = __fmaf_rn(-4.0f, vc, (vr + vl) + (vd + vu));
+    const float f1 = __fmaf_rn(uc, __fmaf_rn(-uc * uc, 0.333333343f, p.c), -vc);
+    const float f2 = neg_eps * (__fmaf_rn(-p.b, vc, uc) + p.a);
+    un = __fmaf_rn(p.dt, __fmaf_rn(p.du, lap_u, f1), uc);
+    vn = __fmaf_rn(p.dt, __fmaf_rn(p.dv, lap_v, f2), vc);
+  }
+}
+
+template <int W>
+struct Row {
+  float u[W];
+  float v[W];
+};
+
+template <int W>
+__device__ __forceinline__ void load_row(const float* __restrict__ u,
+                                         const float* __restrict__ v, size_t off,
+                                         Row<W>& r) {
+  if constexpr (W == 4) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(u + off));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(v + off));
+    r.u[0] = a.x; r.u[1] = a.y; r.u[2] = a.z; r.u[3] = a.w;
+    r.v[0] = b.x; r.v[1] = b.y; r.v[2] = b.z; r.v[3] = b.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      r.u[k] = __ldg(u + off + k);
+      r.v[k] = __ldg(v + off + k);
+    }
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void store_row(float* __restrict__ u, float* __restrict__ v,
+                                          size_t off, const Row<W>& r) {
+  if constexpr (W == 4) {
+    __stcs(reinterpret_cast<float4*>(u + off), make_float4(r.u[0], r.u[1], r.u[2], r.u[3]));
+    __stcs(reinterpret_cast<float4*>(v + off), make_float4(r.v[0], r.v[1], r.v[2], r.v[3]));
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      u[off + k] = r.u[k];
+      v[off + k] = r.v[k];
+    }
+  }
+}
+
+// One level of one row: out = step(center) given the rows above/below.
+template <int W, bool kFast>
+__device__ __forceinline__ void level_row(const Row<W>& up, const Row<W>& c,
+                                          const Row<W>& dn, Row<W>& out,
+                                          const Params& p, float neg_eps,
+                                          int lane_l, int lane_r) {
+  const float ul = __shfl_sync(kFull, c.u[W - 1], lane_l);
+  const float ur = __shfl_sync(kFull, c.u[0], lane_r);
+  const float vl = __shfl_sync(kFull, c.v[W - 1], lane_l);
+  const float vr = __shfl_sync(kFull, c.v[0], lane_r);
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const float u_l = k > 0 ? c.u[k - 1] : ul;
+    const float u_r = k < W - 1 ? c.u[k + 1] : ur;
+    const float v_l = k > 0 ? c.v[k - 1] : vl;
+    const float v_r = k < W - 1 ? c.v[k + 1] : vr;
+    fhn_cell<kFast>(c.u[k], c.v[k], u_r, u_l, dn.u[k], up.u[k], v_r, v_l, dn.v[k],
+                    up.v[k], p, neg_eps, out.u[k], out.v[k]);
+  }
+}
+
+__device__ __forceinline__ int wrap_index(int x, int n) {
+  int r = x % n;
+  return r < 0 ? r + n : r;
+}
+
+// K levels per launch, W columns per lane.
+template <int K, int W, bool kFast>
+__global__ void __launch_bounds__(128) fhn_wavefront_kernel(const StepArgs a) {
+  const int lane = threadIdx.x & 31;
+  const long long warp_id = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long per_grid = (long long)a.n_segs * a.n_bands;
+  if (warp_id >= per_grid * a.batch) return;
+  const int g = int(warp_id / per_grid);
+  const int rem = int(warp_id - (long long)g * per_grid);
+  const int band = rem % a.n_bands;
+  const int seg = rem / a.n_bands;
+
+  // A grid that already blew up in an earlier launch of this advance stays
+  // frozen, so the input of its first bad launch survives for the replay.
+  if (a.flags != nullptr && *(volatile unsigned*)(a.flags + g) != 0u) return;
+
+  const Params p = a.params[(size_t)g * a.params_stride];
+  const float neg_eps = -p.eps;  // reference model.hpp:45 negates eps first
+
+  const int G = a.cols / W;
+  const int gl = band * a.band_groups - a.halo_groups + lane;
+  const int grp = wrap_index(gl, G);
+  // Store the band's useful lanes; gl >= G only when a band overhangs a grid
+  // narrower than itself (the wrapped duplicates are not stored twice).
+  const bool store =
+      lane >= a.halo_groups && lane < a.halo_groups + a.band_groups && gl < G;
+  const int lane_l = (lane + 31) & 31;
+  const int lane_r = (lane + 1) & 31;
+
+  const size_t goff = (size_t)g * (size_t)a.grid_stride + (size_t)grp * W;
+  const float* __restrict__ uin = a.u_in + goff;
+  const float* __restrict__ vin = a.v_in + goff;
+  float* __restrict__ uout = a.u_out + goff;
+  float* __restrict__ vout = a.v_out + goff;
+
+  const int r0 = a.row_begin + seg * a.seg_rows;
+  const int r1 = min(r0 + a.seg_rows, a.row_end);
+  const int nt = (r1 - r0) + 2 * K;
+
+  auto in_row = [&](int x) -> size_t {
+    const int r = a.periodic ? wrap_index(x, a.rows) : x + a.ghost;
+    return (size_t)r * (size_t)a.pitch;
+  };
+  auto out_row = [&](int y) -> size_t {
+    return (size_t)(a.periodic ? y : y + a.ghost) * (size_t)a.pitch;
+  };
+
+  Row<W> win[K][2];
+  Row<W> pre;
+  load_row<W>(uin, vin, in_row(r0 - K), pre);
+  unsigned mx = 0u;
+
+  for (int j = 0; j < nt; ++j) {
+    Row<W> n = pre;
+    if (j + 1 < nt) load_row<W>(uin, vin, in_row(r0 - K + j + 1), pre);
+#pragma unroll
+    for (int t = 1; t <= K; ++t) {
+      Row<W> o;
+      if (j >= 2 * t) {
+        level_row<W, kFast>(win[t - 1][0], win[t - 1][1], n, o, p, neg_eps, lane_l, lane_r);
+      } else {
+        o = n;
+      }
+      win[t - 1][0] = win[t - 1][1];
+      win[t - 1][1] = n;
+      n = o;
+    }
+    if (j >= 2 * K && store) {
+      store_row<W>(uout, vout, out_row(r0 + j - 2 * K), n);
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        mx = max(mx, __float_as_uint(n.u[k]) & 0x7FFFFFFFu);
+        mx = max(mx, __float_as_uint(n.v[k]) & 0x7FFFFFFFu);
+      }
+    }
+  }
+
+  mx = __reduce_max_sync(kFull, mx);
+  if (lane == 0 && mx >= 0x7F800000u && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);
+}
+
+}  // namespace rdcnn_dev

@@ -1,0 +1,178 @@
+"""Row-slab sharding of one large torus across GPUs (one process per GPU).
+
+Each rank owns ``rows // world`` consecutive rows of the global lattice
+(SURVEY.md §8e).  Per block of ``k`` time levels:
+
+1. ``boundary`` kernel: the ``ghost`` rows at each edge of the slab, which
+   need the neighbours' rows (held in the ghost rows from the last exchange);
+2. halo exchange of the freshly computed edge rows with the ring neighbours
+   (rank r-1 above, r+1 below, periodic: rank 0's top ghosts are rank P-1's
+   last rows, the torus row wrap of kernels.hpp:46-47), on the NCCL stream;
+3. ``interior`` kernel on the compute stream, overlapping the exchange;
+4. wait for the exchange, swap buffers.
+
+Column wrap stays inside each slab.  Arithmetic per cell is unchanged, so
+the result is bit-identical to the single-GPU periodic run at any world size.
+
+The exchange is a plain function of four row blocks so it can be exercised on
+CPU tensors with the gloo backend (tests/test_slab_gloo.py) and on GPUs with
+NCCL (bench.py --gpus N).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Callable, Optional
+
+from . import _lib
+from ._lib import RDCNN_FAST, RDCNN_STRICT, check, load
+
+
+class _CudaRows:
+    """Zero-copy view of device rows for torch (``__cuda_array_interface__``)."""
+
+    def __init__(self, ptr: int, rows: int, width: int):
+        self.__cuda_array_interface__ = {
+            "shape": (rows, width), "typestr": "<f4", "data": (int(ptr), False), "version": 2,
+        }
+
+
+def ring_neighbours(rank: int, world: int):
+    """(prev, next): the slab above and the slab below on the periodic ring."""
+    return (rank - 1) % world, (rank + 1) % world
+
+
+def exchange_ops(send_first, send_last, recv_top, recv_bottom, rank: int, world: int):
+    """The four point-to-point transfers of one halo exchange, in the order
+    they must be issued so that sends and receives between one pair of ranks
+    match in issue order even when prev == next (world == 2).
+
+    send_first  -> prev's bottom ghosts     recv_top    <- prev's last rows
+    send_last   -> next's top ghosts        recv_bottom <- next's first rows
+    """
+    prev, nxt = ring_neighbours(rank, world)
+    return [("send", send_last, nxt), ("send", send_first, prev),
+            ("recv", recv_top, prev), ("recv", recv_bottom, nxt)]
+
+
+def exchange_halos(send_first, send_last, recv_top, recv_bottom, rank: int, world: int,
+                   group=None):
+    """Post the halo exchange; returns a list of works to wait on (empty for
+    world == 1, where the ring closes on itself and the wrap is a local copy)."""
+    if world == 1:
+        recv_top.copy_(send_last)
+        recv_bottom.copy_(send_first)
+        return []
+    import torch.distributed as dist
+
+    ops = []
+    for kind, tensor, peer in exchange_ops(send_first, send_last, recv_top, recv_bottom, rank, world):
+        fn = dist.isend if kind == "send" else dist.irecv
+        ops.append(dist.P2POp(fn, tensor, peer, group))
+    return dist.batch_isend_irecv(ops)
+
+
+class SlabStepper:
+    """One rank's slab of a global_rows x cols torus on its own GPU."""
+
+    def __init__(self, global_rows: int, cols: int, rank: int, world: int, ghost: int = 4,
+                 device: int = 0, mode: str = "strict",
+                 exchange: Optional[Callable] = None, seg_rows: int = 0):
+        if global_rows % world:
+            raise ValueError(f"global rows {global_rows} not divisible by world size {world}")
+        self._lib = load()
+        self.global_rows, self.cols, self.rank, self.world = global_rows, cols, rank, world
+        self.rows = global_rows // world
+        self.ghost = ghost
+        self.device = device
+        self.exchange = exchange or exchange_halos
+        h = ctypes.c_void_p()
+        m = RDCNN_FAST if mode == "fast" else RDCNN_STRICT
+        check(self._lib.rdcnn_slab_create(self.rows, cols, ghost, device, m, ctypes.byref(h)))
+        self._h = h
+        check(self._lib.rdcnn_sim_set_tuning(self._h, ghost, seg_rows))
+        self.launches = 0
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.rdcnn_sim_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- state ---------------------------------------------------------------
+    def init(self, typ: int, seed: int):
+        check(self._lib.rdcnn_slab_init(self._h, typ, ctypes.c_uint64(seed), self.global_rows,
+                                        self.rank * self.rows))
+
+    def set_params(self, gene):
+        from .engine import params_from_gene
+        p = params_from_gene(gene)
+        check(self._lib.rdcnn_sim_set_params(self._h, ctypes.byref(p), 1))
+
+    def upload(self, u, v):
+        import numpy as np
+        u = np.ascontiguousarray(u, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        check(self._lib.rdcnn_sim_upload(self._h, u.ctypes.data, v.ctypes.data))
+
+    def download(self):
+        import numpy as np
+        n = self.rows * self.cols
+        u = np.empty(n, np.float32)
+        v = np.empty(n, np.float32)
+        check(self._lib.rdcnn_sim_download(self._h, u.ctypes.data, v.ctypes.data))
+        return u, v
+
+    def _views(self, which: int):
+        import torch
+
+        first, ghost0 = ctypes.c_void_p(), ctypes.c_void_p()
+        check(self._lib.rdcnn_slab_rows_ptr(self._h, which, ctypes.byref(first), ctypes.byref(ghost0)))
+        g, w = self.ghost, 2 * self.cols
+        bpr = 4 * w  # bytes per interleaved row
+        dev = f"cuda:{self.device}"
+        as_t = lambda ptr: torch.as_tensor(_CudaRows(ptr, g, w), device=dev)  # noqa: E731
+        send_first = as_t(first.value)
+        send_last = as_t(first.value + (self.rows - g) * bpr)
+        recv_top = as_t(ghost0.value)
+        recv_bottom = as_t(first.value + self.rows * bpr)
+        return send_first, send_last, recv_top, recv_bottom
+
+    # -- stepping ------------------------------------------------------------
+    def fill_ghosts(self):
+        """Exchange the front buffer's edge rows (before the first block)."""
+        import torch
+
+        works = self.exchange(*self._views(0), self.rank, self.world)
+        for w in works:
+            w.wait()
+        torch.cuda.current_stream(self.device).synchronize()
+
+    def advance(self, steps: int, stream=None):
+        """Advance by `steps` iterations in blocks of <= ghost levels."""
+        import torch
+
+        st = stream or torch.cuda.current_stream(self.device)
+        sp = ctypes.c_void_p(st.cuda_stream)
+        done = 0
+        while done < steps:
+            k = self.ghost
+            while k > steps - done:
+                k //= 2
+            check(self._lib.rdcnn_slab_step_boundary(self._h, k, sp))
+            works = self.exchange(*self._views(1), self.rank, self.world)
+            check(self._lib.rdcnn_slab_step_interior(self._h, k, sp))
+            for w in works:
+                w.wait()
+            check(self._lib.rdcnn_slab_swap(self._h))
+            self.launches += 3
+            done += k
+
+    def blew_up(self) -> bool:
+        bad = ctypes.c_int()
+        check(self._lib.rdcnn_slab_poll_blowup(self._h, ctypes.byref(bad), None))
+        return bool(bad.value)

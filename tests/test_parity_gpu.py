@@ -1,0 +1,364 @@
+"""Parity of the sm_100a path (through the C-ABI) with the reference.
+
+Bit-exact (strict mode) against:
+  * tests/golden/golden.json  -- digests produced by the reference itself
+                                 (oracle/_ref, see tests/golden/make_golden.py)
+  * the C oracle (oracle/fhn_oracle.c) on seeded inputs of many shapes,
+  * size-independent properties at BASELINE sizes (shift equivariance,
+    uniform preservation, slab == periodic).
+The reference's own test names are cited per test.
+"""
+import numpy as np
+import pytest
+
+import paper_2102_10340_b200 as fhn
+from paper_2102_10340_b200 import engine
+
+pytestmark = pytest.mark.gpu
+
+LEVELS = (1, 2, 4, 8)
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def gene_from7(g7):
+    return fhn.Gene(dt=g7[0], a=g7[1], b=g7[2], eps=g7[3], c=g7[4], Du=g7[5], Dv=g7[6])
+
+
+# --------------------------------------------------------------------------
+# Arithmetic self-test
+# --------------------------------------------------------------------------
+
+def test_div3_exhaustive_on_device():
+    """div3_rn == IEEE x/3 for all 2^32 inputs but -0.0, and for every x=u*u."""
+    import ctypes
+    lib = fhn.load()
+    n, first = ctypes.c_uint64(), ctypes.c_uint32()
+    assert lib.rdcnn_selftest_div3(0, 0, ctypes.byref(n), ctypes.byref(first)) == 0
+    assert (n.value, first.value) == (1, 0x80000000)
+    assert lib.rdcnn_selftest_div3(0, 1, ctypes.byref(n), ctypes.byref(first)) == 0
+    assert n.value == 0
+
+
+# --------------------------------------------------------------------------
+# Golden digests from the reference itself
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("levels", LEVELS)
+def test_golden_cases(golden, levels):
+    """criterion 1 / 10 / test_engine blow-up, plus the exact-order backend
+    equivalence cases of test_kernels.cpp:141-213, at every fusion depth."""
+    for case in golden:
+        r, c = case["rows"], case["cols"]
+        with fhn.Simulator(r, c, levels=levels) as sim:
+            sim.set_params(gene_from7(case["gene7"]))
+            sim.init(case["typ"], case["seed"])
+            u0, v0 = sim.download()
+            assert f"{fhn.checksum(fhn.GridState(r, c, u0, v0)):016x}" == case["init_checksum"], case["name"]
+            bad = sim.advance(case["iters"])
+            assert int(bad[0]) == case["bad_iter"], (case["name"], levels)
+            if case["bad_iter"] == 0:
+                u, v = sim.download()
+                got = fhn.checksum(fhn.GridState(r, c, u, v))
+                assert f"{got:016x}" == case["checksum"], (case["name"], levels)
+
+
+def test_golden_split_advances(golden):
+    """Advancing in uneven chunks (snapshot-style) gives the same digest."""
+    case = next(c for c in golden if c["name"] == "kat_crit1_256_typ1_s42_1000")
+    with fhn.Simulator(256, 256, levels=8) as sim:
+        sim.init(1, 42)
+        for chunk in (1, 3, 7, 13, 200, 376, 400):
+            assert int(sim.advance(chunk)[0]) == 0
+        u, v = sim.download()
+    assert f"{fhn.checksum(fhn.GridState(256, 256, u, v)):016x}" == case["checksum"]
+
+
+# --------------------------------------------------------------------------
+# Oracle parity on seeded inputs of many shapes
+# --------------------------------------------------------------------------
+
+SHAPES = [
+    (3, 3), (3, 4), (4, 3), (5, 7), (11, 11), (17, 23), (32, 48), (9, 128), (128, 128),
+    (64, 64), (33, 256), (40, 124), (31, 132), (61, 1000), (200, 36), (257, 120), (96, 512),
+]
+
+
+@pytest.mark.parametrize("rows,cols", SHAPES)
+def test_random_shapes_vs_oracle(oracle, rows, cols):
+    iters = 23
+    u0, v0 = oracle.init(2, rows, cols, 1000 + rows * 7 + cols)
+    ou, ov, obad = oracle.run(rows, cols, u0, v0, iters)
+    assert obad == 0
+    for levels in LEVELS:
+        for seg in (0, 1, 5):
+            with fhn.Simulator(rows, cols, levels=levels, seg_rows=seg) as sim:
+                sim.upload(u0, v0)
+                assert int(sim.advance(iters)[0]) == 0
+                u, v = sim.download()
+            assert np.array_equal(bits(u), bits(ou)), (rows, cols, levels, seg)
+            assert np.array_equal(bits(v), bits(ov)), (rows, cols, levels, seg)
+
+
+def test_device_init_matches_host_init(oracle):
+    """rdcnn_sim_init (device splitmix64) == init_* of the reference (rng.hpp)."""
+    for typ, (r, c) in [(1, (11, 11)), (1, (64, 100)), (1, (513, 257)), (2, (3, 3)), (2, (77, 130)),
+                        (2, (1024, 1024))]:
+        ou, ov = oracle.init(typ, r, c, 1234)
+        with fhn.Simulator(r, c) as sim:
+            sim.init(typ, 1234)
+            u, v = sim.download()
+        assert np.array_equal(bits(u), bits(ou)) and np.array_equal(bits(v), bits(ov)), (typ, r, c)
+        hs = fhn.init_center_square(r, c, 1234) if typ == 1 else fhn.init_full_random(r, c, 1234)
+        assert np.array_equal(bits(hs.u), bits(ou)) and np.array_equal(bits(hs.v), bits(ov))
+
+
+def test_image_init_and_edge_run(oracle):
+    """typ=3 (init.hpp:51-64): u = v = float(ka)*float(px/255); then 200 steps."""
+    rows, cols = 192, 260
+    i, j = np.mgrid[0:rows, 0:cols]
+    px = ((i * 7 + j * 3) & 0xFF).astype(np.uint8)  # test_cli.cpp:183-186 ramp
+    for ka in (1.0, 0.7):
+        ou, ov = oracle.init_image(px, ka)
+        with fhn.Simulator(rows, cols) as sim:
+            sim.init_image(px, ka)
+            u, v = sim.download()
+            assert np.array_equal(bits(u), bits(ou)) and np.array_equal(bits(v), bits(ov))
+            assert int(sim.advance(200)[0]) == 0
+            u, v = sim.download()
+        ru, rv, bad = oracle.run(rows, cols, ou, ov, 200)
+        assert bad == 0 and np.array_equal(bits(u), bits(ru)) and np.array_equal(bits(v), bits(rv))
+        host = fhn.init_from_image(px, fhn.Gene(ka=ka))
+        assert np.array_equal(bits(host.u), bits(ou))
+
+
+# --------------------------------------------------------------------------
+# Blow-up semantics (test_engine.cpp:82-108, acceptance 11)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("levels", LEVELS)
+def test_blowup_iteration(oracle, levels):
+    g = fhn.Gene(dt=100.0)
+    for n in (16, 32, 20):
+        u0, v0 = oracle.init(1, n, n, 42)
+        _, _, want = oracle.run(n, n, u0, v0, 1000, g.to_vector())
+        assert want > 0
+        with fhn.Simulator(n, n, levels=levels) as sim:
+            sim.set_params(g)
+            sim.upload(u0, v0)
+            assert int(sim.advance(1000)[0]) == want
+            u, v = sim.download()
+        # the state is the one right after the bad iteration
+        ou, ov, _ = oracle.run(n, n, u0, v0, want, g.to_vector())
+        assert np.array_equal(np.isfinite(u), np.isfinite(ou))
+        fin = np.isfinite(ou) & np.isfinite(ov)
+        assert np.array_equal(bits(u)[fin], bits(ou)[fin])
+    # the reference API surface raises BlowUpError(4)
+    bufs = fhn.StepBuffers(fhn.init_center_square(16, 16, 42))
+    with pytest.raises(fhn.BlowUpError) as e:
+        fhn.run_timed(bufs, g, fhn.make_backend("cuda"), 1000)
+    assert e.value.iteration == 4
+
+
+def test_blowup_split_across_calls(oracle):
+    g = fhn.Gene(dt=100.0)
+    u0, v0 = oracle.init(1, 16, 16, 42)
+    with fhn.Simulator(16, 16, levels=8) as sim:
+        sim.set_params(g)
+        sim.upload(u0, v0)
+        assert int(sim.advance(2)[0]) == 0
+        assert int(sim.advance(10)[0]) == 2  # iteration 4 overall = 2nd of this call
+
+
+# --------------------------------------------------------------------------
+# Batched sweeps (sweep.hpp:255-326): per-grid genes and blow-up
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("levels", (1, 4, 8))
+def test_batch_per_grid_genes(oracle, levels):
+    rows, cols, iters = 40, 128, 57
+    genes = [fhn.Gene(Du=du, Dv=dv) for du, dv in [(0.02, 0.5), (0.3, 1.0), (0.5, 0.8), (0.7, 0.8)]]
+    genes.append(fhn.Gene(dt=100.0))        # blows up
+    genes.append(fhn.Gene(a=-0.05))
+    B = len(genes)
+    u0, v0 = oracle.init(1, rows, cols, 42)
+    with fhn.Simulator(rows, cols, batch=B, levels=levels) as sim:
+        sim.set_params(genes)
+        sim.init(1, 42)
+        bad = sim.advance(iters)
+        u, v = sim.download()
+    u = u.reshape(B, -1)
+    v = v.reshape(B, -1)
+    for k, g in enumerate(genes):
+        ou, ov, obad = oracle.run(rows, cols, u0, v0, iters, g.to_vector())
+        assert int(bad[k]) == obad, k
+        fin = np.isfinite(ou) & np.isfinite(ov)
+        assert np.array_equal(fin, np.isfinite(u[k]) & np.isfinite(v[k])), k
+        assert np.array_equal(bits(u[k])[fin], bits(ou)[fin]), k
+        assert np.array_equal(bits(v[k])[fin], bits(ov)[fin]), k
+
+
+# --------------------------------------------------------------------------
+# Reference API surface (engine.hpp / kernels.hpp semantics)
+# --------------------------------------------------------------------------
+
+def test_step_api_and_run_snapshots(oracle):
+    cfg = fhn.RunConfig(nn=24, nm=24, iter_max=120, nssp=4, seed=42)
+    init = fhn.init_center_square(24, 24, 42)
+    out = fhn.run(cfg, fhn.Gene(), init.copy())
+    assert out.snapshots.labels == [0, 30, 60, 90, 120]
+    assert np.array_equal(bits(out.snapshots.frames_u[0]), bits(init.u))
+    assert out.final_state == fhn.GridState(24, 24, out.snapshots.frames_u[-1], out.snapshots.frames_v[-1])
+    for f, label in enumerate(out.snapshots.labels):
+        ou, ov, _ = oracle.run(24, 24, init.u, init.v, label)
+        assert np.array_equal(bits(out.snapshots.frames_u[f]), bits(ou))
+        assert np.array_equal(bits(out.snapshots.frames_v[f]), bits(ov))
+    # per-call step() == run
+    bufs = fhn.StepBuffers(init.copy())
+    for _ in range(120):
+        assert fhn.step(bufs, fhn.Gene())
+    assert bufs.front == out.final_state
+    seen = []
+    fhn.run(fhn.RunConfig(nn=16, nm=16, iter_max=50, nssp=5, seed=1), fhn.Gene(),
+            fhn.init_center_square(16, 16, 1), lambda lab, el: seen.append(lab))
+    assert seen == [10, 20, 30, 40, 50]
+
+
+def test_uniform_state_stays_uniform_and_follows_scalar_orbit(oracle):
+    """test_kernels.cpp:65-81 / test_engine.cpp:110-137 at full BASELINE width."""
+    n = 1024
+    u0 = np.full(n * n, 0.5, np.float32)
+    v0 = np.full(n * n, 0.2, np.float32)
+    su, sv, _ = oracle.run(3, 3, u0[:9], v0[:9], 1000)  # 3x3 uniform = same orbit
+    with fhn.Simulator(n, n, levels=8) as sim:
+        sim.upload(u0, v0)
+        assert int(sim.advance(1000)[0]) == 0
+        u, v = sim.download()
+    assert (bits(u) == bits(su)[0]).all() and (bits(v) == bits(sv)[0]).all()
+
+
+def test_shift_equivariance_full_size():
+    """test_kernels.cpp:187-199 / acceptance 2 at the cfg2 lattice (4096^2)."""
+    n, iters, di, dj = 4096, 300, 777, 1301
+    st = fhn.init_full_random(n, n, 7)
+    U = st.u.reshape(n, n)
+    V = st.v.reshape(n, n)
+    with fhn.Simulator(n, n, levels=8) as sim:
+        sim.upload(U, V)
+        assert int(sim.advance(iters)[0]) == 0
+        a_u, a_v = sim.download()
+        sim.upload(np.roll(U, (di, dj), (0, 1)), np.roll(V, (di, dj), (0, 1)))
+        assert int(sim.advance(iters)[0]) == 0
+        b_u, b_v = sim.download()
+    assert np.array_equal(bits(np.roll(a_u.reshape(n, n), (di, dj), (0, 1))), bits(b_u.reshape(n, n)))
+    assert np.array_equal(bits(np.roll(a_v.reshape(n, n), (di, dj), (0, 1))), bits(b_v.reshape(n, n)))
+
+
+def test_full_size_prefix_vs_reference():
+    """cfg2 lattice (4096^2, slow-growth gene) against the reference's own
+    parallel backend on a CPU-feasible prefix."""
+    from oracle.oracle import Reference
+    ref = Reference()
+    n, iters = 4096, 60
+    g7 = [0.1, -0.05, 1.3, -0.1, 1.0, 0.06, 1.0]
+    u0, v0 = ref.init(2, n, n, 42)
+    ru, rv, bad, _ = ref.run_timed(n, n, u0, v0, iters, g7, backend="parallel")
+    assert bad == 0
+    with fhn.Simulator(n, n, levels=8) as sim:
+        sim.set_params(gene_from7(g7))
+        sim.init(2, 42)
+        assert int(sim.advance(iters)[0]) == 0
+        u, v = sim.download()
+    assert np.array_equal(bits(u), bits(ru)) and np.array_equal(bits(v), bits(rv))
+
+
+# --------------------------------------------------------------------------
+# Fast (FMA) mode: tolerance, not bit-exactness (acceptance 3 analogue)
+# --------------------------------------------------------------------------
+
+def test_fast_mode_tolerance(oracle):
+    n = 128
+    u0, v0 = oracle.init(2, n, n, 11)
+    ou, ov, _ = oracle.run(n, n, u0, v0, 10)
+    with fhn.Simulator(n, n, mode="fast", levels=8) as sim:
+        sim.upload(u0, v0)
+        sim.advance(10)
+        u, v = sim.download()
+    scale = max(np.abs(ou).max(), np.abs(ov).max())
+    dev = max(np.abs(u - ou).max(), np.abs(v - ov).max())
+    assert dev <= 1e-5 * scale
+
+
+# --------------------------------------------------------------------------
+# Slab (multi-GPU) kernels on one GPU: slab mode == periodic mode
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("ghost", (1, 2, 4, 8))
+def test_single_slab_ring_equals_periodic(oracle, ghost):
+    """world=1 ring (ghosts = own wrapped rows) reproduces the periodic run."""
+    import torch
+    from paper_2102_10340_b200.slab import SlabStepper
+
+    rows, cols, iters = 64, 96, 37
+    u0, v0 = oracle.init(2, rows, cols, 5)
+    ou, ov, _ = oracle.run(rows, cols, u0, v0, iters)
+    s = SlabStepper(rows, cols, rank=0, world=1, ghost=ghost, device=0)
+    s.upload(u0, v0)
+    s.fill_ghosts()
+    s.advance(iters)
+    torch.cuda.synchronize()
+    u, v = s.download()
+    assert np.array_equal(bits(u), bits(ou)) and np.array_equal(bits(v), bits(ov))
+    s.close()
+
+
+@pytest.mark.parametrize("world", (2, 3, 4))
+def test_multi_slab_emulated_ring(oracle, world):
+    """`world` slabs on one GPU with the exchange done by device copies in the
+    same ring order as NCCL: the torus result is bit-identical."""
+    import torch
+    from paper_2102_10340_b200.slab import SlabStepper
+
+    rows, cols, iters, ghost = 24 * world, 40, 29, 4
+    u0, v0 = oracle.init(1, rows, cols, 42)
+    u0 = u0.copy()
+    v0 = v0.copy()
+    rng = np.random.default_rng(3)
+    u0 += rng.random(u0.size, dtype=np.float32) * 0.5
+    ou, ov, _ = oracle.run(rows, cols, u0, v0, iters)
+
+    slabs = [SlabStepper(rows, cols, rank=r, world=world, ghost=ghost, device=0,
+                         exchange=lambda *a: []) for r in range(world)]
+    S = rows // world
+    for r, s in enumerate(slabs):
+        s.upload(u0[r * S * cols:(r + 1) * S * cols], v0[r * S * cols:(r + 1) * S * cols])
+
+    def ring_copy(which):
+        views = [s._views(which) for s in slabs]
+        for r in range(world):
+            prev, nxt = (r - 1) % world, (r + 1) % world
+            views[r][2].copy_(views[prev][1])   # top ghosts <- prev's last rows
+            views[r][3].copy_(views[nxt][0])    # bottom ghosts <- next's first rows
+
+    ring_copy(0)
+    done = 0
+    sp = torch.cuda.current_stream().cuda_stream
+    import ctypes
+    lib = fhn.load()
+    while done < iters:
+        k = ghost
+        while k > iters - done:
+            k //= 2
+        for s in slabs:
+            assert lib.rdcnn_slab_step_boundary(s._h, k, ctypes.c_void_p(sp)) == 0
+        ring_copy(1)
+        for s in slabs:
+            assert lib.rdcnn_slab_step_interior(s._h, k, ctypes.c_void_p(sp)) == 0
+            assert lib.rdcnn_slab_swap(s._h) == 0
+        done += k
+    torch.cuda.synchronize()
+    got_u = np.concatenate([s.download()[0] for s in slabs])
+    got_v = np.concatenate([s.download()[1] for s in slabs])
+    assert np.array_equal(bits(got_u), bits(ou)) and np.array_equal(bits(got_v), bits(ov))
