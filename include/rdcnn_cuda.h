@@ -118,8 +118,9 @@ int rdcnn_sim_device_state(rdcnn_sim_t sim, float** u, float** v);
  *   ... send back rows [0,ghost) up / [rows-ghost,rows) down, receive ghosts ...
  *   rdcnn_slab_step_interior(k)   rows [ghost, rows-ghost) -> back
  *   rdcnn_slab_swap()
- * k <= ghost levels per block.  `stream` is a cudaStream_t (NULL = the
- * handle's own stream). */
+ * k <= ghost levels per block.  `stream` is the cudaStream_t to launch on,
+ * taken literally (0 = the legacy default stream; pass rdcnn_sim_stream()'s
+ * value for the handle's own stream). */
 int rdcnn_slab_create(int rows, int cols, int ghost, int device, int mode,
                       rdcnn_sim_t* out);
 /* Initialise the slab as rows [row_offset, row_offset+rows) of a

@@ -57,7 +57,9 @@ struct StepArgs {
   int band_groups;        // useful W-groups per band
   int halo_groups;        // halo W-groups each side (0 = full-width wrap)
   int batch;
-  const Params* params;
+  Params shared;          // the gene when every grid shares one (kernel-param
+                          // space: the FP ops read it as constant-bank operands)
+  const Params* params;   // per-grid genes (kPerGrid instances only)
   int params_stride;      // 0: one gene for all grids; 1: one per grid
   unsigned* flags;        // per grid: 0 clean, else tag of the first bad launch
   unsigned tag;           // this launch's tag (launch index + 1)
@@ -89,8 +91,12 @@ __device__ __forceinline__ void fhn_cell(float uc, float vc, float ur, float ul,
                                          float vd, float vu, const Params& p,
                                          float neg_eps, float& un, float& vn) {
   if constexpr (!kFast) {
-    const float lap_u =
-        __fsub_rn(__fadd_rn(__fadd_rn(__fadd_rn(ur, ul), ud), uu), __fmul_rn(4.0f, uc));
+    // RN(s - RN(4*uc)) == RN(s - 4*uc) == fma(-4, uc, s) whenever 4*uc is
+    // finite (scaling by 4 is exact).  When 4*uc overflows, |uc| > 2^125 so
+    // uc*uc overflows and u+ is non-finite in both forms: the
+    // fused form is bit-identical on every finite outcome.  The v plane has
+    // no such guard and keeps the separate multiply.
+    const float lap_u = __fmaf_rn(-4.0f, uc, __fadd_rn(__fadd_rn(__fadd_rn(ur, ul), ud), uu));
     const float lap_v =
         __fsub_rn(__fadd_rn(__fadd_rn(__fadd_rn(vr, vl), vd), vu), __fmul_rn(4.0f, vc));
     const float f1 = __fsub_rn(__fmul_rn(uc, __fsub_rn(p.c, div3_rn(__fmul_rn(uc, uc)))), vc);
@@ -174,9 +180,41 @@ __device__ __forceinline__ int wrap_index(int x, int n) {
   return r < 0 ? r + n : r;
 }
 
+// Ring depth of the level-0 rows: R0 slots give an (R0-2)-tick prefetch.
+// Measured on B200: 3 slots (1 tick) leave the first use of each row stalled
+// on its load (long-scoreboard); 6 slots (4 ticks) hide it at every depth.
+template <int K>
+struct RingDepth {
+  static constexpr int value = 6;
+};
+
+// Running row index on the torus (periodic) or in the ghosted slab buffer.
+struct RowCursor {
+  int r;       // current buffer row
+  int wrap;    // rows (periodic) or INT_MAX (ghosted: never wraps)
+  __device__ __forceinline__ void next() { r = (r + 1 == wrap) ? 0 : r + 1; }
+};
+
 // K levels per launch, W columns per lane.
-template <int K, int W, bool kFast>
+//
+// Schedule (a skewed wavefront, levels visited top-down within a tick): at
+// tick j the warp has level-0 rows x_0..x_j (x_j = r0 - K + j) and
+//   level t computes row x_j - (2t - 1) from the three level-(t-1) rows
+//   produced at ticks j-3, j-2, j-1 (level 1: the level-0 rows of ticks
+//   j-2, j-1, j).
+// Visiting t = K..1 means no level consumes a row produced in the same tick,
+// so the K level updates of one tick are independent instruction streams the
+// scheduler can interleave (ILP x K), and each level's oldest row slot can be
+// overwritten in place once the level above has read it.
+//
+// Register rotation: level-0 rows live in a ring of R0 slots (tick j -> slot
+// j % R0); level-t rows in rings of 3 (tick j -> slot j % 3).  The tick loop
+// is unrolled by R0 (a multiple of 3) so every slot index is a compile-time
+// constant and no register is copied to advance a window.
+template <int K, int W, bool kFast, bool kPerGrid>
 __global__ void __launch_bounds__(128) fhn_wavefront_kernel(const StepArgs a) {
+  constexpr int R0 = RingDepth<K>::value;
+  constexpr int D = R0 - 2;  // prefetch distance in ticks
   const int lane = threadIdx.x & 31;
   const long long warp_id = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const long long per_grid = (long long)a.n_segs * a.n_bands;
@@ -188,9 +226,13 @@ __global__ void __launch_bounds__(128) fhn_wavefront_kernel(const StepArgs a) {
 
   // A grid that already blew up in an earlier launch of this advance stays
   // frozen, so the input of its first bad launch survives for the replay.
-  if (a.flags != nullptr && *(volatile unsigned*)(a.flags + g) != 0u) return;
+  // (Read here, tested after the first loads are in flight.)
+  const unsigned frozen = a.flags != nullptr ? *(volatile unsigned*)(a.flags + g) : 0u;
 
-  const Params p = a.params[(size_t)g * a.params_stride];
+  // Shared gene: read straight from the kernel-parameter bank, so ptxas never
+  // has to hold (or re-load) it in registers.  Per-grid genes (sweeps) come
+  // from global memory once per warp.
+  const Params p = kPerGrid ? a.params[g] : a.shared;
   const float neg_eps = -p.eps;  // reference model.hpp:45 negates eps first
 
   const int G = a.cols / W;
@@ -208,45 +250,90 @@ __global__ void __launch_bounds__(128) fhn_wavefront_kernel(const StepArgs a) {
   const float* __restrict__ vin = a.v_in + goff;
   float* __restrict__ uout = a.u_out + goff;
   float* __restrict__ vout = a.v_out + goff;
+  const size_t pitch = (size_t)a.pitch;
 
   const int r0 = a.row_begin + seg * a.seg_rows;
-  const int r1 = min(r0 + a.seg_rows, a.row_end);
-  const int nt = (r1 - r0) + 2 * K;
+  const int h = min(a.seg_rows, a.row_end - r0);
+  const int n_load = h + 2 * K;       // level-0 rows x_0 .. x_{n_load-1}
+  const int nt = h + 3 * K - 1;       // ticks until level K has produced h rows
 
-  auto in_row = [&](int x) -> size_t {
-    const int r = a.periodic ? wrap_index(x, a.rows) : x + a.ghost;
-    return (size_t)r * (size_t)a.pitch;
-  };
-  auto out_row = [&](int y) -> size_t {
-    return (size_t)(a.periodic ? y : y + a.ghost) * (size_t)a.pitch;
-  };
+  RowCursor cur{a.periodic ? wrap_index(r0 - K, a.rows) : r0 - K + a.ghost,
+                a.periodic ? a.rows : 0x7FFFFFFF};
+  size_t out_off = (size_t)(a.periodic ? r0 : r0 + a.ghost) * pitch;
 
-  Row<W> win[K][2];
-  Row<W> pre;
-  load_row<W>(uin, vin, in_row(r0 - K), pre);
+  Row<W> ring0[R0];
+  Row<W> win[K > 1 ? K - 1 : 1][3];
   unsigned mx = 0u;
 
-  for (int j = 0; j < nt; ++j) {
-    Row<W> n = pre;
-    if (j + 1 < nt) load_row<W>(uin, vin, in_row(r0 - K + j + 1), pre);
+  // Prime the ring with the rows of ticks 0 .. D-1.
 #pragma unroll
-    for (int t = 1; t <= K; ++t) {
-      Row<W> o;
-      if (j >= 2 * t) {
-        level_row<W, kFast>(win[t - 1][0], win[t - 1][1], n, o, p, neg_eps, lane_l, lane_r);
-      } else {
-        o = n;
-      }
-      win[t - 1][0] = win[t - 1][1];
-      win[t - 1][1] = n;
-      n = o;
+  for (int d = 0; d < D; ++d) {
+    if (d < n_load) {
+      load_row<W>(uin, vin, (size_t)cur.r * pitch, ring0[d]);
+      cur.next();
     }
-    if (j >= 2 * K && store) {
-      store_row<W>(uout, vout, out_row(r0 + j - 2 * K), n);
+  }
+
+  if (frozen != 0u) return;
+
+  for (int j0 = 0; j0 < nt; j0 += R0) {
 #pragma unroll
-      for (int k = 0; k < W; ++k) {
-        mx = max(mx, __float_as_uint(n.u[k]) & 0x7FFFFFFFu);
-        mx = max(mx, __float_as_uint(n.v[k]) & 0x7FFFFFFFu);
+    for (int ph = 0; ph < R0; ++ph) {
+      const int j = j0 + ph;
+      if (j < nt) {
+        // Levels K..2, top-down: level t reads the level-(t-1) rows of ticks
+        // j-3, j-2, j-1 (slots ph, ph+1, ph+2 mod 3) and then level t-1
+        // overwrites slot ph with its tick-j row.
+#pragma unroll
+        for (int t = K; t >= 2; --t) {
+          if (j >= 3 * t - 1 && j < h + 2 * K + t - 1) {
+            const Row<W>& up = win[t - 2][ph % 3];
+            const Row<W>& ce = win[t - 2][(ph + 1) % 3];
+            const Row<W>& dn = win[t - 2][(ph + 2) % 3];
+            if (t < K) {
+              level_row<W, kFast>(up, ce, dn, win[t - 1][ph % 3], p, neg_eps, lane_l, lane_r);
+            } else {
+              Row<W> o;
+              level_row<W, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
+              if (store) {
+                store_row<W>(uout, vout, out_off, o);
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                  mx = max(mx, __float_as_uint(o.u[k]) & 0x7FFFFFFFu);
+                  mx = max(mx, __float_as_uint(o.v[k]) & 0x7FFFFFFFu);
+                }
+              }
+              out_off += pitch;
+            }
+          }
+        }
+        // Level 1 from the level-0 rows of ticks j-2, j-1, j.
+        if (j >= 2 && j < n_load) {
+          const Row<W>& up = ring0[(ph + R0 - 2) % R0];
+          const Row<W>& ce = ring0[(ph + R0 - 1) % R0];
+          const Row<W>& dn = ring0[ph % R0];
+          if constexpr (K == 1) {
+            Row<W> o;
+            level_row<W, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
+            if (store) {
+              store_row<W>(uout, vout, out_off, o);
+#pragma unroll
+              for (int k = 0; k < W; ++k) {
+                mx = max(mx, __float_as_uint(o.u[k]) & 0x7FFFFFFFu);
+                mx = max(mx, __float_as_uint(o.v[k]) & 0x7FFFFFFFu);
+              }
+            }
+            out_off += pitch;
+          } else {
+            level_row<W, kFast>(up, ce, dn, win[0][ph % 3], p, neg_eps, lane_l, lane_r);
+          }
+        }
+        // Refill the slot of tick j-2, just consumed by level 1, with the row
+        // of tick j+D (D ticks of latency hiding).
+        if (j + D < n_load) {
+          load_row<W>(uin, vin, (size_t)cur.r * pitch, ring0[(ph + D) % R0]);
+          cur.next();
+        }
       }
     }
   }

@@ -48,29 +48,70 @@ constexpr int kThreads = 128;  // 4 warps per CTA
 // Kernel dispatch over the compiled (K, W, mode) instances.
 // ---------------------------------------------------------------------------
 
-template <int K, int W, bool F>
-cudaError_t launch_one(const StepArgs& a, long long warps, cudaStream_t s) {
-  const long long blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
-  rdcnn_dev::fhn_wavefront_kernel<K, W, F><<<dim3((unsigned)blocks), dim3(kThreads), 0, s>>>(a);
-  return cudaGetLastError();
+using KernelFn = void (*)(StepArgs);
+
+// Every compiled instance: [W=1|4][K=1,2,4,8][strict|fast][shared|per-grid gene].
+template <int W, int KI, int FI, int PI>
+constexpr KernelFn instance() {
+  constexpr int K = 1 << KI;
+  return &rdcnn_dev::fhn_wavefront_kernel<K, W, FI == 1, PI == 1>;
 }
 
-template <int W, bool F>
-cudaError_t launch_k(int k, const StepArgs& a, long long warps, cudaStream_t s) {
-  switch (k) {
-    case 1: return launch_one<1, W, F>(a, warps, s);
-    case 2: return launch_one<2, W, F>(a, warps, s);
-    case 4: return launch_one<4, W, F>(a, warps, s);
-    case 8: return launch_one<8, W, F>(a, warps, s);
+struct KernelTable {
+  KernelFn fn[2][4][2][2];
+  int resident[2][4][2][2];
+};
+
+template <int W, int KI, int FI, int PI>
+void fill_one(KernelTable& t) {
+  t.fn[W == 4][KI][FI][PI] = instance<W, KI, FI, PI>();
+  t.resident[W == 4][KI][FI][PI] = 0;
+}
+
+template <int W, int KI>
+void fill_k(KernelTable& t) {
+  fill_one<W, KI, 0, 0>(t);
+  fill_one<W, KI, 0, 1>(t);
+  fill_one<W, KI, 1, 0>(t);
+  fill_one<W, KI, 1, 1>(t);
+}
+
+KernelTable make_table() {
+  KernelTable t{};
+  fill_k<1, 0>(t); fill_k<1, 1>(t); fill_k<1, 2>(t); fill_k<1, 3>(t);
+  fill_k<4, 0>(t); fill_k<4, 1>(t); fill_k<4, 2>(t); fill_k<4, 3>(t);
+  return t;
+}
+
+KernelTable& table() {
+  static KernelTable t = make_table();
+  return t;
+}
+
+int k_index(int k) { return k == 1 ? 0 : k == 2 ? 1 : k == 4 ? 2 : 3; }
+
+// Resident CTAs per SM of one instance (cached; occupancy is immutable).
+int resident_blocks(int k, int w, bool fast, bool per_grid) {
+  KernelTable& t = table();
+  int& r = t.resident[w == 4][k_index(k)][fast][per_grid];
+  if (r == 0) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, t.fn[w == 4][k_index(k)][fast][per_grid],
+                                                      kThreads, 0) != cudaSuccess || n < 1)
+      n = 1;
+    r = n;
   }
-  return cudaErrorInvalidValue;
+  return r;
 }
 
-cudaError_t launch_stencil(int k, int w, bool fast, const StepArgs& a, long long warps,
-                           cudaStream_t s) {
+cudaError_t launch_stencil(int k, int w, bool fast, bool per_grid, const StepArgs& a,
+                           long long warps, cudaStream_t s) {
   if (warps <= 0) return cudaSuccess;
-  if (w == 4) return fast ? launch_k<4, true>(k, a, warps, s) : launch_k<4, false>(k, a, warps, s);
-  return fast ? launch_k<1, true>(k, a, warps, s) : launch_k<1, false>(k, a, warps, s);
+  if (k != 1 && k != 2 && k != 4 && k != 8) return cudaErrorInvalidValue;
+  const long long blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
+  KernelFn fn = table().fn[w == 4][k_index(k)][fast][per_grid];
+  fn<<<dim3((unsigned)blocks), dim3(kThreads), 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 // Band/segment decomposition of one launch.
@@ -80,7 +121,7 @@ struct Plan {
 };
 
 Plan make_plan(int cols, int w, int k, int batch, int row_begin, int row_end,
-               int seg_override, int sm_count) {
+               int seg_override, int sm_count, int resident_warps_per_sm) {
   Plan p;
   p.w = w;
   const int G = cols / w;
@@ -100,13 +141,18 @@ Plan make_plan(int cols, int w, int k, int batch, int row_begin, int row_end,
   if (seg_override > 0) {
     h = seg_override;
   } else {
-    // Enough warps for ~16 resident per SM, but segments of at least 4K rows
-    // so the 2K-row wavefront start-up stays a small fraction.
-    const long long target = (long long)std::max(sm_count, 1) * 16;
+    // One full wave of resident warps (every warp runs start to finish with
+    // no tail), but segments of at least 8K rows so the 2K-row wavefront
+    // start-up stays a small fraction.
+    const long long target = (long long)std::max(sm_count, 1) * std::max(resident_warps_per_sm, 4);
     const long long per_seg = (long long)batch * p.n_bands;
     const long long segs = std::max<long long>(1, (target + per_seg - 1) / per_seg);
     h = (int)std::max<long long>(1, (nrows + segs - 1) / segs);
-    h = std::max(h, std::min(nrows, std::max(16, 8 * k)));
+    // Long segments amortise the 2K-row wavefront start-up; small lattices
+    // that cannot fill the chip anyway trade that for more warps.
+    const int h_long = std::max(16, 8 * k);
+    const long long warps_long = per_seg * ((nrows + h_long - 1) / h_long);
+    h = std::max(h, std::min(nrows, warps_long >= target / 2 ? h_long : std::max(4, 2 * k)));
   }
   h = std::min(h, nrows);
   p.seg_rows = h;
@@ -233,6 +279,7 @@ struct rdcnn_sim {
   float* buf[2] = {nullptr, nullptr};
   int cur = 0;            // front buffer index
   Params* d_params = nullptr;
+  Params h_params{};      // the shared gene (params_stride == 0)
   int params_stride = 0;
   unsigned* d_flags = nullptr;  // batch words (+1 scratch for replays)
   unsigned* h_flags = nullptr;  // pinned mirror
@@ -268,6 +315,7 @@ StepArgs base_args(const rdcnn_sim* s, int in_buf, int out_buf) {
   a.periodic = s->slab ? 0 : 1;
   a.ghost = s->slab ? s->ghost : 0;
   a.batch = s->batch;
+  a.shared = s->h_params;
   a.params = s->d_params;
   a.params_stride = s->params_stride;
   a.flags = s->d_flags;
@@ -277,7 +325,10 @@ StepArgs base_args(const rdcnn_sim* s, int in_buf, int out_buf) {
 cudaError_t launch_range(rdcnn_sim* s, int k, StepArgs a, int row_begin, int row_end,
                          cudaStream_t st) {
   const int w = width_for(s);
-  Plan p = make_plan(s->cols, w, k, a.batch, row_begin, row_end, s->seg_rows, s->sm_count);
+  const bool fast = s->mode == RDCNN_FAST;
+  const bool per_grid = a.params_stride != 0;
+  const int rw = resident_blocks(k, w, fast, per_grid) * (kThreads / 32);
+  Plan p = make_plan(s->cols, w, k, a.batch, row_begin, row_end, s->seg_rows, s->sm_count, rw);
   if (p.warps == 0) return cudaSuccess;
   a.row_begin = row_begin;
   a.row_end = row_end;
@@ -287,7 +338,7 @@ cudaError_t launch_range(rdcnn_sim* s, int k, StepArgs a, int row_begin, int row
   a.band_groups = p.band_groups;
   a.halo_groups = p.halo;
   ++s->launches;
-  return launch_stencil(k, w, s->mode == RDCNN_FAST, a, p.warps, st);
+  return launch_stencil(k, w, fast, per_grid, a, p.warps, st);
 }
 
 int alloc_common(rdcnn_sim* s) {
@@ -309,6 +360,7 @@ int alloc_common(rdcnn_sim* s) {
   rdcnn_params_f32 p;
   rdcnn_params_from_gene(g7, &p);
   RDCNN_CUDA_TRY(cudaMemcpyAsync(s->d_params, &p, sizeof(Params), cudaMemcpyHostToDevice, s->stream));
+  std::memcpy(&s->h_params, &p, sizeof(Params));
   s->params_stride = 0;
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
   return RDCNN_OK;
@@ -375,6 +427,12 @@ int replay_grid(rdcnn_sim* s, int g, int in_buf, int k, int final_buf, int* leve
     a.batch = 1;
     a.params = s->d_params + (size_t)g * s->params_stride;
     a.flags = scratch;
+    if (s->params_stride != 0) {
+      // One grid: run it on the shared-gene instance with its own gene.
+      RDCNN_CUDA_TRY(cudaMemcpyAsync(&a.shared, a.params, sizeof(Params), cudaMemcpyDeviceToHost, s->stream));
+      RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+      a.params_stride = 0;
+    }
     a.tag = 1;
     RDCNN_CUDA_TRY(launch_range(s, 1, a, 0, s->rows, s->stream));
     unsigned hv = 0;
@@ -497,6 +555,7 @@ int rdcnn_sim_set_params(rdcnn_sim_t s, const rdcnn_params_f32* p, int n) {
   RDCNN_CUDA_TRY(cudaMemcpyAsync(s->d_params, p, sizeof(Params) * (size_t)n, cudaMemcpyHostToDevice, s->stream));
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
   s->params_stride = (n == 1) ? 0 : 1;
+  if (n == 1) std::memcpy(&s->h_params, p, sizeof(Params));
   return RDCNN_OK;
 }
 
@@ -515,6 +574,8 @@ int rdcnn_sim_set_tuning(rdcnn_sim_t s, int max_levels, int seg_rows) {
 int rdcnn_sim_upload(rdcnn_sim_t s, const float* u, const float* v) {
   if (!s || !u || !v) return fail(RDCNN_EINVAL, "null argument");
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  // Slab phases run on caller streams: drain them before touching the state.
+  if (s->slab) RDCNN_CUDA_TRY(cudaDeviceSynchronize());
   const size_t plane = (size_t)s->rows * s->cols;
   if (!s->slab) {
     RDCNN_CUDA_TRY(cudaMemcpyAsync(s->u_ptr(s->cur), u, plane * s->batch * sizeof(float), cudaMemcpyHostToDevice, s->stream));
@@ -532,6 +593,7 @@ int rdcnn_sim_upload(rdcnn_sim_t s, const float* u, const float* v) {
 int rdcnn_sim_download(rdcnn_sim_t s, float* u, float* v) {
   if (!s || !u || !v) return fail(RDCNN_EINVAL, "null argument");
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  if (s->slab) RDCNN_CUDA_TRY(cudaDeviceSynchronize());
   const size_t plane = (size_t)s->rows * s->cols;
   if (!s->slab) {
     RDCNN_CUDA_TRY(cudaMemcpyAsync(u, s->u_ptr(s->cur), plane * s->batch * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
@@ -679,7 +741,9 @@ static int slab_step(rdcnn_sim_t s, int k, void* stream, bool boundary) {
   if (k != 1 && k != 2 && k != 4 && k != 8) return fail(RDCNN_EINVAL, "k must be 1, 2, 4 or 8");
   if (k > s->ghost) return fail(RDCNN_EINVAL, "k=%d exceeds ghost depth %d", k, s->ghost);
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
-  cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+  // The stream is taken literally: 0 is the legacy default stream (what
+  // torch.cuda.current_stream() reports by default), not the handle's stream.
+  cudaStream_t st = (cudaStream_t)stream;
   StepArgs a = base_args(s, s->cur, s->cur ^ 1);
   if (boundary) ++s->slab_tag;
   a.tag = s->slab_tag;
