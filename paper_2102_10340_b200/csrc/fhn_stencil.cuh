@@ -180,13 +180,57 @@ __device__ __forceinline__ int wrap_index(int x, int n) {
   return r < 0 ? r + n : r;
 }
 
-// Ring depth of the level-0 rows: R0 slots give an (R0-2)-tick prefetch.
-// Measured on B200: 3 slots (1 tick) leave the first use of each row stalled
-// on its load (long-scoreboard); 6 slots (4 ticks) hide it at every depth.
-template <int K>
-struct RingDepth {
-  static constexpr int value = 6;
-};
+// Level-0 rows are staged through a per-warp shared-memory ring with
+// cp.async (LDGSTS, L1-bypassing): kStage slots, prefetch distance
+// kStage - 3 ticks.  Each lane copies and later reads back only its own W
+// columns of each plane, so no cross-lane synchronisation is needed beyond
+// the lane's own cp.async.wait_group.
+constexpr int kStage = 8;
+constexpr int kPrefetch = kStage - 3;
+
+template <int W>
+__device__ __forceinline__ void stage_row(uint32_t dst, const float* __restrict__ u,
+                                          const float* __restrict__ v, size_t off) {
+  constexpr int B = 4 * W;  // bytes per lane per plane
+  if constexpr (W == 4) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(u + off) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 32 * B), "l"(v + off) : "memory");
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst + 4 * k), "l"(u + off + k) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst + 32 * B + 4 * k), "l"(v + off + k) : "memory");
+    }
+  }
+}
+
+__device__ __forceinline__ void stage_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int W>
+__device__ __forceinline__ void read_staged(uint32_t src, Row<W>& r) {
+  constexpr int B = 4 * W;
+  if constexpr (W == 4) {
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=f"(r.u[0]), "=f"(r.u[1]), "=f"(r.u[2]), "=f"(r.u[3]) : "r"(src) : "memory");
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]) : "r"(src + 32 * B) : "memory");
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(r.u[k]) : "r"(src + 4 * k) : "memory");
+      asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(r.v[k]) : "r"(src + 32 * B + 4 * k) : "memory");
+    }
+  }
+}
+
+// Shared memory per CTA of the wavefront kernel.
+template <int W>
+constexpr int wavefront_smem_bytes(int warps) {
+  return warps * kStage * 2 * 32 * 4 * W;
+}
 
 // Running row index on the torus (periodic) or in the ghosted slab buffer.
 struct RowCursor {
@@ -201,22 +245,21 @@ struct RowCursor {
 // tick j the warp has level-0 rows x_0..x_j (x_j = r0 - K + j) and
 //   level t computes row x_j - (2t - 1) from the three level-(t-1) rows
 //   produced at ticks j-3, j-2, j-1 (level 1: the level-0 rows of ticks
-//   j-2, j-1, j).
+//   j-2, j-1, j, read back from the staging ring).
 // Visiting t = K..1 means no level consumes a row produced in the same tick,
 // so the K level updates of one tick are independent instruction streams the
-// scheduler can interleave (ILP x K), and each level's oldest row slot can be
+// scheduler can interleave, and each level's oldest row slot can be
 // overwritten in place once the level above has read it.
 //
-// Register rotation: level-0 rows live in a ring of R0 slots (tick j -> slot
-// j % R0); level-t rows in rings of 3 (tick j -> slot j % 3).  The tick loop
-// is unrolled by R0 (a multiple of 3) so every slot index is a compile-time
-// constant and no register is copied to advance a window.
+// Register rotation: level-t rows (t = 1..K-1) live in rings of 3 (tick j ->
+// slot j % 3); the tick loop is unrolled by 3 so every slot index is a
+// compile-time constant and no register is copied to advance a window.
 template <int K, int W, bool kFast, bool kPerGrid>
 __global__ void __launch_bounds__(128) fhn_wavefront_kernel(const StepArgs a) {
-  constexpr int R0 = RingDepth<K>::value;
-  constexpr int D = R0 - 2;  // prefetch distance in ticks
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
-  const long long warp_id = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int wib = threadIdx.x >> 5;
+  const long long warp_id = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
   const long long per_grid = (long long)a.n_segs * a.n_bands;
   if (warp_id >= per_grid * a.batch) return;
   const int g = int(warp_id / per_grid);
@@ -225,13 +268,12 @@ __global__ void __launch_bounds__(128) fhn_wavefront_kernel(const StepArgs a) {
   const int seg = rem / a.n_bands;
 
   // A grid that already blew up in an earlier launch of this advance stays
-  // frozen, so the input of its first bad launch survives for the replay.
-  // (Read here, tested after the first loads are in flight.)
+  // frozen (no stores), so the input of its first bad launch survives for
+  // the host-side replay.  The flag is only needed at the first store.
   const unsigned frozen = a.flags != nullptr ? *(volatile unsigned*)(a.flags + g) : 0u;
 
-  // Shared gene: read straight from the kernel-parameter bank, so ptxas never
-  // has to hold (or re-load) it in registers.  Per-grid genes (sweeps) come
-  // from global memory once per warp.
+  // Shared gene: read straight from the kernel-parameter bank.  Per-grid
+  // genes (sweeps) come from global memory once per warp.
   const Params p = kPerGrid ? a.params[g] : a.shared;
   const float neg_eps = -p.eps;  // reference model.hpp:45 negates eps first
 
@@ -240,7 +282,7 @@ __global__ void __launch_bounds__(128) fhn_wavefront_kernel(const StepArgs a) {
   const int grp = wrap_index(gl, G);
   // Store the band's useful lanes; gl >= G only when a band overhangs a grid
   // narrower than itself (the wrapped duplicates are not stored twice).
-  const bool store =
+  const bool owner =
       lane >= a.halo_groups && lane < a.halo_groups + a.band_groups && gl < G;
   const int lane_l = (lane + 31) & 31;
   const int lane_r = (lane + 1) & 31;
@@ -261,37 +303,42 @@ __global__ void __launch_bounds__(128) fhn_wavefront_kernel(const StepArgs a) {
                 a.periodic ? a.rows : 0x7FFFFFFF};
   size_t out_off = (size_t)(a.periodic ? r0 : r0 + a.ghost) * pitch;
 
-  Row<W> ring0[R0];
-  Row<W> win[K > 1 ? K - 1 : 1][3];
-  unsigned mx = 0u;
+  constexpr uint32_t kSlot = 2 * 32 * 4 * W;  // bytes of one staged row (u,v)
+  const uint32_t ring =
+      (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)wib * (kStage * kSlot) + lane * 4 * W;
 
-  // Prime the ring with the rows of ticks 0 .. D-1.
+  // Prime the staging ring with the rows of ticks 0 .. kPrefetch-1.
 #pragma unroll
-  for (int d = 0; d < D; ++d) {
+  for (int d = 0; d < kPrefetch; ++d) {
     if (d < n_load) {
-      load_row<W>(uin, vin, (size_t)cur.r * pitch, ring0[d]);
+      stage_row<W>(ring + d * kSlot, uin, vin, (size_t)cur.r * pitch);
       cur.next();
     }
+    stage_commit();
   }
 
-  if (frozen != 0u) return;
+  Row<W> win[K > 1 ? K - 1 : 1][3];
+  unsigned mx = 0u;
+  int slot_now = 0;          // staging slot of tick j
+  int slot_pre = kPrefetch;  // staging slot of tick j + kPrefetch
 
-  for (int j0 = 0; j0 < nt; j0 += R0) {
+  for (int j0 = 0; j0 < nt; j0 += 3) {
 #pragma unroll
-    for (int ph = 0; ph < R0; ++ph) {
+    for (int ph = 0; ph < 3; ++ph) {
       const int j = j0 + ph;
       if (j < nt) {
+        const bool store = owner && frozen == 0u;
         // Levels K..2, top-down: level t reads the level-(t-1) rows of ticks
-        // j-3, j-2, j-1 (slots ph, ph+1, ph+2 mod 3) and then level t-1
+        // j-3, j-2, j-1 (slots ph, ph+1, ph+2 mod 3), then level t-1
         // overwrites slot ph with its tick-j row.
 #pragma unroll
         for (int t = K; t >= 2; --t) {
           if (j >= 3 * t - 1 && j < h + 2 * K + t - 1) {
-            const Row<W>& up = win[t - 2][ph % 3];
+            const Row<W>& up = win[t - 2][ph];
             const Row<W>& ce = win[t - 2][(ph + 1) % 3];
             const Row<W>& dn = win[t - 2][(ph + 2) % 3];
             if (t < K) {
-              level_row<W, kFast>(up, ce, dn, win[t - 1][ph % 3], p, neg_eps, lane_l, lane_r);
+              level_row<W, kFast>(up, ce, dn, win[t - 1][ph], p, neg_eps, lane_l, lane_r);
             } else {
               Row<W> o;
               level_row<W, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
@@ -307,11 +354,23 @@ __global__ void __launch_bounds__(128) fhn_wavefront_kernel(const StepArgs a) {
             }
           }
         }
+        // Stage the row of tick j + kPrefetch (an empty group past the end
+        // keeps the wait_group accounting uniform).
+        if (j + kPrefetch < n_load) {
+          stage_row<W>(ring + slot_pre * kSlot, uin, vin, (size_t)cur.r * pitch);
+          cur.next();
+        }
+        stage_commit();
+        slot_pre = (slot_pre + 1 == kStage) ? 0 : slot_pre + 1;
         // Level 1 from the level-0 rows of ticks j-2, j-1, j.
         if (j >= 2 && j < n_load) {
-          const Row<W>& up = ring0[(ph + R0 - 2) % R0];
-          const Row<W>& ce = ring0[(ph + R0 - 1) % R0];
-          const Row<W>& dn = ring0[ph % R0];
+          stage_wait<kPrefetch>();  // the row of tick j has landed
+          Row<W> up, ce, dn;
+          const int s2 = slot_now >= 2 ? slot_now - 2 : slot_now + kStage - 2;
+          const int s1 = slot_now >= 1 ? slot_now - 1 : slot_now + kStage - 1;
+          read_staged<W>(ring + s2 * kSlot, up);
+          read_staged<W>(ring + s1 * kSlot, ce);
+          read_staged<W>(ring + slot_now * kSlot, dn);
           if constexpr (K == 1) {
             Row<W> o;
             level_row<W, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
@@ -325,18 +384,14 @@ __global__ void __launch_bounds__(128) fhn_wavefront_kernel(const StepArgs a) {
             }
             out_off += pitch;
           } else {
-            level_row<W, kFast>(up, ce, dn, win[0][ph % 3], p, neg_eps, lane_l, lane_r);
+            level_row<W, kFast>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
           }
         }
-        // Refill the slot of tick j-2, just consumed by level 1, with the row
-        // of tick j+D (D ticks of latency hiding).
-        if (j + D < n_load) {
-          load_row<W>(uin, vin, (size_t)cur.r * pitch, ring0[(ph + D) % R0]);
-          cur.next();
-        }
+        slot_now = (slot_now + 1 == kStage) ? 0 : slot_now + 1;
       }
     }
   }
+  stage_wait<0>();
 
   mx = __reduce_max_sync(kFull, mx);
   if (lane == 0 && mx >= 0x7F800000u && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);

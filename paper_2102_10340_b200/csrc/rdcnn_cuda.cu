@@ -90,6 +90,12 @@ KernelTable& table() {
 
 int k_index(int k) { return k == 1 ? 0 : k == 2 ? 1 : k == 4 ? 2 : 3; }
 
+// Dynamic shared memory of one CTA (the level-0 staging rings).
+size_t smem_for(int w) {
+  return w == 4 ? rdcnn_dev::wavefront_smem_bytes<4>(kThreads / 32)
+                : rdcnn_dev::wavefront_smem_bytes<1>(kThreads / 32);
+}
+
 // Resident CTAs per SM of one instance (cached; occupancy is immutable).
 int resident_blocks(int k, int w, bool fast, bool per_grid) {
   KernelTable& t = table();
@@ -97,7 +103,7 @@ int resident_blocks(int k, int w, bool fast, bool per_grid) {
   if (r == 0) {
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, t.fn[w == 4][k_index(k)][fast][per_grid],
-                                                      kThreads, 0) != cudaSuccess || n < 1)
+                                                      kThreads, smem_for(w)) != cudaSuccess || n < 1)
       n = 1;
     r = n;
   }
@@ -110,7 +116,7 @@ cudaError_t launch_stencil(int k, int w, bool fast, bool per_grid, const StepArg
   if (k != 1 && k != 2 && k != 4 && k != 8) return cudaErrorInvalidValue;
   const long long blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
   KernelFn fn = table().fn[w == 4][k_index(k)][fast][per_grid];
-  fn<<<dim3((unsigned)blocks), dim3(kThreads), 0, s>>>(a);
+  fn<<<dim3((unsigned)blocks), dim3(kThreads), smem_for(w), s>>>(a);
   return cudaGetLastError();
 }
 
