@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--size", type=int, default=4096)
     ap.add_argument("--iters-per-step", type=int, default=10000)
-    ap.add_argument("--levels", type=int, default=8, choices=(1, 2, 4, 8))
+    ap.add_argument("--levels", type=int, default=4, choices=(1, 2, 4, 8))
     ap.add_argument("--seg-rows", type=int, default=0)
     ap.add_argument("--mode", default="strict", choices=("strict", "fast"))
     ap.add_argument("--e2e-steps", type=int, default=3)

@@ -232,6 +232,15 @@ constexpr int wavefront_smem_bytes(int warps) {
   return warps * kStage * 2 * 32 * 4 * W;
 }
 
+template <int V>
+struct Int {
+  static constexpr int value = V;
+};
+template <bool V>
+struct Bool {
+  static constexpr bool value = V;
+};
+
 // Running row index on the torus (periodic) or in the ghosted slab buffer.
 struct RowCursor {
   int r;       // current buffer row
@@ -254,8 +263,15 @@ struct RowCursor {
 // Register rotation: level-t rows (t = 1..K-1) live in rings of 3 (tick j ->
 // slot j % 3); the tick loop is unrolled by 3 so every slot index is a
 // compile-time constant and no register is copied to advance a window.
+// Resident CTAs per SM the register budget is capped for (128 threads each):
+// 4 CTAs = 16 warps (<= 128 registers) for K <= 4; K = 8 needs ~220.
+template <int K>
+struct MinBlocks {
+  static constexpr int value = K <= 4 ? 4 : 2;
+};
+
 template <int K, int W, bool kFast, bool kPerGrid>
-__global__ void __launch_bounds__(128) fhn_wavefront_kernel(const StepArgs a) {
+__global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel(const StepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -321,74 +337,94 @@ __global__ void __launch_bounds__(128) fhn_wavefront_kernel(const StepArgs a) {
   unsigned mx = 0u;
   int slot_now = 0;          // staging slot of tick j
   int slot_pre = kPrefetch;  // staging slot of tick j + kPrefetch
+  const bool store = owner && frozen == 0u;
 
-  for (int j0 = 0; j0 < nt; j0 += 3) {
+  // One tick.  PH = j % 3 (compile-time ring slot); kSteady = every level is
+  // active in this tick, so the validity tests (and the divergence guards
+  // ptxas puts around shuffles under a branch) disappear.
+  auto tick = [&](auto ph_c, auto steady_c, int j) {
+    constexpr int ph = decltype(ph_c)::value;
+    constexpr bool kSteady = decltype(steady_c)::value;
+    // Levels K..2, top-down: level t reads the level-(t-1) rows of ticks
+    // j-3, j-2, j-1 (slots ph, ph+1, ph+2 mod 3), then level t-1 overwrites
+    // slot ph with its tick-j row.
 #pragma unroll
-    for (int ph = 0; ph < 3; ++ph) {
-      const int j = j0 + ph;
-      if (j < nt) {
-        const bool store = owner && frozen == 0u;
-        // Levels K..2, top-down: level t reads the level-(t-1) rows of ticks
-        // j-3, j-2, j-1 (slots ph, ph+1, ph+2 mod 3), then level t-1
-        // overwrites slot ph with its tick-j row.
+    for (int t = K; t >= 2; --t) {
+      if (kSteady || (j >= 3 * t - 1 && j < h + 2 * K + t - 1)) {
+        const Row<W>& up = win[t - 2][ph];
+        const Row<W>& ce = win[t - 2][(ph + 1) % 3];
+        const Row<W>& dn = win[t - 2][(ph + 2) % 3];
+        if (t < K) {
+          level_row<W, kFast>(up, ce, dn, win[t - 1][ph], p, neg_eps, lane_l, lane_r);
+        } else {
+          Row<W> o;
+          level_row<W, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
+          if (store) {
+            store_row<W>(uout, vout, out_off, o);
 #pragma unroll
-        for (int t = K; t >= 2; --t) {
-          if (j >= 3 * t - 1 && j < h + 2 * K + t - 1) {
-            const Row<W>& up = win[t - 2][ph];
-            const Row<W>& ce = win[t - 2][(ph + 1) % 3];
-            const Row<W>& dn = win[t - 2][(ph + 2) % 3];
-            if (t < K) {
-              level_row<W, kFast>(up, ce, dn, win[t - 1][ph], p, neg_eps, lane_l, lane_r);
-            } else {
-              Row<W> o;
-              level_row<W, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
-              if (store) {
-                store_row<W>(uout, vout, out_off, o);
-#pragma unroll
-                for (int k = 0; k < W; ++k) {
-                  mx = max(mx, __float_as_uint(o.u[k]) & 0x7FFFFFFFu);
-                  mx = max(mx, __float_as_uint(o.v[k]) & 0x7FFFFFFFu);
-                }
-              }
-              out_off += pitch;
+            for (int k = 0; k < W; ++k) {
+              mx = max(mx, __float_as_uint(o.u[k]) & 0x7FFFFFFFu);
+              mx = max(mx, __float_as_uint(o.v[k]) & 0x7FFFFFFFu);
             }
           }
+          out_off += pitch;
         }
-        // Stage the row of tick j + kPrefetch (an empty group past the end
-        // keeps the wait_group accounting uniform).
-        if (j + kPrefetch < n_load) {
-          stage_row<W>(ring + slot_pre * kSlot, uin, vin, (size_t)cur.r * pitch);
-          cur.next();
-        }
-        stage_commit();
-        slot_pre = (slot_pre + 1 == kStage) ? 0 : slot_pre + 1;
-        // Level 1 from the level-0 rows of ticks j-2, j-1, j.
-        if (j >= 2 && j < n_load) {
-          stage_wait<kPrefetch>();  // the row of tick j has landed
-          Row<W> up, ce, dn;
-          const int s2 = slot_now >= 2 ? slot_now - 2 : slot_now + kStage - 2;
-          const int s1 = slot_now >= 1 ? slot_now - 1 : slot_now + kStage - 1;
-          read_staged<W>(ring + s2 * kSlot, up);
-          read_staged<W>(ring + s1 * kSlot, ce);
-          read_staged<W>(ring + slot_now * kSlot, dn);
-          if constexpr (K == 1) {
-            Row<W> o;
-            level_row<W, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
-            if (store) {
-              store_row<W>(uout, vout, out_off, o);
-#pragma unroll
-              for (int k = 0; k < W; ++k) {
-                mx = max(mx, __float_as_uint(o.u[k]) & 0x7FFFFFFFu);
-                mx = max(mx, __float_as_uint(o.v[k]) & 0x7FFFFFFFu);
-              }
-            }
-            out_off += pitch;
-          } else {
-            level_row<W, kFast>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
-          }
-        }
-        slot_now = (slot_now + 1 == kStage) ? 0 : slot_now + 1;
       }
+    }
+    // Stage the row of tick j + kPrefetch (an empty group past the end keeps
+    // the wait_group accounting uniform).
+    if (j + kPrefetch < n_load) {
+      stage_row<W>(ring + slot_pre * kSlot, uin, vin, (size_t)cur.r * pitch);
+      cur.next();
+    }
+    stage_commit();
+    slot_pre = (slot_pre + 1 == kStage) ? 0 : slot_pre + 1;
+    // Level 1 from the level-0 rows of ticks j-2, j-1, j.
+    if (kSteady || (j >= 2 && j < n_load)) {
+      stage_wait<kPrefetch>();  // the row of tick j has landed
+      Row<W> up, ce, dn;
+      const int s2 = slot_now >= 2 ? slot_now - 2 : slot_now + kStage - 2;
+      const int s1 = slot_now >= 1 ? slot_now - 1 : slot_now + kStage - 1;
+      read_staged<W>(ring + s2 * kSlot, up);
+      read_staged<W>(ring + s1 * kSlot, ce);
+      read_staged<W>(ring + slot_now * kSlot, dn);
+      if constexpr (K == 1) {
+        Row<W> o;
+        level_row<W, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
+        if (store) {
+          store_row<W>(uout, vout, out_off, o);
+#pragma unroll
+          for (int k = 0; k < W; ++k) {
+            mx = max(mx, __float_as_uint(o.u[k]) & 0x7FFFFFFFu);
+            mx = max(mx, __float_as_uint(o.v[k]) & 0x7FFFFFFFu);
+          }
+        }
+        out_off += pitch;
+      } else {
+        level_row<W, kFast>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
+      }
+    }
+    slot_now = (slot_now + 1 == kStage) ? 0 : slot_now + 1;
+  };
+
+  using I0 = Int<0>;
+  using I1 = Int<1>;
+  using I2 = Int<2>;
+  // Steady ticks: every level active, j in [3K-1, n_load).
+  const int steady_lo = 3 * K - 1, steady_hi = n_load;
+  // Only the deepest instance gets a separate steady-state copy of the loop
+  // body: for K <= 4 the doubled code costs more in instruction-cache misses
+  // than the removed tests save (measured, profiles/README.md).
+  constexpr bool kSplit = K >= 8;
+  for (int j0 = 0; j0 < nt; j0 += 3) {
+    if (kSplit && j0 >= steady_lo && j0 + 3 <= steady_hi) {
+      tick(I0{}, Bool<true>{}, j0);
+      tick(I1{}, Bool<true>{}, j0 + 1);
+      tick(I2{}, Bool<true>{}, j0 + 2);
+    } else {
+      tick(I0{}, Bool<false>{}, j0);
+      if (j0 + 1 < nt) tick(I1{}, Bool<false>{}, j0 + 1);
+      if (j0 + 2 < nt) tick(I2{}, Bool<false>{}, j0 + 2);
     }
   }
   stage_wait<0>();
