@@ -1,0 +1,703 @@
+// cuda_api.hpp -- source-compatible C++ API of the reference's time-stepping
+// path (proj/include/rdcnn/*.hpp), implemented over the C-ABI in
+// include/rdcnn_cuda.h.  Host code written against the reference keeps its
+// types and calls (Gene, GridState, StepBuffers, step, run, run_timed,
+// init_*, checksum, make_backend) and selects the B200 kernels with
+// make_backend("cuda").  Link with -lrdcnn_cuda.
+//
+// Reference interface -> here:
+//   gene.hpp:13-85        Gene, gene_valid, gene_to_vector, vector_to_gene,
+//                         gene_field, stability_advisory
+//   grid.hpp:13-126       Precision, GridState, finite check, cyclic_shift,
+//                         fnv1a, checksum, checksum_hex
+//   rng.hpp:11-39         SeededRng
+//   model.hpp:13-86       CellModel, FhnParams, make_params, reaction_u/v,
+//                         cell_update, FhnModel (host scalar utilities)
+//   backend.hpp:12-50     BackendKind (+Cuda), Backend, make_backend
+//   kernels.hpp:22-259    StepBuffers, step
+//   config.hpp:20-95      InitMode, RunConfig, validate_config
+//   init.hpp:20-82        init_full_random, init_center_square,
+//                         init_from_image, initial_state (no file I/O)
+//   engine.hpp:15-106     ScheduleError, BlowUpError, SnapshotBuffer,
+//                         RunOutput, run, run_timed
+//   bench.hpp:21-33       Throughput, throughput
+//
+// Behavioural contract: identical to the reference for the cuda backend
+// (bit-exact states in strict mode; BlowUpError at the same iteration;
+// step() swaps and returns false on a non-finite result).  The reference's
+// CPU backends are not re-implemented: selecting one throws
+// std::invalid_argument (there is no silent fallback).  The CUDA kernels are
+// fp32 FitzHugh-Nagumo; other CellModels or T=double throw.
+#pragma once
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <concepts>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include "rdcnn_cuda.h"
+
+namespace rdcnn {
+
+// ===========================================================================
+// Parameters
+// ===========================================================================
+
+struct Gene {
+  double a = -0.3;
+  double b = 1.3;
+  double eps = -0.1;
+  double c = 1.0;
+  double Du = 0.06;
+  double Dv = 1.0;
+  double dt = 0.1;
+  double ka = 1.0;  // image-input scaling, init only
+  bool operator==(const Gene&) const = default;
+};
+
+inline bool gene_finite(const Gene& g) {
+  for (double x : {g.a, g.b, g.eps, g.c, g.Du, g.Dv, g.dt, g.ka})
+    if (!std::isfinite(x)) return false;
+  return true;
+}
+
+inline bool gene_valid(const Gene& g) {
+  return gene_finite(g) && g.dt >= 0.0 && g.Du >= 0.0 && g.Dv >= 0.0;
+}
+
+// Kernel order {dt, a, b, eps, c, Du, Dv}; ka excluded.
+inline std::array<double, 7> gene_to_vector(const Gene& g) {
+  return {g.dt, g.a, g.b, g.eps, g.c, g.Du, g.Dv};
+}
+
+inline Gene vector_to_gene(const std::array<double, 7>& p, double ka = 1.0) {
+  return Gene{p[1], p[2], p[3], p[4], p[5], p[6], p[0], ka};
+}
+
+inline bool stability_advisory(const Gene& g) { return g.dt * std::fmax(g.Du, g.Dv) > 0.25; }
+
+inline double& gene_field(Gene& g, const std::string& name) {
+  static const std::pair<const char*, double Gene::*> fields[] = {
+      {"a", &Gene::a},   {"b", &Gene::b},   {"eps", &Gene::eps}, {"c", &Gene::c},
+      {"du", &Gene::Du}, {"dv", &Gene::Dv}, {"dt", &Gene::dt},   {"ka", &Gene::ka}};
+  for (const auto& [n, m] : fields)
+    if (name == n) return g.*m;
+  throw std::invalid_argument("unknown gene field: " + name);
+}
+
+inline double gene_field(const Gene& g, const std::string& name) {
+  return gene_field(const_cast<Gene&>(g), name);
+}
+
+inline bool is_gene_field(const std::string& name) {
+  Gene g;
+  try {
+    (void)gene_field(g, name);
+    return true;
+  } catch (const std::invalid_argument&) {
+    return false;
+  }
+}
+
+// ===========================================================================
+// Lattice state and digest
+// ===========================================================================
+
+enum class Precision { Single, Double };
+
+inline const char* precision_name(Precision p) { return p == Precision::Single ? "single" : "double"; }
+
+inline Precision parse_precision(const std::string& s) {
+  if (s == "single") return Precision::Single;
+  if (s == "double") return Precision::Double;
+  throw std::invalid_argument("unknown precision: " + s);
+}
+
+template <class T>
+constexpr Precision precision_of() {
+  return sizeof(T) == 4 ? Precision::Single : Precision::Double;
+}
+
+template <class T>
+struct GridState {
+  static_assert(std::is_floating_point_v<T>);
+  int rows = 0;
+  int cols = 0;
+  std::vector<T> u;
+  std::vector<T> v;
+
+  GridState() = default;
+  GridState(int nn, int nm) : rows(nn), cols(nm) {
+    if (nn < 3 || nm < 3) throw std::invalid_argument("grid must be at least 3x3");
+    u.assign(size_t(nn) * nm, T(0));
+    v.assign(size_t(nn) * nm, T(0));
+  }
+  size_t cells() const { return size_t(rows) * cols; }
+  T& at_u(int i, int j) { return u[size_t(i) * cols + j]; }
+  T at_u(int i, int j) const { return u[size_t(i) * cols + j]; }
+  T& at_v(int i, int j) { return v[size_t(i) * cols + j]; }
+  T at_v(int i, int j) const { return v[size_t(i) * cols + j]; }
+  bool operator==(const GridState&) const = default;
+};
+
+namespace detail {
+template <class T>
+inline bool finite_bits(T x) {
+  if constexpr (sizeof(T) == 4) {
+    uint32_t b;
+    std::memcpy(&b, &x, 4);
+    return (b & 0x7F800000u) != 0x7F800000u;
+  } else {
+    uint64_t b;
+    std::memcpy(&b, &x, 8);
+    return (b & 0x7FF0000000000000ull) != 0x7FF0000000000000ull;
+  }
+}
+}  // namespace detail
+
+template <class T>
+bool all_finite(std::span<const T> xs) {
+  return std::all_of(xs.begin(), xs.end(), [](T x) { return detail::finite_bits(x); });
+}
+
+template <class T>
+bool all_finite(const GridState<T>& s) {
+  return all_finite(std::span<const T>(s.u)) && all_finite(std::span<const T>(s.v));
+}
+
+template <class T>
+GridState<T> cyclic_shift(const GridState<T>& s, int di, int dj) {
+  GridState<T> out(s.rows, s.cols);
+  for (int i = 0; i < s.rows; ++i) {
+    const int si = ((i - di) % s.rows + s.rows) % s.rows;
+    for (int j = 0; j < s.cols; ++j) {
+      const int sj = ((j - dj) % s.cols + s.cols) % s.cols;
+      out.at_u(i, j) = s.at_u(si, sj);
+      out.at_v(i, j) = s.at_v(si, sj);
+    }
+  }
+  return out;
+}
+
+inline uint64_t fnv1a(const void* data, size_t n, uint64_t h = 0xcbf29ce484222325ull) {
+  const auto* p = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < n; ++i) h = (h ^ p[i]) * 0x100000001b3ull;
+  return h;
+}
+
+template <class T>
+uint64_t checksum(const GridState<T>& s) {
+  return fnv1a(s.v.data(), s.v.size() * sizeof(T), fnv1a(s.u.data(), s.u.size() * sizeof(T)));
+}
+
+inline std::string checksum_hex(uint64_t x) {
+  static const char* digits = "0123456789abcdef";
+  std::string out(16, '0');
+  for (int k = 15; k >= 0; --k, x >>= 4) out[size_t(k)] = digits[x & 0xF];
+  return out;
+}
+
+// ===========================================================================
+// RNG and initial states
+// ===========================================================================
+
+class SeededRng {
+ public:
+  explicit SeededRng(uint64_t seed) : s_(seed) {}
+  uint64_t next_u64() {
+    uint64_t z = (s_ += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  double next_double() { return double(next_u64() >> 11) * 0x1.0p-53; }
+  float next_float() { return float(next_u64() >> 40) * 0x1.0p-24f; }
+  template <class T>
+  T next_unit() {
+    if constexpr (sizeof(T) == 4) return next_float();
+    else return next_double();
+  }
+
+ private:
+  uint64_t s_;
+};
+
+struct GridTooSmall : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct ImageTooSmall : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+inline constexpr int kSeedSquare = 11;
+
+template <class T>
+GridState<T> init_full_random(int nn, int nm, uint64_t seed) {
+  GridState<T> s(nn, nm);
+  SeededRng rng(seed);
+  for (T& x : s.u) x = rng.next_unit<T>();
+  for (T& x : s.v) x = rng.next_unit<T>();
+  return s;
+}
+
+template <class T>
+GridState<T> init_center_square(int nn, int nm, uint64_t seed) {
+  if (nn < kSeedSquare || nm < kSeedSquare)
+    throw GridTooSmall("typ=1 needs a grid of at least 11x11, got " + std::to_string(nn) + "x" +
+                       std::to_string(nm));
+  GridState<T> s(nn, nm);
+  SeededRng rng(seed);
+  const int i0 = (nn - kSeedSquare) / 2, j0 = (nm - kSeedSquare) / 2;
+  for (T* plane : {s.u.data(), s.v.data()})
+    for (int i = i0; i < i0 + kSeedSquare; ++i)
+      for (int j = j0; j < j0 + kSeedSquare; ++j) plane[size_t(i) * nm + j] = rng.next_unit<T>();
+  return s;
+}
+
+// A [0,1] grayscale raster (what the reference's load_grayscale returns).
+struct GrayImage {
+  int rows = 0, cols = 0;
+  std::vector<double> px;
+  double at(int i, int j) const { return px[size_t(i) * cols + j]; }
+};
+
+template <class T>
+GridState<T> init_from_image(const GrayImage& img, const Gene& gene) {
+  if (img.rows < 3 || img.cols < 3)
+    throw ImageTooSmall("image must be at least 3x3, got " + std::to_string(img.rows) + "x" +
+                        std::to_string(img.cols));
+  GridState<T> s(img.rows, img.cols);
+  const T ka = T(gene.ka);
+  for (size_t k = 0; k < img.px.size(); ++k) s.u[k] = s.v[k] = ka * T(img.px[k]);
+  return s;
+}
+
+// ===========================================================================
+// Cell model (host scalar utilities; the device kernel is FHN fp32)
+// ===========================================================================
+
+template <class M>
+concept CellModel = requires(const M m, typename M::value_type x) {
+  requires std::is_floating_point_v<typename M::value_type>;
+  { m.reaction_u(x, x) } -> std::same_as<typename M::value_type>;
+  { m.reaction_v(x, x) } -> std::same_as<typename M::value_type>;
+  { m.diffusion_u() } -> std::same_as<typename M::value_type>;
+  { m.diffusion_v() } -> std::same_as<typename M::value_type>;
+  { m.time_step() } -> std::same_as<typename M::value_type>;
+};
+
+template <class T>
+struct FhnParams {
+  T dt, a, b, eps, c, du, dv;
+};
+
+template <class T>
+FhnParams<T> make_params(const Gene& g) {
+  return {T(g.dt), T(g.a), T(g.b), T(g.eps), T(g.c), T(g.Du), T(g.Dv)};
+}
+
+template <class T>
+inline T reaction_u(T u, T v, const FhnParams<T>& p) {
+  return u * (p.c - u * u / T(3)) - v;
+}
+template <class T>
+inline T reaction_v(T u, T v, const FhnParams<T>& p) {
+  return -p.eps * (u - p.b * v + p.a);
+}
+template <class T>
+inline void cell_update(T u, T v, T lu, T lv, const FhnParams<T>& p, T& un, T& vn) {
+  un = u + p.dt * (reaction_u(u, v, p) + p.du * lu);
+  vn = v + p.dt * (reaction_v(u, v, p) + p.dv * lv);
+}
+template <class T>
+inline T reaction_u(T u, T v, const Gene& g) { return reaction_u(u, v, make_params<T>(g)); }
+template <class T>
+inline T reaction_v(T u, T v, const Gene& g) { return reaction_v(u, v, make_params<T>(g)); }
+template <class T>
+inline void cell_update(T u, T v, T lu, T lv, const Gene& g, T& un, T& vn) {
+  cell_update(u, v, lu, lv, make_params<T>(g), un, vn);
+}
+
+template <class T>
+struct FhnModel {
+  using value_type = T;
+  FhnParams<T> p;
+  explicit FhnModel(const Gene& g) : p(make_params<T>(g)) {}
+  explicit FhnModel(const FhnParams<T>& q) : p(q) {}
+  T reaction_u(T u, T v) const { return rdcnn::reaction_u(u, v, p); }
+  T reaction_v(T u, T v) const { return rdcnn::reaction_v(u, v, p); }
+  T diffusion_u() const { return p.du; }
+  T diffusion_v() const { return p.dv; }
+  T time_step() const { return p.dt; }
+};
+
+// ===========================================================================
+// Backend selection
+// ===========================================================================
+
+enum class BackendKind { Reference, Shift, Blocked, Parallel, Cuda };
+
+struct Backend {
+  BackendKind kind = BackendKind::Cuda;
+  int tile_rows = 64;
+  int tile_cols = 64;
+  int threads = 0;
+  int device = 0;                // CUDA ordinal
+  int mode = RDCNN_STRICT;       // RDCNN_STRICT (bit-exact) or RDCNN_FAST
+  int levels = 4;                // time levels fused per launch (1, 2, 4, 8)
+  bool exact_order() const { return kind != BackendKind::Shift && mode == RDCNN_STRICT; }
+};
+
+inline const char* backend_name(BackendKind k) {
+  switch (k) {
+    case BackendKind::Reference: return "reference";
+    case BackendKind::Shift: return "shift";
+    case BackendKind::Blocked: return "blocked";
+    case BackendKind::Parallel: return "parallel";
+    case BackendKind::Cuda: return "cuda";
+  }
+  return "?";
+}
+inline const char* backend_name(const Backend& b) { return backend_name(b.kind); }
+
+inline BackendKind parse_backend_kind(const std::string& s) {
+  for (BackendKind k : {BackendKind::Reference, BackendKind::Shift, BackendKind::Blocked,
+                        BackendKind::Parallel, BackendKind::Cuda})
+    if (s == backend_name(k)) return k;
+  throw std::invalid_argument("unknown backend: " + s +
+                              " (expected reference|shift|blocked|parallel|cuda)");
+}
+
+inline Backend make_backend(const std::string& name, int tile_rows = 64, int tile_cols = 64,
+                            int threads = 0) {
+  if (tile_rows < 1 || tile_cols < 1) throw std::invalid_argument("tile dimensions must be >= 1");
+  if (threads < 0) throw std::invalid_argument("thread count must be >= 0");
+  Backend b;
+  b.kind = parse_backend_kind(name);
+  b.tile_rows = tile_rows;
+  b.tile_cols = tile_cols;
+  b.threads = threads;
+  return b;
+}
+
+// ===========================================================================
+// Device handle (RAII over rdcnn_sim_t)
+// ===========================================================================
+
+struct CudaError : std::runtime_error {
+  int code;
+  CudaError(int c, const std::string& what) : std::runtime_error(what), code(c) {}
+};
+
+namespace detail {
+
+inline void require_cuda(const Backend& b) {
+  if (b.kind != BackendKind::Cuda)
+    throw std::invalid_argument(std::string("backend '") + backend_name(b) +
+                                "' is a reference CPU backend; this library provides 'cuda'");
+}
+
+inline void check(int rc, const char* what) {
+  if (rc != RDCNN_OK && rc != RDCNN_EBLOWUP)
+    throw CudaError(rc, std::string(what) + ": " + rdcnn_last_error());
+}
+
+class Sim {
+ public:
+  Sim(int rows, int cols, const Backend& b) : rows_(rows), cols_(cols) {
+    rdcnn_sim_t h = nullptr;
+    check(rdcnn_sim_create(rows, cols, 1, b.device, b.mode, &h), "rdcnn_sim_create");
+    h_.reset(h);
+    check(rdcnn_sim_set_tuning(h, b.levels, 0), "rdcnn_sim_set_tuning");
+  }
+  void set_gene(const Gene& g) {
+    const auto v = gene_to_vector(g);
+    rdcnn_params_f32 p;
+    rdcnn_params_from_gene(v.data(), &p);
+    check(rdcnn_sim_set_params(h_.get(), &p, 1), "rdcnn_sim_set_params");
+  }
+  void upload(const GridState<float>& s) {
+    check(rdcnn_sim_upload(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_upload");
+  }
+  void download(GridState<float>& s) {
+    check(rdcnn_sim_download(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_download");
+  }
+  // Returns the 1-based bad iteration within this call, or 0.
+  long advance(long steps) {
+    long bad = 0;
+    check(rdcnn_sim_advance(h_.get(), steps, &bad), "rdcnn_sim_advance");
+    return bad;
+  }
+  int rows() const { return rows_; }
+  int cols() const { return cols_; }
+
+ private:
+  struct Del {
+    void operator()(rdcnn_sim_t h) const { rdcnn_sim_destroy(h); }
+  };
+  std::unique_ptr<rdcnn_sim, Del> h_;
+  int rows_, cols_;
+};
+
+}  // namespace detail
+
+// ===========================================================================
+// StepBuffers / step
+// ===========================================================================
+
+/// Double buffer with the reference's public members.  `front` is the host
+/// view of the current state; for the cuda backend the state is also held on
+/// the device, created on the first step.
+template <class T>
+struct StepBuffers {
+  GridState<T> front;
+  GridState<T> back;
+  std::vector<T> scratch;
+  std::shared_ptr<detail::Sim> device;  // cuda backend state (lazily created)
+
+  explicit StepBuffers(GridState<T> initial) : front(std::move(initial)), back(front.rows, front.cols) {}
+  int rows() const { return front.rows; }
+  int cols() const { return front.cols; }
+  void swap() {
+    std::swap(front.u, back.u);
+    std::swap(front.v, back.v);
+  }
+};
+
+namespace detail {
+
+template <class T>
+Sim& device_for(StepBuffers<T>& bufs, const Backend& b) {
+  static_assert(std::is_same_v<T, float>, "the cuda backend computes in fp32");
+  if (!bufs.device) bufs.device = std::make_shared<Sim>(bufs.rows(), bufs.cols(), b);
+  return *bufs.device;
+}
+
+// Per-call protocol of kernels.hpp:233-259: upload front, advance `n`,
+// download into back, swap (always).  Returns the bad iteration or 0.
+template <class T>
+long advance_host(StepBuffers<T>& bufs, const Gene& g, const Backend& b, long n) {
+  require_cuda(b);
+  Sim& sim = device_for(bufs, b);
+  sim.set_gene(g);
+  sim.upload(bufs.front);
+  const long bad = sim.advance(n);
+  sim.download(bufs.back);
+  bufs.swap();
+  return bad;
+}
+
+}  // namespace detail
+
+/// One iteration on the selected backend; swaps; false on a non-finite value.
+template <class T>
+bool step(StepBuffers<T>& bufs, const Gene& gene, const Backend& backend) {
+  return detail::advance_host(bufs, gene, backend, 1) == 0;
+}
+
+/// The CellModel overload: the FHN model runs on the device; any other model
+/// is rejected (the sm_100a kernel is specialised to FHN).
+template <class M, class T = typename M::value_type>
+  requires CellModel<M>
+bool step(StepBuffers<T>& bufs, const M& model, const Backend& backend) {
+  if constexpr (std::is_same_v<M, FhnModel<T>>) {
+    const FhnParams<T>& p = model.p;
+    Gene g;
+    g.dt = p.dt; g.a = p.a; g.b = p.b; g.eps = p.eps; g.c = p.c; g.Du = p.du; g.Dv = p.dv;
+    return step(bufs, g, backend);  // float -> double -> float is exact
+  } else {
+    throw std::invalid_argument("the cuda backend implements the FitzHugh-Nagumo model only");
+  }
+}
+
+// ===========================================================================
+// Run configuration and engine
+// ===========================================================================
+
+enum class InitMode : int { CenterSquare = 1, FullRandom = 2, Image = 3 };
+
+inline InitMode parse_init_mode(int typ) {
+  if (typ < 1 || typ > 3) throw std::invalid_argument("typ must be 1, 2 or 3");
+  return InitMode(typ);
+}
+
+struct RunConfig {
+  InitMode init_mode = InitMode::CenterSquare;
+  int nn = 512;
+  int nm = 512;
+  std::optional<std::string> image_path;
+  std::optional<int> image_size;
+  long iter_max = 10000;
+  int nssp = 5;
+  uint64_t seed = 1;
+  Backend backend;
+  Precision precision = Precision::Single;
+};
+
+enum class ConfigErrorKind { InvalidSize, InvalidSchedule, MissingImage, NonFiniteGene };
+
+struct ConfigIssue {
+  ConfigErrorKind kind;
+  std::string message;
+};
+
+inline std::vector<ConfigIssue> validate_config(const RunConfig& cfg, const Gene& gene) {
+  std::vector<ConfigIssue> out;
+  const std::string shape = std::to_string(cfg.nn) + "x" + std::to_string(cfg.nm);
+  if (cfg.nn < 3 || cfg.nm < 3)
+    out.push_back({ConfigErrorKind::InvalidSize, "grid must be at least 3x3, got " + shape});
+  if (cfg.init_mode == InitMode::CenterSquare && (cfg.nn < 11 || cfg.nm < 11))
+    out.push_back({ConfigErrorKind::InvalidSize, "typ=1 needs room for the 11x11 seed square, got " + shape});
+  if (cfg.iter_max < 1)
+    out.push_back({ConfigErrorKind::InvalidSchedule, "iter_max must be >= 1, got " + std::to_string(cfg.iter_max)});
+  if (cfg.nssp < 1 || cfg.nssp > cfg.iter_max)
+    out.push_back({ConfigErrorKind::InvalidSchedule, "nssp must satisfy 1 <= nssp <= iter_max, got nssp=" +
+                                                         std::to_string(cfg.nssp) +
+                                                         " iter_max=" + std::to_string(cfg.iter_max)});
+  else if (cfg.iter_max >= 1 && cfg.iter_max % cfg.nssp != 0)
+    out.push_back({ConfigErrorKind::InvalidSchedule, "nssp (" + std::to_string(cfg.nssp) +
+                                                         ") must divide iter_max (" +
+                                                         std::to_string(cfg.iter_max) + ")"});
+  if (cfg.init_mode == InitMode::Image && !cfg.image_path)
+    out.push_back({ConfigErrorKind::MissingImage, "typ=3 requires an image path"});
+  if (!gene_finite(gene))
+    out.push_back({ConfigErrorKind::NonFiniteGene, "gene has non-finite fields"});
+  else if (!gene_valid(gene))
+    out.push_back({ConfigErrorKind::NonFiniteGene, "gene invariant violated (need dt >= 0, Du >= 0, Dv >= 0)"});
+  return out;
+}
+
+template <class T>
+GridState<T> initial_state(const RunConfig& cfg, const Gene& gene,
+                           const std::optional<GrayImage>& image = std::nullopt) {
+  switch (cfg.init_mode) {
+    case InitMode::CenterSquare: return init_center_square<T>(cfg.nn, cfg.nm, cfg.seed);
+    case InitMode::FullRandom: return init_full_random<T>(cfg.nn, cfg.nm, cfg.seed);
+    case InitMode::Image:
+      if (!image) throw std::invalid_argument("typ=3 requires an image");
+      return init_from_image<T>(*image, gene);
+  }
+  throw std::logic_error("unreachable init mode");
+}
+
+struct ScheduleError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct BlowUpError : std::runtime_error {
+  long iteration;
+  explicit BlowUpError(long iter)
+      : std::runtime_error("blow-up: non-finite state after iteration " + std::to_string(iter)),
+        iteration(iter) {}
+};
+
+template <class T>
+struct SnapshotBuffer {
+  int rows = 0, cols = 0;
+  std::vector<std::vector<T>> frames_u;
+  std::vector<std::vector<T>> frames_v;
+  std::vector<long> labels;
+  size_t frame_count() const { return labels.size(); }
+};
+
+template <class T>
+struct RunOutput {
+  GridState<T> final_state;
+  SnapshotBuffer<T> snapshots;
+  double wall_seconds = 0;
+  std::vector<double> snapshot_elapsed;
+};
+
+using SnapshotCallback = std::function<void(long, double)>;
+
+/// engine.hpp:54-94 with the state resident on the device between snapshots:
+/// one advance per snapshot interval, one download per frame.
+template <class T>
+RunOutput<T> run(const RunConfig& cfg, const Gene& gene, GridState<T> initial,
+                 const SnapshotCallback& on_snapshot = {}) {
+  if (initial.rows != cfg.nn || initial.cols != cfg.nm)
+    throw std::invalid_argument("initial state shape does not match config");
+  if (cfg.nssp < 1 || cfg.nssp > cfg.iter_max || cfg.iter_max % cfg.nssp != 0)
+    throw ScheduleError("nssp (" + std::to_string(cfg.nssp) + ") must divide iter_max (" +
+                        std::to_string(cfg.iter_max) + ")");
+  detail::require_cuda(cfg.backend);
+  static_assert(std::is_same_v<T, float>, "the cuda backend computes in fp32");
+  const long test_mod = cfg.iter_max / cfg.nssp;
+  RunOutput<T> out;
+  auto& snaps = out.snapshots;
+  snaps.rows = cfg.nn;
+  snaps.cols = cfg.nm;
+  snaps.frames_u.push_back(initial.u);
+  snaps.frames_v.push_back(initial.v);
+  snaps.labels.push_back(0);
+
+  detail::Sim sim(cfg.nn, cfg.nm, cfg.backend);
+  sim.set_gene(gene);
+  sim.upload(initial);
+  GridState<T> cur(std::move(initial));
+  const auto t0 = std::chrono::steady_clock::now();
+  for (long done = 0; done < cfg.iter_max; done += test_mod) {
+    const long bad = sim.advance(test_mod);
+    if (bad) throw BlowUpError(done + bad);
+    const double elapsed =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    sim.download(cur);
+    snaps.frames_u.push_back(cur.u);
+    snaps.frames_v.push_back(cur.v);
+    snaps.labels.push_back(done + test_mod);
+    out.snapshot_elapsed.push_back(elapsed);
+    if (on_snapshot) on_snapshot(done + test_mod, elapsed);
+  }
+  out.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  out.final_state = std::move(cur);
+  return out;
+}
+
+/// engine.hpp:98-106: bare timed loop (device-resident), BlowUpError(iter).
+/// Leaves bufs.front = the state after the last (or the first bad) iteration.
+template <class T>
+double run_timed(StepBuffers<T>& bufs, const Gene& gene, const Backend& backend, long iters) {
+  detail::require_cuda(backend);
+  detail::Sim& sim = detail::device_for(bufs, backend);
+  sim.set_gene(gene);
+  sim.upload(bufs.front);
+  const auto t0 = std::chrono::steady_clock::now();
+  const long bad = sim.advance(iters);
+  const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  sim.download(bufs.front);
+  if (bad) throw BlowUpError(bad);
+  return sec;
+}
+
+// ===========================================================================
+// Throughput metric (bench.hpp:21-33)
+// ===========================================================================
+
+struct ZeroDuration : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+struct Throughput {
+  double mcells_per_s = 0;
+  double ns_per_cell_iter = 0;
+};
+
+inline Throughput throughput(long nn, long nm, long iter_max, double seconds) {
+  if (!(seconds > 0)) throw ZeroDuration("throughput needs seconds > 0");
+  const double work = double(nn) * double(nm) * double(iter_max);
+  return {work / (seconds * 1e6), seconds * 1e9 / work};
+}
+
+}  // namespace rdcnn

@@ -1,0 +1,287 @@
+// test_api.cpp -- the reference's unit/acceptance tests for the time-stepping
+// path, re-expressed against the drop-in C++ API (include/rdcnn/*.hpp) on the
+// cuda backend.  Built by __graft_entry__.build(); run on a GPU by
+// tests/test_cpp_api_gpu.py.  Each case names the reference test it mirrors.
+// Exit code = number of failed checks.
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "rdcnn/engine.hpp"
+#include "rdcnn/init.hpp"
+
+using namespace rdcnn;
+
+namespace {
+
+int g_fail = 0;
+int g_pass = 0;
+
+#define CHECK(cond)                                                                    \
+  do {                                                                                 \
+    if (cond) {                                                                        \
+      ++g_pass;                                                                        \
+    } else {                                                                           \
+      ++g_fail;                                                                        \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);                      \
+    }                                                                                  \
+  } while (0)
+
+template <class F>
+bool throws_blowup(F&& f, long* iter) {
+  try {
+    f();
+  } catch (const BlowUpError& e) {
+    *iter = e.iteration;
+    return true;
+  }
+  return false;
+}
+
+const Backend kCuda = make_backend("cuda");
+
+RunConfig config(int n, long iters, int nssp, uint64_t seed = 42) {
+  RunConfig cfg;
+  cfg.nn = cfg.nm = n;
+  cfg.iter_max = iters;
+  cfg.nssp = nssp;
+  cfg.seed = seed;
+  cfg.backend = kCuda;
+  return cfg;
+}
+
+GridState<float> evolve(GridState<float> s, const Gene& g, int steps) {
+  StepBuffers<float> bufs(std::move(s));
+  for (int k = 0; k < steps; ++k)
+    if (!step(bufs, g, kCuda)) ++g_fail;
+  return bufs.front;
+}
+
+// acceptance 1 / test_output.txt:8
+void kat_criterion1() {
+  auto out = run(config(256, 1000, 1), Gene{}, init_center_square<float>(256, 256, 42));
+  CHECK(checksum_hex(checksum(out.final_state)) == "1026befcb693b1e5");
+}
+
+// acceptance 10 / test_output.txt:23
+void kat_criterion10() {
+  auto out = run(config(64, 200, 5), Gene{}, init_center_square<float>(64, 64, 42));
+  CHECK(checksum_hex(checksum(out.final_state)) == "ced829150965fba9");
+}
+
+// test_engine.cpp:82-108
+void blowup_iteration() {
+  Gene g;
+  g.dt = 100;
+  long it = 0;
+  CHECK(throws_blowup([&] { run(config(16, 1000, 1), g, init_center_square<float>(16, 16, 42)); }, &it));
+  CHECK(it == 4);
+  StepBuffers<float> bufs(init_center_square<float>(16, 16, 42));
+  it = 0;
+  CHECK(throws_blowup([&] { run_timed(bufs, g, kCuda, 1000); }, &it));
+  CHECK(it == 4);
+  CHECK(!all_finite(bufs.front));  // the post-blow-up state, like the reference
+  // per-call step(): the 4th call is the first to return false
+  StepBuffers<float> b2(init_center_square<float>(16, 16, 42));
+  int first_false = 0;
+  for (int k = 1; k <= 6 && !first_false; ++k)
+    if (!step(b2, g, kCuda)) first_false = k;
+  CHECK(first_false == 4);
+}
+
+// test_engine.cpp:24-50
+void snapshot_schedule() {
+  auto out = run(config(16, 200, 5), Gene{}, init_center_square<float>(16, 16, 42));
+  CHECK((out.snapshots.labels == std::vector<long>{0, 40, 80, 120, 160, 200}));
+  CHECK(out.snapshot_elapsed.size() == 5);
+  for (size_t k = 1; k < out.snapshot_elapsed.size(); ++k)
+    CHECK(out.snapshot_elapsed[k] >= out.snapshot_elapsed[k - 1]);
+  auto big = run(config(16, 10000, 5), Gene{}, init_center_square<float>(16, 16, 42));
+  CHECK((big.snapshots.labels == std::vector<long>{0, 2000, 4000, 6000, 8000, 10000}));
+
+  auto initial = init_full_random<float>(16, 16, 9);
+  auto keep = initial;
+  auto o = run(config(16, 60, 3), Gene{}, std::move(initial));
+  CHECK(o.snapshots.frames_u.front() == keep.u);
+  CHECK(o.snapshots.frames_v.front() == keep.v);
+  CHECK(o.snapshots.frames_u.back() == o.final_state.u);
+  CHECK(o.snapshots.frames_v.back() == o.final_state.v);
+}
+
+// test_engine.cpp:52-80
+void schedule_and_shape_errors() {
+  bool sched = false, shape = false;
+  try {
+    run(config(16, 100, 3), Gene{}, init_center_square<float>(16, 16, 1));
+  } catch (const ScheduleError&) {
+    sched = true;
+  }
+  try {
+    run(config(16, 10, 1), Gene{}, init_center_square<float>(32, 32, 1));
+  } catch (const std::invalid_argument&) {
+    shape = true;
+  }
+  CHECK(sched && shape);
+  auto a = run(config(24, 120, 4), Gene{}, init_center_square<float>(24, 24, 42));
+  auto b = run(config(24, 120, 4), Gene{}, init_center_square<float>(24, 24, 42));
+  CHECK(checksum(a.final_state) == checksum(b.final_state));
+  std::vector<long> seen;
+  run(config(16, 50, 5, 1), Gene{}, init_center_square<float>(16, 16, 1),
+      [&](long label, double el) {
+        seen.push_back(label);
+        CHECK(el >= 0);
+      });
+  CHECK((seen == std::vector<long>{10, 20, 30, 40, 50}));
+}
+
+// test_engine.cpp:110-137, acceptance 4
+void uniform_scalar_orbit() {
+  GridState<float> s(16, 16);
+  std::fill(s.u.begin(), s.u.end(), 0.5f);
+  std::fill(s.v.begin(), s.v.end(), 0.2f);
+  StepBuffers<float> bufs(std::move(s));
+  Gene g;
+  double su = 0.5, sv = 0.2, worst = 0;
+  bool uniform = true;
+  for (int it = 0; it < 1000; ++it) {
+    if (!step(bufs, g, kCuda)) ++g_fail;
+    const double f1 = g.c * su - su * su * su / 3.0 - sv;
+    const double f2 = -g.eps * (su - g.b * sv + g.a);
+    su += g.dt * f1;
+    sv += g.dt * f2;
+    const float gu = bufs.front.u[0], gv = bufs.front.v[0];
+    for (float x : bufs.front.u) uniform &= x == gu;
+    for (float x : bufs.front.v) uniform &= x == gv;
+    worst = std::max({worst, std::abs(gu - su) / std::max(1.0, std::abs(su)),
+                      std::abs(gv - sv) / std::max(1.0, std::abs(sv))});
+  }
+  CHECK(uniform);
+  CHECK(worst <= 1e-4);
+  std::printf("uniform orbit: worst relative error %.3g\n", worst);
+}
+
+// test_kernels.cpp:83-139
+void stencil_properties() {
+  Gene g0;
+  g0.dt = 0;
+  auto s = init_full_random<float>(16, 16, 8);
+  auto same = evolve(s, g0, 1);
+  CHECK(same == s);
+
+  GridState<float> zero(16, 16), pert(16, 16);
+  pert.at_u(8, 8) = 1.0f;
+  auto base = evolve(zero, Gene{}, 1), hit = evolve(pert, Gene{}, 1);
+  int du = 0, dv = 0;
+  for (int i = 0; i < 16; ++i)
+    for (int j = 0; j < 16; ++j) {
+      du += hit.at_u(i, j) != base.at_u(i, j);
+      dv += hit.at_v(i, j) != base.at_v(i, j);
+    }
+  CHECK(du == 5 && dv == 1);
+
+  auto b0 = init_full_random<float>(17, 19, 31);
+  auto p0 = b0;
+  p0.at_u(9, 9) += 0.25f;
+  for (int k = 1; k <= 5; ++k) {
+    auto bk = evolve(b0, Gene{}, k), pk = evolve(p0, Gene{}, k);
+    bool local = true;
+    for (int i = 0; i < 17; ++i)
+      for (int j = 0; j < 19; ++j)
+        if (std::max(std::abs(i - 9), std::abs(j - 9)) > k)
+          local &= bk.at_u(i, j) == pk.at_u(i, j) && bk.at_v(i, j) == pk.at_v(i, j);
+    CHECK(local);
+  }
+}
+
+// test_kernels.cpp:141-157 -- the per-step, run() and run_timed() paths agree
+void exact_order_paths_agree() {
+  auto s = init_full_random<float>(32, 48, 1001);
+  auto stepped = evolve(s, Gene{}, 25);
+  RunConfig cfg;
+  cfg.nn = 32;
+  cfg.nm = 48;
+  cfg.iter_max = 25;
+  cfg.nssp = 5;
+  cfg.backend = kCuda;
+  auto ran = run(cfg, Gene{}, s);
+  StepBuffers<float> bufs(s);
+  run_timed(bufs, Gene{}, kCuda, 25);
+  CHECK(checksum(stepped) == checksum(ran.final_state));
+  CHECK(checksum(stepped) == checksum(bufs.front));
+  CHECK(checksum_hex(checksum(stepped)) == "e900e1d1818ec230");  // tests/golden (reference)
+}
+
+// test_kernels.cpp:187-199, acceptance 2
+void shift_equivariance() {
+  auto s = init_full_random<float>(128, 128, 7);
+  auto direct = evolve(s, Gene{}, 0);
+  RunConfig cfg = config(128, 500, 1);
+  auto a = run(cfg, Gene{}, s).final_state;
+  auto b = run(cfg, Gene{}, cyclic_shift(s, 7, 13)).final_state;
+  CHECK(cyclic_shift(b, -7, -13) == a);
+  CHECK(checksum_hex(checksum(a)) == "b0426af20a320cb7");  // tests/golden (reference)
+}
+
+// backend.hpp:35-50 and the no-fallback rule
+void backend_selection() {
+  CHECK(make_backend("cuda").kind == BackendKind::Cuda);
+  bool unknown = false, cpu_rejected = false, bad_tile = false;
+  try {
+    make_backend("gpu");
+  } catch (const std::invalid_argument&) {
+    unknown = true;
+  }
+  try {
+    StepBuffers<float> b(init_full_random<float>(8, 8, 1));
+    step(b, Gene{}, make_backend("parallel"));
+  } catch (const std::invalid_argument&) {
+    cpu_rejected = true;
+  }
+  try {
+    make_backend("cuda", 0, 64, 0);
+  } catch (const std::invalid_argument&) {
+    bad_tile = true;
+  }
+  CHECK(unknown && cpu_rejected && bad_tile);
+  FhnModel<float> m(Gene{});
+  StepBuffers<float> b(init_center_square<float>(64, 64, 42));
+  for (int k = 0; k < 200; ++k) step(b, m, kCuda);  // CellModel overload
+  CHECK(checksum_hex(checksum(b.front)) == "ced829150965fba9");
+}
+
+// gene.hpp / test_gene_config.cpp / test_bench.cpp / acceptance 5
+void gene_and_metric() {
+  Gene g;
+  CHECK(g.a == -0.3 && g.b == 1.3 && g.eps == -0.1 && g.c == 1.0 && g.Du == 0.06 && g.Dv == 1.0 &&
+        g.dt == 0.1 && g.ka == 1.0 && gene_valid(g));
+  CHECK((gene_to_vector(Gene{}) == std::array<double, 7>{0.1, -0.3, 1.3, -0.1, 1.0, 0.06, 1.0}));
+  Gene h;
+  h.eps = 0.25;
+  h.ka = 3.5;
+  CHECK(vector_to_gene(gene_to_vector(h), h.ka) == h);
+  gene_field(h, "du") = 0.5;
+  CHECK(h.Du == 0.5 && is_gene_field("dt") && !is_gene_field("nn"));
+  auto tp = throughput(512, 512, 10000, 49.630551);
+  CHECK(std::abs(tp.mcells_per_s - 52.82) <= 0.005 && std::abs(tp.ns_per_cell_iter - 18.93) <= 0.005);
+  CHECK(std::abs(throughput(4096, 4096, 10000, 11.53).mcells_per_s / 14545.0 - 1.0) <= 1e-3);
+  CHECK(validate_config(RunConfig{}, Gene{}).empty());
+}
+
+}  // namespace
+
+int main() {
+  gene_and_metric();
+  kat_criterion1();
+  kat_criterion10();
+  blowup_iteration();
+  snapshot_schedule();
+  schedule_and_shape_errors();
+  uniform_scalar_orbit();
+  stencil_properties();
+  exact_order_paths_agree();
+  shift_equivariance();
+  backend_selection();
+  std::printf("cpp api: %d checks passed, %d failed\n", g_pass, g_fail);
+  return g_fail;
+}
