@@ -121,6 +121,21 @@ struct Row {
   float v[W];
 };
 
+// m = max(m, |a|, |b|) propagating NaN (sm_100 three-input FMNMX3.NAN with
+// |.| operand modifiers: one ALU op per two values).  The running max is
+// non-finite iff some value seen was inf or NaN (reference grid.hpp:58-67).
+__device__ __forceinline__ float max3_nan(float m, float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(m), "f"(fabsf(a)), "f"(fabsf(b)));
+  return r;
+}
+
+template <int W>
+__device__ __forceinline__ void absmax_nan(float& m, const Row<W>& r) {
+#pragma unroll
+  for (int k = 0; k < W; ++k) m = max3_nan(m, r.u[k], r.v[k]);
+}
+
 template <int W>
 __device__ __forceinline__ void load_row(const float* __restrict__ u,
                                          const float* __restrict__ v, size_t off,
@@ -243,9 +258,13 @@ struct Bool {
 
 // Running row index on the torus (periodic) or in the ghosted slab buffer.
 struct RowCursor {
-  int r;       // current buffer row
-  int wrap;    // rows (periodic) or INT_MAX (ghosted: never wraps)
-  __device__ __forceinline__ void next() { r = (r + 1 == wrap) ? 0 : r + 1; }
+  size_t off;   // element offset of the current row (row * pitch)
+  size_t step;  // pitch
+  size_t end;   // rows * pitch (periodic) or SIZE_MAX (ghosted: never wraps)
+  __device__ __forceinline__ void next() {
+    off += step;
+    if (off == end) off = 0;
+  }
 };
 
 // K levels per launch, W columns per lane.
@@ -315,8 +334,8 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel
   const int n_load = h + 2 * K;       // level-0 rows x_0 .. x_{n_load-1}
   const int nt = h + 3 * K - 1;       // ticks until level K has produced h rows
 
-  RowCursor cur{a.periodic ? wrap_index(r0 - K, a.rows) : r0 - K + a.ghost,
-                a.periodic ? a.rows : 0x7FFFFFFF};
+  RowCursor cur{(size_t)(a.periodic ? wrap_index(r0 - K, a.rows) : r0 - K + a.ghost) * pitch, pitch,
+                a.periodic ? (size_t)a.rows * pitch : ~size_t(0)};
   size_t out_off = (size_t)(a.periodic ? r0 : r0 + a.ghost) * pitch;
 
   constexpr uint32_t kSlot = 2 * 32 * 4 * W;  // bytes of one staged row (u,v)
@@ -327,16 +346,18 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel
 #pragma unroll
   for (int d = 0; d < kPrefetch; ++d) {
     if (d < n_load) {
-      stage_row<W>(ring + d * kSlot, uin, vin, (size_t)cur.r * pitch);
+      stage_row<W>(ring + d * kSlot, uin, vin, cur.off);
       cur.next();
     }
     stage_commit();
   }
 
   Row<W> win[K > 1 ? K - 1 : 1][3];
-  unsigned mx = 0u;
-  int slot_now = 0;          // staging slot of tick j
-  int slot_pre = kPrefetch;  // staging slot of tick j + kPrefetch
+  float mx = 0.0f;  // NaN-propagating max of |stored values|
+  const uint32_t ring_end = ring + kStage * kSlot;
+  uint32_t at_now = ring;                     // staging slot of tick j
+  uint32_t at_pre = ring + kPrefetch * kSlot; // staging slot of tick j + kPrefetch
+  auto prev_slot = [&](uint32_t x) { return x == ring ? ring_end - kSlot : x - kSlot; };
   const bool store = owner && frozen == 0u;
 
   // One tick.  PH = j % 3 (compile-time ring slot); kSteady = every level is
@@ -361,11 +382,7 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel
           level_row<W, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
           if (store) {
             store_row<W>(uout, vout, out_off, o);
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-              mx = max(mx, __float_as_uint(o.u[k]) & 0x7FFFFFFFu);
-              mx = max(mx, __float_as_uint(o.v[k]) & 0x7FFFFFFFu);
-            }
+            absmax_nan<W>(mx, o);
           }
           out_off += pitch;
         }
@@ -374,37 +391,32 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel
     // Stage the row of tick j + kPrefetch (an empty group past the end keeps
     // the wait_group accounting uniform).
     if (j + kPrefetch < n_load) {
-      stage_row<W>(ring + slot_pre * kSlot, uin, vin, (size_t)cur.r * pitch);
+      stage_row<W>(at_pre, uin, vin, cur.off);
       cur.next();
     }
     stage_commit();
-    slot_pre = (slot_pre + 1 == kStage) ? 0 : slot_pre + 1;
+    at_pre = (at_pre + kSlot == ring_end) ? ring : at_pre + kSlot;
     // Level 1 from the level-0 rows of ticks j-2, j-1, j.
     if (kSteady || (j >= 2 && j < n_load)) {
       stage_wait<kPrefetch>();  // the row of tick j has landed
       Row<W> up, ce, dn;
-      const int s2 = slot_now >= 2 ? slot_now - 2 : slot_now + kStage - 2;
-      const int s1 = slot_now >= 1 ? slot_now - 1 : slot_now + kStage - 1;
-      read_staged<W>(ring + s2 * kSlot, up);
-      read_staged<W>(ring + s1 * kSlot, ce);
-      read_staged<W>(ring + slot_now * kSlot, dn);
+      const uint32_t at1 = prev_slot(at_now);
+      read_staged<W>(prev_slot(at1), up);
+      read_staged<W>(at1, ce);
+      read_staged<W>(at_now, dn);
       if constexpr (K == 1) {
         Row<W> o;
         level_row<W, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
         if (store) {
           store_row<W>(uout, vout, out_off, o);
-#pragma unroll
-          for (int k = 0; k < W; ++k) {
-            mx = max(mx, __float_as_uint(o.u[k]) & 0x7FFFFFFFu);
-            mx = max(mx, __float_as_uint(o.v[k]) & 0x7FFFFFFFu);
-          }
+          absmax_nan<W>(mx, o);
         }
         out_off += pitch;
       } else {
         level_row<W, kFast>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
       }
     }
-    slot_now = (slot_now + 1 == kStage) ? 0 : slot_now + 1;
+    at_now = (at_now + kSlot == ring_end) ? ring : at_now + kSlot;
   };
 
   using I0 = Int<0>;
@@ -429,8 +441,10 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel
   }
   stage_wait<0>();
 
-  mx = __reduce_max_sync(kFull, mx);
-  if (lane == 0 && mx >= 0x7F800000u && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);
+  // mx >= 0, so its bit pattern orders like its value; NaN (0x7FFFFFFF) and
+  // +inf (0x7F800000) are the only patterns >= 0x7F800000.
+  const unsigned mb = __reduce_max_sync(kFull, __float_as_uint(mx));
+  if (lane == 0 && mb >= 0x7F800000u && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);
 }
 
 }  // namespace rdcnn_dev
