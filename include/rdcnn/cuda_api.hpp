@@ -27,7 +27,8 @@
 // step() swaps and returns false on a non-finite result).  The reference's
 // CPU backends are not re-implemented: selecting one throws
 // std::invalid_argument (there is no silent fallback).  The CUDA kernels are
-// fp32 FitzHugh-Nagumo; other CellModels or T=double throw.
+// FitzHugh-Nagumo in fp32 (strict or fast) and fp64 (strict); other
+// CellModels throw.
 #pragma once
 
 #include <algorithm>
@@ -414,25 +415,46 @@ inline void check(int rc, const char* what) {
     throw CudaError(rc, std::string(what) + ": " + rdcnn_last_error());
 }
 
+// One device lattice of element type T (fp32, or fp64 in strict mode).
+template <class T>
 class Sim {
+  static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>);
+
  public:
   Sim(int rows, int cols, const Backend& b) : rows_(rows), cols_(cols) {
     rdcnn_sim_t h = nullptr;
-    check(rdcnn_sim_create(rows, cols, 1, b.device, b.mode, &h), "rdcnn_sim_create");
+    if constexpr (sizeof(T) == 4) {
+      check(rdcnn_sim_create(rows, cols, 1, b.device, b.mode, &h), "rdcnn_sim_create");
+    } else {
+      if (b.mode != RDCNN_STRICT) throw std::invalid_argument("fp64 runs in strict mode only");
+      check(rdcnn_sim_create_f64(rows, cols, 1, b.device, &h), "rdcnn_sim_create_f64");
+    }
     h_.reset(h);
-    check(rdcnn_sim_set_tuning(h, b.levels, 0), "rdcnn_sim_set_tuning");
+    const int levels = sizeof(T) == 8 ? std::min(b.levels, 4) : b.levels;
+    check(rdcnn_sim_set_tuning(h, levels, 0), "rdcnn_sim_set_tuning");
   }
   void set_gene(const Gene& g) {
     const auto v = gene_to_vector(g);
-    rdcnn_params_f32 p;
-    rdcnn_params_from_gene(v.data(), &p);
-    check(rdcnn_sim_set_params(h_.get(), &p, 1), "rdcnn_sim_set_params");
+    if constexpr (sizeof(T) == 4) {
+      rdcnn_params_f32 p;
+      rdcnn_params_from_gene(v.data(), &p);
+      check(rdcnn_sim_set_params(h_.get(), &p, 1), "rdcnn_sim_set_params");
+    } else {
+      const rdcnn_params_f64 p{v[0], v[1], v[2], v[3], v[4], v[5], v[6]};
+      check(rdcnn_sim_set_params_f64(h_.get(), &p, 1), "rdcnn_sim_set_params_f64");
+    }
   }
-  void upload(const GridState<float>& s) {
-    check(rdcnn_sim_upload(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_upload");
+  void upload(const GridState<T>& s) {
+    if constexpr (sizeof(T) == 4)
+      check(rdcnn_sim_upload(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_upload");
+    else
+      check(rdcnn_sim_upload_f64(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_upload_f64");
   }
-  void download(GridState<float>& s) {
-    check(rdcnn_sim_download(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_download");
+  void download(GridState<T>& s) {
+    if constexpr (sizeof(T) == 4)
+      check(rdcnn_sim_download(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_download");
+    else
+      check(rdcnn_sim_download_f64(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_download_f64");
   }
   // Returns the 1-based bad iteration within this call, or 0.
   long advance(long steps) {
@@ -465,7 +487,7 @@ struct StepBuffers {
   GridState<T> front;
   GridState<T> back;
   std::vector<T> scratch;
-  std::shared_ptr<detail::Sim> device;  // cuda backend state (lazily created)
+  std::shared_ptr<detail::Sim<T>> device;  // cuda backend state (lazily created)
 
   explicit StepBuffers(GridState<T> initial) : front(std::move(initial)), back(front.rows, front.cols) {}
   int rows() const { return front.rows; }
@@ -479,9 +501,8 @@ struct StepBuffers {
 namespace detail {
 
 template <class T>
-Sim& device_for(StepBuffers<T>& bufs, const Backend& b) {
-  static_assert(std::is_same_v<T, float>, "the cuda backend computes in fp32");
-  if (!bufs.device) bufs.device = std::make_shared<Sim>(bufs.rows(), bufs.cols(), b);
+Sim<T>& device_for(StepBuffers<T>& bufs, const Backend& b) {
+  if (!bufs.device) bufs.device = std::make_shared<Sim<T>>(bufs.rows(), bufs.cols(), b);
   return *bufs.device;
 }
 
@@ -490,7 +511,7 @@ Sim& device_for(StepBuffers<T>& bufs, const Backend& b) {
 template <class T>
 long advance_host(StepBuffers<T>& bufs, const Gene& g, const Backend& b, long n) {
   require_cuda(b);
-  Sim& sim = device_for(bufs, b);
+  Sim<T>& sim = device_for(bufs, b);
   sim.set_gene(g);
   sim.upload(bufs.front);
   const long bad = sim.advance(n);
@@ -633,7 +654,6 @@ RunOutput<T> run(const RunConfig& cfg, const Gene& gene, GridState<T> initial,
     throw ScheduleError("nssp (" + std::to_string(cfg.nssp) + ") must divide iter_max (" +
                         std::to_string(cfg.iter_max) + ")");
   detail::require_cuda(cfg.backend);
-  static_assert(std::is_same_v<T, float>, "the cuda backend computes in fp32");
   const long test_mod = cfg.iter_max / cfg.nssp;
   RunOutput<T> out;
   auto& snaps = out.snapshots;
@@ -643,7 +663,7 @@ RunOutput<T> run(const RunConfig& cfg, const Gene& gene, GridState<T> initial,
   snaps.frames_v.push_back(initial.v);
   snaps.labels.push_back(0);
 
-  detail::Sim sim(cfg.nn, cfg.nm, cfg.backend);
+  detail::Sim<T> sim(cfg.nn, cfg.nm, cfg.backend);
   sim.set_gene(gene);
   sim.upload(initial);
   GridState<T> cur(std::move(initial));
@@ -670,7 +690,7 @@ RunOutput<T> run(const RunConfig& cfg, const Gene& gene, GridState<T> initial,
 template <class T>
 double run_timed(StepBuffers<T>& bufs, const Gene& gene, const Backend& backend, long iters) {
   detail::require_cuda(backend);
-  detail::Sim& sim = detail::device_for(bufs, backend);
+  detail::Sim<T>& sim = detail::device_for(bufs, backend);
   sim.set_gene(gene);
   sim.upload(bufs.front);
   const auto t0 = std::chrono::steady_clock::now();

@@ -13,7 +13,8 @@
  *   rdcnn_sim_advance        step() x n / run_timed()          kernels.hpp:233-259,
  *                                                               engine.hpp:98-106
  *   rdcnn_sim_download       bufs.front readback               engine.hpp:83-92
- *   rdcnn_checksum_f32       checksum(GridState<float>)        grid.hpp:101-116
+ *   rdcnn_checksum_f32/_f64  checksum(GridState<T>)            grid.hpp:101-116
+ *   rdcnn_sim_create_f64     StepBuffers<double>               kernels.hpp:22-38
  *   rdcnn_init_*_host        init_* on host buffers            init.hpp:20-48
  *
  * Conventions: plain pointers and sizes only; status codes mirror the CLI
@@ -55,6 +56,11 @@ typedef struct rdcnn_params_f32 {
   float dt, a, b, eps, c, du, dv;
 } rdcnn_params_f32;
 
+/* fp64 gene (make_params<double>, model.hpp:24-32: no narrowing). */
+typedef struct rdcnn_params_f64 {
+  double dt, a, b, eps, c, du, dv;
+} rdcnn_params_f64;
+
 typedef struct rdcnn_sim* rdcnn_sim_t;
 
 int rdcnn_abi_version(void);
@@ -68,15 +74,25 @@ void rdcnn_params_from_gene(const double gene7[7], rdcnn_params_f32* out);
  * shape; device = CUDA ordinal; mode = rdcnn_mode. */
 int rdcnn_sim_create(int rows, int cols, int batch, int device, int mode,
                      rdcnn_sim_t* out);
+/* fp64 lattice (GridState<double>; the reference templates instantiate both
+ * precisions, grid.hpp:13-28).  Strict mode only.  Use the *_f64 entry
+ * points for its state and genes; the fp32 ones reject it. */
+int rdcnn_sim_create_f64(int rows, int cols, int batch, int device,
+                         rdcnn_sim_t* out);
+/* 4 (fp32) or 8 (fp64). */
+int rdcnn_sim_precision(rdcnn_sim_t sim, int* bytes);
 void rdcnn_sim_destroy(rdcnn_sim_t sim);
 
 /* n = 1 (shared gene) or n = batch (one gene per grid, sweep.hpp:296-309). */
 int rdcnn_sim_set_params(rdcnn_sim_t sim, const rdcnn_params_f32* p, int n);
+int rdcnn_sim_set_params_f64(rdcnn_sim_t sim, const rdcnn_params_f64* p, int n);
 
 /* Synchronous host<->device copies of the current state (front buffer).
  * Pinned host memory gets full link bandwidth; pageable memory also works. */
 int rdcnn_sim_upload(rdcnn_sim_t sim, const float* u, const float* v);
 int rdcnn_sim_download(rdcnn_sim_t sim, float* u, float* v);
+int rdcnn_sim_upload_f64(rdcnn_sim_t sim, const double* u, const double* v);
+int rdcnn_sim_download_f64(rdcnn_sim_t sim, double* u, double* v);
 
 /* Device-side initial states, bit-identical to the reference initialisers:
  * typ 1 = init_center_square, typ 2 = init_full_random (every grid of a
@@ -104,9 +120,10 @@ int rdcnn_sim_launch_count(rdcnn_sim_t sim, long* n);
 int rdcnn_sim_set_tuning(rdcnn_sim_t sim, int max_levels, int seg_rows);
 /* The handle's CUDA stream (cudaStream_t) for interop with other libraries. */
 int rdcnn_sim_stream(rdcnn_sim_t sim, void** stream);
-/* Device pointers of the current front planes (plane u, plane v), for
- * zero-copy interop; valid until the next advance/destroy. */
-int rdcnn_sim_device_state(rdcnn_sim_t sim, float** u, float** v);
+/* Device pointers of the current front planes (plane u, plane v; float or
+ * double per rdcnn_sim_precision), for zero-copy interop; valid until the
+ * next advance/destroy. */
+int rdcnn_sim_device_state(rdcnn_sim_t sim, void** u, void** v);
 
 /* ---- slab mode: one row slab of a larger torus, for multi-GPU runs -------
  * The slab owns rows [0, rows) of its shard and `ghost` halo rows above and
@@ -144,6 +161,11 @@ int rdcnn_init_center_square_host(int rows, int cols, uint64_t seed, float* u,
 int rdcnn_init_full_random_host(int rows, int cols, uint64_t seed, float* u,
                                 float* v);
 uint64_t rdcnn_checksum_f32(const float* u, const float* v, size_t cells);
+int rdcnn_init_center_square_host_f64(int rows, int cols, uint64_t seed,
+                                      double* u, double* v);
+int rdcnn_init_full_random_host_f64(int rows, int cols, uint64_t seed, double* u,
+                                    double* v);
+uint64_t rdcnn_checksum_f64(const double* u, const double* v, size_t cells);
 
 /* ---- self-test of the device arithmetic -------------------------------------
  * Sweeps all 2^32 fp32 bit patterns x on the device and counts those where
@@ -151,6 +173,10 @@ uint64_t rdcnn_checksum_f32(const float* u, const float* v, size_t cells);
  * domain 0: every x, domain 1: x = u*u for every u.  */
 int rdcnn_selftest_div3(int device, int domain, uint64_t* mismatches,
                         uint32_t* first_bad);
+/* fp64: `samples` inputs spanning every exponent (and their squares) against
+ * IEEE division; mismatches and the smallest failing bit pattern. */
+int rdcnn_selftest_div3_f64(int device, uint64_t samples, uint64_t* mismatches,
+                            uint64_t* first_bad);
 
 #ifdef __cplusplus
 }

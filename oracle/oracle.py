@@ -100,6 +100,28 @@ class Oracle:
         v = np.ascontiguousarray(v)
         return int(self.L.orc_checksum(_p(u), _p(v), u.nbytes))
 
+    # ---- fp64 (the reference templates instantiate double as well) --------
+    def init_f64(self, typ: int, rows: int, cols: int, seed: int):
+        u = np.zeros(rows * cols, np.float64)
+        v = np.zeros(rows * cols, np.float64)
+        if typ == 1:
+            self.L.orc_init_center_square_f64.argtypes = [c_int, c_int, c_uint64, c_void_p, c_void_p]
+            if self.L.orc_init_center_square_f64(rows, cols, seed, _p(u), _p(v)) != 0:
+                raise ValueError("grid too small for typ=1")
+        else:
+            self.L.orc_init_full_random_f64.argtypes = [c_int, c_int, c_uint64, c_void_p, c_void_p]
+            self.L.orc_init_full_random_f64(rows, cols, seed, _p(u), _p(v))
+        return u, v
+
+    def run_f64(self, rows: int, cols: int, u, v, iters: int, gene7=DEFAULT_GENE7):
+        u = np.array(u, np.float64, copy=True).reshape(-1)
+        v = np.array(v, np.float64, copy=True).reshape(-1)
+        su = np.empty_like(u)
+        sv = np.empty_like(v)
+        p = np.asarray(gene7, np.float64)  # make_params<double>: no narrowing
+        bad = self.L.orc_run_f64(rows, cols, _p(u), _p(v), _p(su), _p(sv), _p(p), iters)
+        return u, v, int(bad)
+
     def div3_sweep(self, lo: int = 0, hi: int = 1 << 32):
         first = c_uint32(0)
         n = self.L.div3_sweep(lo, hi, ctypes.byref(first))
@@ -167,4 +189,35 @@ class Reference:
         return fu.reshape(nssp + 1, n), fv.reshape(nssp + 1, n), labels, rc, int(bad.value)
 
     def checksum(self, rows, cols, u, v) -> int:
+        if np.asarray(u).dtype == np.float64:
+            f = self.L.ref_checksum_f64
+            f.restype = c_uint64
+            f.argtypes = [c_int, c_int, c_void_p, c_void_p]
+            return int(f(rows, cols, _p(np.ascontiguousarray(u)), _p(np.ascontiguousarray(v))))
         return int(self.L.ref_checksum_f32(rows, cols, _p(np.ascontiguousarray(u)), _p(np.ascontiguousarray(v))))
+
+    def init_f64(self, typ: int, rows: int, cols: int, seed: int):
+        u = np.zeros(rows * cols, np.float64)
+        v = np.zeros(rows * cols, np.float64)
+        f = self.L.ref_init_f64
+        f.restype = c_int
+        f.argtypes = [c_int, c_int, c_int, c_uint64, c_void_p, c_void_p]
+        if f(typ, rows, cols, seed, _p(u), _p(v)) != 0:
+            raise ValueError("reference init rejected the shape")
+        return u, v
+
+    def run_timed_f64(self, rows, cols, u, v, iters, gene7=DEFAULT_GENE7, ka=1.0, backend="parallel",
+                      threads=0):
+        u = np.array(u, np.float64, copy=True).reshape(-1)
+        v = np.array(v, np.float64, copy=True).reshape(-1)
+        g8 = np.asarray(list(gene7) + [ka], np.float64)
+        bad = c_long(0)
+        sec = c_double(0)
+        f = self.L.ref_run_timed_f64
+        f.restype = c_int
+        f.argtypes = self.L.ref_run_timed_f32.argtypes
+        rc = f(rows, cols, _p(u), _p(v), _p(g8), backend.encode(), threads, iters, ctypes.byref(bad),
+               ctypes.byref(sec))
+        if rc == 1:
+            raise ValueError("reference rejected the arguments")
+        return u, v, int(bad.value), float(sec.value)

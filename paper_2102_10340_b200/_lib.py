@@ -29,6 +29,12 @@ class ParamsF32(ctypes.Structure):
     _fields_ = [(n, c_float) for n in ("dt", "a", "b", "eps", "c", "du", "dv")]
 
 
+class ParamsF64(ctypes.Structure):
+    """rdcnn_params_f64: the gene in fp64, kernel order."""
+
+    _fields_ = [(n, c_double) for n in ("dt", "a", "b", "eps", "c", "du", "dv")]
+
+
 # name -> (restype, argtypes); exactly the symbols include/rdcnn_cuda.h declares.
 SIGNATURES = {
     "rdcnn_abi_version": (c_int, []),
@@ -36,7 +42,16 @@ SIGNATURES = {
     "rdcnn_device_count": (c_int, [POINTER(c_int)]),
     "rdcnn_params_from_gene": (None, [POINTER(c_double), POINTER(ParamsF32)]),
     "rdcnn_sim_create": (c_int, [c_int, c_int, c_int, c_int, c_int, POINTER(c_void_p)]),
+    "rdcnn_sim_create_f64": (c_int, [c_int, c_int, c_int, c_int, POINTER(c_void_p)]),
+    "rdcnn_sim_precision": (c_int, [c_void_p, POINTER(c_int)]),
     "rdcnn_sim_destroy": (None, [c_void_p]),
+    "rdcnn_sim_set_params_f64": (c_int, [c_void_p, POINTER(ParamsF64), c_int]),
+    "rdcnn_sim_upload_f64": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "rdcnn_sim_download_f64": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "rdcnn_init_center_square_host_f64": (c_int, [c_int, c_int, c_uint64, c_void_p, c_void_p]),
+    "rdcnn_init_full_random_host_f64": (c_int, [c_int, c_int, c_uint64, c_void_p, c_void_p]),
+    "rdcnn_checksum_f64": (c_uint64, [c_void_p, c_void_p, c_size_t]),
+    "rdcnn_selftest_div3_f64": (c_int, [c_int, c_uint64, POINTER(c_uint64), POINTER(c_uint64)]),
     "rdcnn_sim_set_params": (c_int, [c_void_p, POINTER(ParamsF32), c_int]),
     "rdcnn_sim_upload": (c_int, [c_void_p, c_void_p, c_void_p]),
     "rdcnn_sim_download": (c_int, [c_void_p, c_void_p, c_void_p]),

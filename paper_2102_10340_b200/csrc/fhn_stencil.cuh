@@ -1,18 +1,20 @@
 // fhn_stencil.cuh -- sm_100a register-wavefront stencil for the coupled u/v
 // FitzHugh-Nagumo RD-CNN step (reference proj/include/rdcnn/kernels.hpp:63-72,
-// model.hpp:37-56), advancing K time levels per launch.
+// model.hpp:37-56), advancing K time levels per launch, in fp32 (default) or
+// fp64 (the reference templates instantiate both, grid.hpp:13-28).
 //
 // Mapping:
 //   * one warp owns a column BAND x row SEGMENT of one grid;
-//   * each lane owns W consecutive columns (W=4: one float4 per plane);
-//   * the warp marches down the segment; for each newly loaded level-0 row it
-//     advances every level t=1..K by one row (a skewed wavefront), keeping
-//     only two rows per level in registers;
+//   * each lane owns W consecutive columns (16 bytes per plane: W=4 fp32,
+//     W=2 fp64; W=1 when the column count is not a multiple of that);
+//   * the warp marches down the segment in a skewed wavefront, keeping three
+//     rows per level in registers and staging the level-0 rows through a
+//     per-warp shared-memory ring filled by cp.async;
 //   * left/right neighbours come from the adjacent lanes by warp shuffle;
 //     the outermost `halo_groups` lanes of a band are halo (their values go
 //     stale one column per level and are never stored);
 //   * rows wrap on the torus by index arithmetic (periodic mode) or read
-//     K ghost rows written by the halo exchange (slab mode);
+//     ghost rows written by the halo exchange (slab mode);
 //   * only level-K rows are stored; their finiteness is folded into one word
 //     per grid (atomicCAS of the launch tag).  Non-finite values are absorbing
 //     and spread one cell per level, so a non-finite value at any level of
@@ -20,10 +22,10 @@
 //     one level at a time to recover the exact iteration.
 //
 // Arithmetic: in strict mode each operation is one IEEE round-to-nearest op
-// in the reference order (__fadd_rn/__fmul_rn are never contracted), with
-// subnormals preserved (no -ftz).  x/3 uses a three-op corrected reciprocal
-// proven equal to IEEE division on the only domain it sees (x = u*u), see
-// div3_rn below and oracle/div3_check.c.
+// in the reference order (__fadd_rn/__fmul_rn/__dadd_rn/... are never
+// contracted), with subnormals preserved (no -ftz).  x/3 uses a three-op
+// corrected reciprocal proven equal to IEEE division on the only domain it
+// sees (x = u*u), see div3_rn below and oracle/div3_check.c.
 #pragma once
 
 #include <cstdint>
@@ -33,21 +35,24 @@ namespace rdcnn_dev {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
-// Gene narrowed once to fp32, kernel order {dt,a,b,eps,c,du,dv}
-// (reference model.hpp:24-32, gene.hpp:39-41).
-struct Params {
-  float dt, a, b, eps, c, du, dv;
+// Gene narrowed once to the working precision, kernel order
+// {dt,a,b,eps,c,du,dv} (reference model.hpp:24-32, gene.hpp:39-41).
+template <class T>
+struct ParamsT {
+  T dt, a, b, eps, c, du, dv;
 };
+using Params = ParamsT<float>;
 
-struct StepArgs {
-  const float* u_in;
-  const float* v_in;
-  float* u_out;
-  float* v_out;
-  long long grid_stride;  // floats between consecutive grids (same for in/out)
+template <class T>
+struct StepArgsT {
+  const T* u_in;
+  const T* v_in;
+  T* u_out;
+  T* v_out;
+  long long grid_stride;  // elements between consecutive grids (same for in/out)
   int rows;               // lattice rows (periodic) or slab rows (ghosted)
   int cols;               // lattice cols (W divides cols)
-  int pitch;              // floats between consecutive rows
+  int pitch;              // elements between consecutive rows
   int periodic;           // 1: rows wrap mod rows; 0: ghost rows present
   int ghost;              // ghosted mode: ghost rows above row 0 in the buffer
   int row_begin, row_end; // output rows computed by this launch
@@ -57,13 +62,14 @@ struct StepArgs {
   int band_groups;        // useful W-groups per band
   int halo_groups;        // halo W-groups each side (0 = full-width wrap)
   int batch;
-  Params shared;          // the gene when every grid shares one (kernel-param
+  ParamsT<T> shared;      // the gene when every grid shares one (kernel-param
                           // space: the FP ops read it as constant-bank operands)
-  const Params* params;   // per-grid genes (kPerGrid instances only)
+  const ParamsT<T>* params;  // per-grid genes (kPerGrid instances only)
   int params_stride;      // 0: one gene for all grids; 1: one per grid
   unsigned* flags;        // per grid: 0 clean, else tag of the first bad launch
   unsigned tag;           // this launch's tag (launch index + 1)
 };
+using StepArgs = StepArgsT<float>;
 
 // ---------------------------------------------------------------------------
 // Per-cell arithmetic.
@@ -71,9 +77,12 @@ struct StepArgs {
 
 // RN(x/3) for every x the kernel can present (x = RN(u*u): +0, positive,
 // +inf or NaN).  q0 = RN(x*R), e = x - 3*q0 exactly (FMA), q = RN(q0 + e*R).
-// Exhaustively verified over all 2^32 inputs (CPU: oracle/div3_check.c; GPU:
-// rdcnn_selftest_div3); the single mismatch is x = -0.0, which u*u never
-// produces.  Non-finite x yields a non-finite q, so blow-up is preserved.
+// fp32: exhaustively verified over all 2^32 inputs (CPU: oracle/div3_check.c;
+// GPU: rdcnn_selftest_div3); the single mismatch is x = -0.0, which u*u never
+// produces.  fp64: the same argument (the exact quotient's fraction of an ulp
+// is 0, 1/3 or 2/3, never within the FMA's 2^-53-ulp error of a midpoint),
+// checked on random and boundary patterns by rdcnn_selftest_div3_f64.
+// Non-finite x yields a non-finite q, so blow-up is preserved.
 __device__ __forceinline__ float div3_rn(float x) {
   const float R = __uint_as_float(0x3EAAAAABu);  // RN(1/3)
   const float q0 = __fmul_rn(x, R);
@@ -81,85 +90,109 @@ __device__ __forceinline__ float div3_rn(float x) {
   return __fmaf_rn(e, R, q0);
 }
 
+__device__ __forceinline__ double div3_rn(double x) {
+  const double R = __longlong_as_double(0x3FD5555555555555ll);  // RN(1/3)
+  const double q0 = __dmul_rn(x, R);
+  const double e = __fma_rn(-q0, 3.0, x);
+  return __fma_rn(e, R, q0);
+}
+
+// Round-to-nearest primitives that the compiler never contracts.
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
 // kern::stencil_cell (kernels.hpp:63-72) with reaction_u/v (model.hpp:37-46):
 //   lap   = right + left + down + up - 4*c          (down = row i+1)
 //   u+    = u + dt*( u*(c - u*u/3) - v + Du*lap_u )
 //   v+    = v + dt*( -eps*(u - b*v + a) + Dv*lap_v )
-template <bool kFast>
-__device__ __forceinline__ void fhn_cell(float uc, float vc, float ur, float ul,
-                                         float ud, float uu, float vr, float vl,
-                                         float vd, float vu, const Params& p,
-                                         float neg_eps, float& un, float& vn) {
+template <class T, bool kFast>
+__device__ __forceinline__ void fhn_cell(T uc, T vc, T ur, T ul, T ud, T uu, T vr, T vl, T vd,
+                                         T vu, const ParamsT<T>& p, T neg_eps, T& un, T& vn) {
   if constexpr (!kFast) {
     // RN(s - RN(4*uc)) == RN(s - 4*uc) == fma(-4, uc, s) whenever 4*uc is
-    // finite (scaling by 4 is exact).  When 4*uc overflows, |uc| > 2^125 so
-    // uc*uc overflows and u+ is non-finite in both forms: the
-    // fused form is bit-identical on every finite outcome.  The v plane has
-    // no such guard and keeps the separate multiply.
-    const float lap_u = __fmaf_rn(-4.0f, uc, __fadd_rn(__fadd_rn(__fadd_rn(ur, ul), ud), uu));
-    const float lap_v =
-        __fsub_rn(__fadd_rn(__fadd_rn(__fadd_rn(vr, vl), vd), vu), __fmul_rn(4.0f, vc));
-    const float f1 = __fsub_rn(__fmul_rn(uc, __fsub_rn(p.c, div3_rn(__fmul_rn(uc, uc)))), vc);
-    const float f2 = __fmul_rn(neg_eps, __fadd_rn(__fsub_rn(uc, __fmul_rn(p.b, vc)), p.a));
-    un = __fadd_rn(uc, __fmul_rn(p.dt, __fadd_rn(f1, __fmul_rn(p.du, lap_u))));
-    vn = __fadd_rn(vc, __fmul_rn(p.dt, __fadd_rn(f2, __fmul_rn(p.dv, lap_v))));
+    // finite (scaling by 4 is exact).  When 4*uc overflows, |uc| is so large
+    // that uc*uc overflows and u+ is non-finite in both forms:
+    // the fused form is bit-identical on every finite outcome.  The v plane
+    // has no such guard and keeps the separate multiply.
+    const T lap_u = fma_rn(T(-4), uc, add_rn(add_rn(add_rn(ur, ul), ud), uu));
+    const T lap_v = sub_rn(add_rn(add_rn(add_rn(vr, vl), vd), vu), mul_rn(T(4), vc));
+    const T f1 = sub_rn(mul_rn(uc, sub_rn(p.c, div3_rn(mul_rn(uc, uc)))), vc);
+    const T f2 = mul_rn(neg_eps, add_rn(sub_rn(uc, mul_rn(p.b, vc)), p.a));
+    un = add_rn(uc, mul_rn(p.dt, add_rn(f1, mul_rn(p.du, lap_u))));
+    vn = add_rn(vc, mul_rn(p.dt, add_rn(f2, mul_rn(p.dv, lap_v))));
   } else {
     // Opt-in fast mode: same formula, FMA-contracted and reassociated.
     // Validated statistically, never bit-exact.
-    const float lap_u = __fmaf_rn(-4.0f, uc, (ur + ul) + (ud + uu));
-    const float lap_v = __fmaf_rn(-4.0f, vc, (vr + vl) + (vd + vu));
-    const float f1 = __fmaf_rn(uc, __fmaf_rn(-uc * uc, 0.333333343f, p.c), -vc);
-    const float f2 = neg_eps * (__fmaf_rn(-p.b, vc, uc) + p.a);
-    un = __fmaf_rn(p.dt, __fmaf_rn(p.du, lap_u, f1), uc);
-    vn = __fmaf_rn(p.dt, __fmaf_rn(p.dv, lap_v, f2), vc);
+    const T lap_u = fma_rn(T(-4), uc, (ur + ul) + (ud + uu));
+    const T lap_v = fma_rn(T(-4), vc, (vr + vl) + (vd + vu));
+    const T f1 = fma_rn(uc, fma_rn(-uc * uc, T(1) / T(3), p.c), -vc);
+    const T f2 = neg_eps * (fma_rn(-p.b, vc, uc) + p.a);
+    un = fma_rn(p.dt, fma_rn(p.du, lap_u, f1), uc);
+    vn = fma_rn(p.dt, fma_rn(p.dv, lap_v, f2), vc);
   }
 }
 
-template <int W>
+template <int W, class T>
 struct Row {
-  float u[W];
-  float v[W];
+  T u[W];
+  T v[W];
 };
 
-// m = max(m, |a|, |b|) propagating NaN (sm_100 three-input FMNMX3.NAN with
-// |.| operand modifiers: one ALU op per two values).  The running max is
-// non-finite iff some value seen was inf or NaN (reference grid.hpp:58-67).
-__device__ __forceinline__ float max3_nan(float m, float a, float b) {
-  float r;
-  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(m), "f"(fabsf(a)), "f"(fabsf(b)));
-  return r;
-}
+// Running "largest |value|" that turns non-finite once any value is inf/NaN
+// (reference grid.hpp:58-67 finite_bits).  fp32: sm_100 three-input
+// FMNMX3.NAN with |.| operand modifiers, one ALU op per two values.  fp64:
+// the high words' magnitudes in an integer max.
+template <class T>
+struct Finite;
 
-template <int W>
-__device__ __forceinline__ void absmax_nan(float& m, const Row<W>& r) {
-#pragma unroll
-  for (int k = 0; k < W; ++k) m = max3_nan(m, r.u[k], r.v[k]);
-}
-
-template <int W>
-__device__ __forceinline__ void load_row(const float* __restrict__ u,
-                                         const float* __restrict__ v, size_t off,
-                                         Row<W>& r) {
-  if constexpr (W == 4) {
-    const float4 a = __ldg(reinterpret_cast<const float4*>(u + off));
-    const float4 b = __ldg(reinterpret_cast<const float4*>(v + off));
-    r.u[0] = a.x; r.u[1] = a.y; r.u[2] = a.z; r.u[3] = a.w;
-    r.v[0] = b.x; r.v[1] = b.y; r.v[2] = b.z; r.v[3] = b.w;
-  } else {
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-      r.u[k] = __ldg(u + off + k);
-      r.v[k] = __ldg(v + off + k);
-    }
+template <>
+struct Finite<float> {
+  float m = 0.0f;
+  __device__ __forceinline__ void add(float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(m), "f"(fabsf(a)), "f"(fabsf(b)));
+    m = r;
   }
+  // m >= 0, so its bit pattern orders like its value; NaN and +inf are the
+  // only patterns >= 0x7F800000.
+  __device__ __forceinline__ bool bad_in_warp() const {
+    return __reduce_max_sync(kFull, __float_as_uint(m)) >= 0x7F800000u;
+  }
+};
+
+template <>
+struct Finite<double> {
+  unsigned m = 0u;
+  __device__ __forceinline__ void add(double a, double b) {
+    m = max(m, max((unsigned)__double2hiint(a) & 0x7FFFFFFFu, (unsigned)__double2hiint(b) & 0x7FFFFFFFu));
+  }
+  __device__ __forceinline__ bool bad_in_warp() const {
+    return __reduce_max_sync(kFull, m) >= 0x7FF00000u;
+  }
+};
+
+template <int W, class T>
+__device__ __forceinline__ void fold_finite(Finite<T>& f, const Row<W, T>& r) {
+#pragma unroll
+  for (int k = 0; k < W; ++k) f.add(r.u[k], r.v[k]);
 }
 
-template <int W>
-__device__ __forceinline__ void store_row(float* __restrict__ u, float* __restrict__ v,
-                                          size_t off, const Row<W>& r) {
-  if constexpr (W == 4) {
+// 16-byte vector store when a lane's group is 16 bytes, else scalar stores.
+template <int W, class T>
+__device__ __forceinline__ void store_row(T* __restrict__ u, T* __restrict__ v, size_t off,
+                                          const Row<W, T>& r) {
+  if constexpr (W * sizeof(T) == 16 && sizeof(T) == 4) {
     __stcs(reinterpret_cast<float4*>(u + off), make_float4(r.u[0], r.u[1], r.u[2], r.u[3]));
     __stcs(reinterpret_cast<float4*>(v + off), make_float4(r.v[0], r.v[1], r.v[2], r.v[3]));
+  } else if constexpr (W * sizeof(T) == 16 && sizeof(T) == 8) {
+    __stcs(reinterpret_cast<double2*>(u + off), make_double2(r.u[0], r.u[1]));
+    __stcs(reinterpret_cast<double2*>(v + off), make_double2(r.v[0], r.v[1]));
   } else {
 #pragma unroll
     for (int k = 0; k < W; ++k) {
@@ -170,23 +203,23 @@ __device__ __forceinline__ void store_row(float* __restrict__ u, float* __restri
 }
 
 // One level of one row: out = step(center) given the rows above/below.
-template <int W, bool kFast>
-__device__ __forceinline__ void level_row(const Row<W>& up, const Row<W>& c,
-                                          const Row<W>& dn, Row<W>& out,
-                                          const Params& p, float neg_eps,
-                                          int lane_l, int lane_r) {
-  const float ul = __shfl_sync(kFull, c.u[W - 1], lane_l);
-  const float ur = __shfl_sync(kFull, c.u[0], lane_r);
-  const float vl = __shfl_sync(kFull, c.v[W - 1], lane_l);
-  const float vr = __shfl_sync(kFull, c.v[0], lane_r);
+template <int W, class T, bool kFast>
+__device__ __forceinline__ void level_row(const Row<W, T>& up, const Row<W, T>& c,
+                                          const Row<W, T>& dn, Row<W, T>& out,
+                                          const ParamsT<T>& p, T neg_eps, int lane_l,
+                                          int lane_r) {
+  const T ul = __shfl_sync(kFull, c.u[W - 1], lane_l);
+  const T ur = __shfl_sync(kFull, c.u[0], lane_r);
+  const T vl = __shfl_sync(kFull, c.v[W - 1], lane_l);
+  const T vr = __shfl_sync(kFull, c.v[0], lane_r);
 #pragma unroll
   for (int k = 0; k < W; ++k) {
-    const float u_l = k > 0 ? c.u[k - 1] : ul;
-    const float u_r = k < W - 1 ? c.u[k + 1] : ur;
-    const float v_l = k > 0 ? c.v[k - 1] : vl;
-    const float v_r = k < W - 1 ? c.v[k + 1] : vr;
-    fhn_cell<kFast>(c.u[k], c.v[k], u_r, u_l, dn.u[k], up.u[k], v_r, v_l, dn.v[k],
-                    up.v[k], p, neg_eps, out.u[k], out.v[k]);
+    const T u_l = k > 0 ? c.u[k - 1] : ul;
+    const T u_r = k < W - 1 ? c.u[k + 1] : ur;
+    const T v_l = k > 0 ? c.v[k - 1] : vl;
+    const T v_r = k < W - 1 ? c.v[k + 1] : vr;
+    fhn_cell<T, kFast>(c.u[k], c.v[k], u_r, u_l, dn.u[k], up.u[k], v_r, v_l, dn.v[k], up.v[k],
+                       p, neg_eps, out.u[k], out.v[k]);
   }
 }
 
@@ -196,25 +229,26 @@ __device__ __forceinline__ int wrap_index(int x, int n) {
 }
 
 // Level-0 rows are staged through a per-warp shared-memory ring with
-// cp.async (LDGSTS, L1-bypassing): kStage slots, prefetch distance
-// kStage - 3 ticks.  Each lane copies and later reads back only its own W
-// columns of each plane, so no cross-lane synchronisation is needed beyond
-// the lane's own cp.async.wait_group.
+// cp.async (LDGSTS; 16-byte copies bypass L1): kStage slots, prefetch
+// distance kStage - 3 ticks.  Each lane copies and later reads back only its
+// own W columns of each plane, so no cross-lane synchronisation is needed
+// beyond the lane's own cp.async.wait_group.
 constexpr int kStage = 8;
 constexpr int kPrefetch = kStage - 3;
 
-template <int W>
-__device__ __forceinline__ void stage_row(uint32_t dst, const float* __restrict__ u,
-                                          const float* __restrict__ v, size_t off) {
-  constexpr int B = 4 * W;  // bytes per lane per plane
-  if constexpr (W == 4) {
+template <int W, class T>
+__device__ __forceinline__ void stage_row(uint32_t dst, const T* __restrict__ u,
+                                          const T* __restrict__ v, size_t off) {
+  constexpr int B = int(sizeof(T)) * W;  // bytes per lane per plane
+  if constexpr (B == 16) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(u + off) : "memory");
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 32 * B), "l"(v + off) : "memory");
   } else {
+    constexpr int E = int(sizeof(T));
 #pragma unroll
     for (int k = 0; k < W; ++k) {
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst + 4 * k), "l"(u + off + k) : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst + 32 * B + 4 * k), "l"(v + off + k) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(dst + E * k), "l"(u + off + k), "n"(E) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(dst + 32 * B + E * k), "l"(v + off + k), "n"(E) : "memory");
     }
   }
 }
@@ -224,27 +258,37 @@ __device__ __forceinline__ void stage_commit() { asm volatile("cp.async.commit_g
 template <int N>
 __device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-template <int W>
-__device__ __forceinline__ void read_staged(uint32_t src, Row<W>& r) {
-  constexpr int B = 4 * W;
-  if constexpr (W == 4) {
+__device__ __forceinline__ void lds(uint32_t a, float& x) {
+  asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(x) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void lds(uint32_t a, double& x) {
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(x) : "r"(a) : "memory");
+}
+
+template <int W, class T>
+__device__ __forceinline__ void read_staged(uint32_t src, Row<W, T>& r) {
+  constexpr int B = int(sizeof(T)) * W;
+  if constexpr (B == 16 && sizeof(T) == 4) {
     asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
                  : "=f"(r.u[0]), "=f"(r.u[1]), "=f"(r.u[2]), "=f"(r.u[3]) : "r"(src) : "memory");
     asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
                  : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]) : "r"(src + 32 * B) : "memory");
+  } else if constexpr (B == 16 && sizeof(T) == 8) {
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(r.u[0]), "=d"(r.u[1]) : "r"(src) : "memory");
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(r.v[0]), "=d"(r.v[1]) : "r"(src + 32 * B) : "memory");
   } else {
 #pragma unroll
     for (int k = 0; k < W; ++k) {
-      asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(r.u[k]) : "r"(src + 4 * k) : "memory");
-      asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(r.v[k]) : "r"(src + 32 * B + 4 * k) : "memory");
+      lds(src + int(sizeof(T)) * k, r.u[k]);
+      lds(src + 32 * B + int(sizeof(T)) * k, r.v[k]);
     }
   }
 }
 
 // Shared memory per CTA of the wavefront kernel.
-template <int W>
+template <int W, class T>
 constexpr int wavefront_smem_bytes(int warps) {
-  return warps * kStage * 2 * 32 * 4 * W;
+  return warps * kStage * 2 * 32 * int(sizeof(T)) * W;
 }
 
 template <int V>
@@ -256,7 +300,7 @@ struct Bool {
   static constexpr bool value = V;
 };
 
-// Running row index on the torus (periodic) or in the ghosted slab buffer.
+// Running row offset on the torus (periodic) or in the ghosted slab buffer.
 struct RowCursor {
   size_t off;   // element offset of the current row (row * pitch)
   size_t step;  // pitch
@@ -267,7 +311,14 @@ struct RowCursor {
   }
 };
 
-// K levels per launch, W columns per lane.
+// Resident CTAs per SM the register budget is capped for (128 threads each):
+// 4 CTAs = 16 warps (<= 128 registers) for fp32 K <= 4 and fp64 K <= 2.
+template <int K, class T>
+struct MinBlocks {
+  static constexpr int value = (sizeof(T) == 4 ? K <= 4 : K <= 2) ? 4 : 2;
+};
+
+// K levels per launch, W columns per lane, element type T.
 //
 // Schedule (a skewed wavefront, levels visited top-down within a tick): at
 // tick j the warp has level-0 rows x_0..x_j (x_j = r0 - K + j) and
@@ -282,15 +333,9 @@ struct RowCursor {
 // Register rotation: level-t rows (t = 1..K-1) live in rings of 3 (tick j ->
 // slot j % 3); the tick loop is unrolled by 3 so every slot index is a
 // compile-time constant and no register is copied to advance a window.
-// Resident CTAs per SM the register budget is capped for (128 threads each):
-// 4 CTAs = 16 warps (<= 128 registers) for K <= 4; K = 8 needs ~220.
-template <int K>
-struct MinBlocks {
-  static constexpr int value = K <= 4 ? 4 : 2;
-};
-
-template <int K, int W, bool kFast, bool kPerGrid>
-__global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel(const StepArgs a) {
+template <int K, int W, class T, bool kFast, bool kPerGrid>
+__global__ void __launch_bounds__(128, MinBlocks<K, T>::value)
+    fhn_wavefront_kernel(const StepArgsT<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -309,8 +354,8 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel
 
   // Shared gene: read straight from the kernel-parameter bank.  Per-grid
   // genes (sweeps) come from global memory once per warp.
-  const Params p = kPerGrid ? a.params[g] : a.shared;
-  const float neg_eps = -p.eps;  // reference model.hpp:45 negates eps first
+  const ParamsT<T> p = kPerGrid ? a.params[g] : a.shared;
+  const T neg_eps = -p.eps;  // reference model.hpp:45 negates eps first
 
   const int G = a.cols / W;
   const int gl = band * a.band_groups - a.halo_groups + lane;
@@ -323,10 +368,10 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel
   const int lane_r = (lane + 1) & 31;
 
   const size_t goff = (size_t)g * (size_t)a.grid_stride + (size_t)grp * W;
-  const float* __restrict__ uin = a.u_in + goff;
-  const float* __restrict__ vin = a.v_in + goff;
-  float* __restrict__ uout = a.u_out + goff;
-  float* __restrict__ vout = a.v_out + goff;
+  const T* __restrict__ uin = a.u_in + goff;
+  const T* __restrict__ vin = a.v_in + goff;
+  T* __restrict__ uout = a.u_out + goff;
+  T* __restrict__ vout = a.v_out + goff;
   const size_t pitch = (size_t)a.pitch;
 
   const int r0 = a.row_begin + seg * a.seg_rows;
@@ -338,22 +383,23 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel
                 a.periodic ? (size_t)a.rows * pitch : ~size_t(0)};
   size_t out_off = (size_t)(a.periodic ? r0 : r0 + a.ghost) * pitch;
 
-  constexpr uint32_t kSlot = 2 * 32 * 4 * W;  // bytes of one staged row (u,v)
-  const uint32_t ring =
-      (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)wib * (kStage * kSlot) + lane * 4 * W;
+  constexpr uint32_t kLaneBytes = uint32_t(sizeof(T)) * W;
+  constexpr uint32_t kSlot = 2 * 32 * kLaneBytes;  // bytes of one staged row (u,v)
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem_raw) +
+                        (uint32_t)wib * (kStage * kSlot) + lane * kLaneBytes;
 
   // Prime the staging ring with the rows of ticks 0 .. kPrefetch-1.
 #pragma unroll
   for (int d = 0; d < kPrefetch; ++d) {
     if (d < n_load) {
-      stage_row<W>(ring + d * kSlot, uin, vin, cur.off);
+      stage_row<W, T>(ring + d * kSlot, uin, vin, cur.off);
       cur.next();
     }
     stage_commit();
   }
 
-  Row<W> win[K > 1 ? K - 1 : 1][3];
-  float mx = 0.0f;  // NaN-propagating max of |stored values|
+  Row<W, T> win[K > 1 ? K - 1 : 1][3];
+  Finite<T> fin;
   const uint32_t ring_end = ring + kStage * kSlot;
   uint32_t at_now = ring;                     // staging slot of tick j
   uint32_t at_pre = ring + kPrefetch * kSlot; // staging slot of tick j + kPrefetch
@@ -372,17 +418,17 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel
 #pragma unroll
     for (int t = K; t >= 2; --t) {
       if (kSteady || (j >= 3 * t - 1 && j < h + 2 * K + t - 1)) {
-        const Row<W>& up = win[t - 2][ph];
-        const Row<W>& ce = win[t - 2][(ph + 1) % 3];
-        const Row<W>& dn = win[t - 2][(ph + 2) % 3];
+        const Row<W, T>& up = win[t - 2][ph];
+        const Row<W, T>& ce = win[t - 2][(ph + 1) % 3];
+        const Row<W, T>& dn = win[t - 2][(ph + 2) % 3];
         if (t < K) {
-          level_row<W, kFast>(up, ce, dn, win[t - 1][ph], p, neg_eps, lane_l, lane_r);
+          level_row<W, T, kFast>(up, ce, dn, win[t - 1][ph], p, neg_eps, lane_l, lane_r);
         } else {
-          Row<W> o;
-          level_row<W, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
+          Row<W, T> o;
+          level_row<W, T, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
           if (store) {
-            store_row<W>(uout, vout, out_off, o);
-            absmax_nan<W>(mx, o);
+            store_row<W, T>(uout, vout, out_off, o);
+            fold_finite<W, T>(fin, o);
           }
           out_off += pitch;
         }
@@ -391,7 +437,7 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel
     // Stage the row of tick j + kPrefetch (an empty group past the end keeps
     // the wait_group accounting uniform).
     if (j + kPrefetch < n_load) {
-      stage_row<W>(at_pre, uin, vin, cur.off);
+      stage_row<W, T>(at_pre, uin, vin, cur.off);
       cur.next();
     }
     stage_commit();
@@ -399,29 +445,26 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel
     // Level 1 from the level-0 rows of ticks j-2, j-1, j.
     if (kSteady || (j >= 2 && j < n_load)) {
       stage_wait<kPrefetch>();  // the row of tick j has landed
-      Row<W> up, ce, dn;
+      Row<W, T> up, ce, dn;
       const uint32_t at1 = prev_slot(at_now);
-      read_staged<W>(prev_slot(at1), up);
-      read_staged<W>(at1, ce);
-      read_staged<W>(at_now, dn);
+      read_staged<W, T>(prev_slot(at1), up);
+      read_staged<W, T>(at1, ce);
+      read_staged<W, T>(at_now, dn);
       if constexpr (K == 1) {
-        Row<W> o;
-        level_row<W, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
+        Row<W, T> o;
+        level_row<W, T, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
         if (store) {
-          store_row<W>(uout, vout, out_off, o);
-          absmax_nan<W>(mx, o);
+          store_row<W, T>(uout, vout, out_off, o);
+          fold_finite<W, T>(fin, o);
         }
         out_off += pitch;
       } else {
-        level_row<W, kFast>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
+        level_row<W, T, kFast>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
       }
     }
     at_now = (at_now + kSlot == ring_end) ? ring : at_now + kSlot;
   };
 
-  using I0 = Int<0>;
-  using I1 = Int<1>;
-  using I2 = Int<2>;
   // Steady ticks: every level active, j in [3K-1, n_load).
   const int steady_lo = 3 * K - 1, steady_hi = n_load;
   // Only the deepest instance gets a separate steady-state copy of the loop
@@ -430,21 +473,18 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) fhn_wavefront_kernel
   constexpr bool kSplit = K >= 8;
   for (int j0 = 0; j0 < nt; j0 += 3) {
     if (kSplit && j0 >= steady_lo && j0 + 3 <= steady_hi) {
-      tick(I0{}, Bool<true>{}, j0);
-      tick(I1{}, Bool<true>{}, j0 + 1);
-      tick(I2{}, Bool<true>{}, j0 + 2);
+      tick(Int<0>{}, Bool<true>{}, j0);
+      tick(Int<1>{}, Bool<true>{}, j0 + 1);
+      tick(Int<2>{}, Bool<true>{}, j0 + 2);
     } else {
-      tick(I0{}, Bool<false>{}, j0);
-      if (j0 + 1 < nt) tick(I1{}, Bool<false>{}, j0 + 1);
-      if (j0 + 2 < nt) tick(I2{}, Bool<false>{}, j0 + 2);
+      tick(Int<0>{}, Bool<false>{}, j0);
+      if (j0 + 1 < nt) tick(Int<1>{}, Bool<false>{}, j0 + 1);
+      if (j0 + 2 < nt) tick(Int<2>{}, Bool<false>{}, j0 + 2);
     }
   }
   stage_wait<0>();
 
-  // mx >= 0, so its bit pattern orders like its value; NaN (0x7FFFFFFF) and
-  // +inf (0x7F800000) are the only patterns >= 0x7F800000.
-  const unsigned mb = __reduce_max_sync(kFull, __float_as_uint(mx));
-  if (lane == 0 && mb >= 0x7F800000u && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);
+  if (fin.bad_in_warp() && lane == 0 && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);
 }
 
 }  // namespace rdcnn_dev

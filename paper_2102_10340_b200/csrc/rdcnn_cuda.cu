@@ -18,8 +18,8 @@
 #include "fhn_stencil.cuh"
 #include "rdcnn_cuda.h"
 
-using rdcnn_dev::Params;
-using rdcnn_dev::StepArgs;
+using rdcnn_dev::ParamsT;
+using rdcnn_dev::StepArgsT;
 
 namespace {
 
@@ -42,81 +42,108 @@ int fail(int code, const char* fmt, ...) {
       return fail(RDCNN_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(e_));  \
   } while (0)
 
+#define RDCNN_TRY(expr)           \
+  do {                            \
+    int rc_ = (expr);             \
+    if (rc_ != RDCNN_OK) return rc_; \
+  } while (0)
+
 constexpr int kThreads = 128;  // 4 warps per CTA
 
 // ---------------------------------------------------------------------------
-// Kernel dispatch over the compiled (K, W, mode) instances.
+// Kernel dispatch over the compiled instances.
+//   fp32: W in {1,4}, K in {1,2,4,8}, strict|fast, shared|per-grid gene
+//   fp64: W in {1,2}, K in {1,2,4},   strict,      shared|per-grid gene
 // ---------------------------------------------------------------------------
 
-using KernelFn = void (*)(StepArgs);
-
-// Every compiled instance: [W=1|4][K=1,2,4,8][strict|fast][shared|per-grid gene].
-template <int W, int KI, int FI, int PI>
-constexpr KernelFn instance() {
-  constexpr int K = 1 << KI;
-  return &rdcnn_dev::fhn_wavefront_kernel<K, W, FI == 1, PI == 1>;
-}
-
-struct KernelTable {
-  KernelFn fn[2][4][2][2];
-  int resident[2][4][2][2];
+template <class T>
+struct Traits;
+template <>
+struct Traits<float> {
+  static constexpr int kWide = 4;
+  static constexpr int kMaxLevels = 8;
 };
-
-template <int W, int KI, int FI, int PI>
-void fill_one(KernelTable& t) {
-  t.fn[W == 4][KI][FI][PI] = instance<W, KI, FI, PI>();
-  t.resident[W == 4][KI][FI][PI] = 0;
-}
-
-template <int W, int KI>
-void fill_k(KernelTable& t) {
-  fill_one<W, KI, 0, 0>(t);
-  fill_one<W, KI, 0, 1>(t);
-  fill_one<W, KI, 1, 0>(t);
-  fill_one<W, KI, 1, 1>(t);
-}
-
-KernelTable make_table() {
-  KernelTable t{};
-  fill_k<1, 0>(t); fill_k<1, 1>(t); fill_k<1, 2>(t); fill_k<1, 3>(t);
-  fill_k<4, 0>(t); fill_k<4, 1>(t); fill_k<4, 2>(t); fill_k<4, 3>(t);
-  return t;
-}
-
-KernelTable& table() {
-  static KernelTable t = make_table();
-  return t;
-}
+template <>
+struct Traits<double> {
+  static constexpr int kWide = 2;
+  static constexpr int kMaxLevels = 4;
+};
 
 int k_index(int k) { return k == 1 ? 0 : k == 2 ? 1 : k == 4 ? 2 : 3; }
 
+template <class T>
+struct KernelTable {
+  using Fn = void (*)(StepArgsT<T>);
+  Fn fn[2][4][2][2] = {};        // [wide][k][fast][per_grid]
+  int resident[2][4][2][2] = {};
+};
+
+template <class T, int W, int KI, int FI, int PI>
+void fill_one(KernelTable<T>& t) {
+  constexpr int K = 1 << KI;
+  if constexpr (K <= Traits<T>::kMaxLevels && (FI == 0 || sizeof(T) == 4))
+    t.fn[W > 1][KI][FI][PI] = &rdcnn_dev::fhn_wavefront_kernel<K, W, T, FI == 1, PI == 1>;
+}
+
+template <class T, int W, int KI>
+void fill_k(KernelTable<T>& t) {
+  fill_one<T, W, KI, 0, 0>(t);
+  fill_one<T, W, KI, 0, 1>(t);
+  fill_one<T, W, KI, 1, 0>(t);
+  fill_one<T, W, KI, 1, 1>(t);
+}
+
+template <class T, int W>
+void fill_w(KernelTable<T>& t) {
+  fill_k<T, W, 0>(t);
+  fill_k<T, W, 1>(t);
+  fill_k<T, W, 2>(t);
+  fill_k<T, W, 3>(t);
+}
+
+template <class T>
+KernelTable<T>& table() {
+  static KernelTable<T> t = [] {
+    KernelTable<T> x;
+    fill_w<T, 1>(x);
+    fill_w<T, Traits<T>::kWide>(x);
+    return x;
+  }();
+  return t;
+}
+
 // Dynamic shared memory of one CTA (the level-0 staging rings).
+template <class T>
 size_t smem_for(int w) {
-  return w == 4 ? rdcnn_dev::wavefront_smem_bytes<4>(kThreads / 32)
-                : rdcnn_dev::wavefront_smem_bytes<1>(kThreads / 32);
+  return w > 1 ? rdcnn_dev::wavefront_smem_bytes<Traits<T>::kWide, T>(kThreads / 32)
+               : rdcnn_dev::wavefront_smem_bytes<1, T>(kThreads / 32);
 }
 
 // Resident CTAs per SM of one instance (cached; occupancy is immutable).
+template <class T>
 int resident_blocks(int k, int w, bool fast, bool per_grid) {
-  KernelTable& t = table();
-  int& r = t.resident[w == 4][k_index(k)][fast][per_grid];
+  KernelTable<T>& t = table<T>();
+  int& r = t.resident[w > 1][k_index(k)][fast][per_grid];
   if (r == 0) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, t.fn[w == 4][k_index(k)][fast][per_grid],
-                                                      kThreads, smem_for(w)) != cudaSuccess || n < 1)
+    auto fn = t.fn[w > 1][k_index(k)][fast][per_grid];
+    if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kThreads, smem_for<T>(w)) !=
+                   cudaSuccess || n < 1)
       n = 1;
     r = n;
   }
   return r;
 }
 
-cudaError_t launch_stencil(int k, int w, bool fast, bool per_grid, const StepArgs& a,
+template <class T>
+cudaError_t launch_stencil(int k, int w, bool fast, bool per_grid, const StepArgsT<T>& a,
                            long long warps, cudaStream_t s) {
   if (warps <= 0) return cudaSuccess;
   if (k != 1 && k != 2 && k != 4 && k != 8) return cudaErrorInvalidValue;
+  auto fn = table<T>().fn[w > 1][k_index(k)][fast][per_grid];
+  if (!fn) return cudaErrorInvalidValue;
   const long long blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
-  KernelFn fn = table().fn[w == 4][k_index(k)][fast][per_grid];
-  fn<<<dim3((unsigned)blocks), dim3(kThreads), smem_for(w), s>>>(a);
+  fn<<<dim3((unsigned)blocks), dim3(kThreads), smem_for<T>(w), s>>>(a);
   return cudaGetLastError();
 }
 
@@ -180,15 +207,19 @@ __device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64_t d) {
   return z ^ (z >> 31);
 }
 
-__device__ __forceinline__ float unit_f32(uint64_t z) {
-  return __fmul_rn((float)(z >> 40), 0x1.0p-24f);  // rng.hpp:28, exact
+__device__ __forceinline__ void unit_of(uint64_t z, float& x) {
+  x = __fmul_rn((float)(z >> 40), 0x1.0p-24f);  // rng.hpp:28, exact
+}
+__device__ __forceinline__ void unit_of(uint64_t z, double& x) {
+  x = __dmul_rn((double)(z >> 11), 0x1.0p-53);  // rng.hpp:25, exact
 }
 
 // Writes rows [row_offset, row_offset + local_rows) of a global
 // global_rows x cols lattice initialised with typ (1 or 2).
-__global__ void init_kernel(float* u, float* v, int pitch, long long grid_stride,
-                            int batch, int local_rows, int cols, int global_rows,
-                            int row_offset, int typ, uint64_t seed) {
+template <class T>
+__global__ void init_kernel(T* u, T* v, int pitch, long long grid_stride, int batch,
+                            int local_rows, int cols, int global_rows, int row_offset, int typ,
+                            uint64_t seed) {
   const long long n = (long long)local_rows * cols;
   const long long gcells = (long long)global_rows * cols;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n * batch;
@@ -198,17 +229,17 @@ __global__ void init_kernel(float* u, float* v, int pitch, long long grid_stride
     const int li = int(c / cols);
     const int j = int(c - (long long)li * cols);
     const int i = li + row_offset;  // global row
-    float uu = 0.0f, vv = 0.0f;
+    T uu = T(0), vv = T(0);
     if (typ == 2) {
       const long long cell = (long long)i * cols + j;
-      uu = unit_f32(splitmix_draw(seed, (uint64_t)cell));
-      vv = unit_f32(splitmix_draw(seed, (uint64_t)(gcells + cell)));
+      unit_of(splitmix_draw(seed, (uint64_t)cell), uu);
+      unit_of(splitmix_draw(seed, (uint64_t)(gcells + cell)), vv);
     } else {
       const int i0 = (global_rows - 11) / 2, j0 = (cols - 11) / 2;  // init.hpp:36-37
       if (i >= i0 && i < i0 + 11 && j >= j0 && j < j0 + 11) {
         const int d = (i - i0) * 11 + (j - j0);
-        uu = unit_f32(splitmix_draw(seed, (uint64_t)d));
-        vv = unit_f32(splitmix_draw(seed, (uint64_t)(121 + d)));
+        unit_of(splitmix_draw(seed, (uint64_t)d), uu);
+        unit_of(splitmix_draw(seed, (uint64_t)(121 + d)), vv);
       }
     }
     const size_t off = (size_t)g * grid_stride + (size_t)li * pitch + j;
@@ -217,9 +248,9 @@ __global__ void init_kernel(float* u, float* v, int pitch, long long grid_stride
   }
 }
 
-__global__ void image_kernel(float* u, float* v, int pitch, long long grid_stride,
-                             int batch, int rows, int cols, const uint8_t* px,
-                             const float* lut) {
+template <class T>
+__global__ void image_kernel(T* u, T* v, int pitch, long long grid_stride, int batch, int rows,
+                             int cols, const uint8_t* px, const T* lut) {
   const long long n = (long long)rows * cols;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n * batch;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -227,15 +258,14 @@ __global__ void image_kernel(float* u, float* v, int pitch, long long grid_strid
     const long long c = idx - (long long)g * n;
     const int i = int(c / cols);
     const int j = int(c - (long long)i * cols);
-    const float x = lut[px[c]];
+    const T x = lut[px[c]];
     const size_t off = (size_t)g * grid_stride + (size_t)i * pitch + j;
     u[off] = x;
     v[off] = x;
   }
 }
 
-__global__ void div3_selftest_kernel(int domain, unsigned long long* count,
-                                     unsigned* first_bad) {
+__global__ void div3_selftest_kernel(int domain, unsigned long long* count, unsigned* first_bad) {
   unsigned long long local = 0;
   unsigned first = 0xFFFFFFFFu;
   const unsigned long long total = 1ull << 32;
@@ -246,14 +276,44 @@ __global__ void div3_selftest_kernel(int domain, unsigned long long* count,
     if (domain == 1) x = __fmul_rn(x, x);
     const float want = __fdiv_rn(x, 3.0f);
     const float got = rdcnn_dev::div3_rn(x);
-    bool ok;
-    if (isfinite(x))
-      ok = __float_as_uint(got) == __float_as_uint(want);
-    else
-      ok = !isfinite(got);
+    const bool ok = isfinite(x) ? __float_as_uint(got) == __float_as_uint(want) : !isfinite(got);
     if (!ok) {
       ++local;
       first = min(first, bits);
+    }
+  }
+  if (local) {
+    atomicAdd(count, local);
+    atomicMin(first_bad, first);
+  }
+}
+
+// fp64: every exponent (all 2048) x a hashed stream of mantissas, plus the
+// same inputs squared (the x = u*u domain), against IEEE __ddiv_rn.
+__global__ void div3_selftest_f64_kernel(unsigned long long samples, unsigned long long* count,
+                                         unsigned long long* first_bad) {
+  unsigned long long local = 0, first = ~0ull;
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+       k < samples; k += (unsigned long long)gridDim.x * blockDim.x) {
+    uint64_t z = splitmix_draw(0x5EEDull, k);
+    const uint64_t expo = k & 0x7FFull;                 // sweep every exponent
+    uint64_t bits = (z & 0x800FFFFFFFFFFFFFull) | (expo << 52);
+    if ((k >> 11) % 7 == 0) bits &= ~0xFFFFFFFFull;     // low mantissa words zero
+    if ((k >> 11) % 11 == 0) bits |= 0xFFFFFFFFull;     // ... and all ones
+    for (int sq = 0; sq < 2; ++sq) {
+      double x = __longlong_as_double((long long)bits);
+      if (sq) x = __dmul_rn(x, x);
+      const double want = __ddiv_rn(x, 3.0);
+      const double got = rdcnn_dev::div3_rn(x);
+      bool ok;
+      if (isfinite(x))
+        ok = __double_as_longlong(got) == __double_as_longlong(want) || (x == 0.0 && got == 0.0);
+      else
+        ok = !isfinite(got);
+      if (!ok) {
+        ++local;
+        first = min(first, (unsigned long long)bits);
+      }
     }
   }
   if (local) {
@@ -276,16 +336,18 @@ int sm_count_for(int device) {
 
 struct rdcnn_sim {
   int rows = 0, cols = 0, batch = 1, device = 0, mode = RDCNN_STRICT;
+  int elem = 4;           // bytes per value: 4 (fp32) or 8 (fp64)
   bool slab = false;
   int ghost = 0;          // slab mode: ghost rows per side
-  int pitch = 0;          // floats between rows
-  int plane_off = 0;      // floats from u row start to v row start (slab: cols)
-  long long grid_stride = 0;  // floats between grids (periodic planar: rows*cols)
-  size_t buf_floats = 0;  // floats per buffer (both planes, all grids)
-  float* buf[2] = {nullptr, nullptr};
+  int pitch = 0;          // elements between rows
+  int plane_off = 0;      // elements from u row start to v row start (slab: cols)
+  long long grid_stride = 0;  // elements between grids (periodic planar: rows*cols)
+  size_t buf_elems = 0;   // elements per buffer (both planes, all grids)
+  void* buf[2] = {nullptr, nullptr};
   int cur = 0;            // front buffer index
-  Params* d_params = nullptr;
-  Params h_params{};      // the shared gene (params_stride == 0)
+  void* d_params = nullptr;   // ParamsT<T>[batch]
+  ParamsT<float> h_params_f{};   // the shared gene (params_stride == 0)
+  ParamsT<double> h_params_d{};
   int params_stride = 0;
   unsigned* d_flags = nullptr;  // batch words (+1 scratch for replays)
   unsigned* h_flags = nullptr;  // pinned mirror
@@ -298,22 +360,38 @@ struct rdcnn_sim {
   int sm_count = 148;
   unsigned slab_tag = 0;
 
-  float* u_ptr(int b) { return buf[b]; }
-  float* v_ptr(int b) { return slab ? buf[b] + plane_off : buf[b] + (size_t)rows * cols * batch; }
+  template <class T>
+  T* u_ptr(int b) {
+    return static_cast<T*>(buf[b]);
+  }
+  template <class T>
+  T* v_ptr(int b) {
+    return slab ? static_cast<T*>(buf[b]) + plane_off
+                : static_cast<T*>(buf[b]) + (size_t)rows * cols * batch;
+  }
+  template <class T>
+  const ParamsT<T>& shared_params() const;
 };
+
+template <>
+const ParamsT<float>& rdcnn_sim::shared_params<float>() const { return h_params_f; }
+template <>
+const ParamsT<double>& rdcnn_sim::shared_params<double>() const { return h_params_d; }
 
 namespace {
 
-int width_for(const rdcnn_sim* s) { return (s->cols % 4 == 0) ? 4 : 1; }
+template <class T>
+int width_for(const rdcnn_sim* s) {
+  return (s->cols % Traits<T>::kWide == 0) ? Traits<T>::kWide : 1;
+}
 
-// Periodic handles: planar layout, u planes of all grids then v planes.
-StepArgs base_args(const rdcnn_sim* s, int in_buf, int out_buf) {
-  StepArgs a{};
-  rdcnn_sim* m = const_cast<rdcnn_sim*>(s);
-  a.u_in = m->u_ptr(in_buf);
-  a.v_in = m->v_ptr(in_buf);
-  a.u_out = m->u_ptr(out_buf);
-  a.v_out = m->v_ptr(out_buf);
+template <class T>
+StepArgsT<T> base_args(rdcnn_sim* s, int in_buf, int out_buf) {
+  StepArgsT<T> a{};
+  a.u_in = s->u_ptr<T>(in_buf);
+  a.v_in = s->v_ptr<T>(in_buf);
+  a.u_out = s->u_ptr<T>(out_buf);
+  a.v_out = s->v_ptr<T>(out_buf);
   a.grid_stride = s->grid_stride;
   a.rows = s->rows;
   a.cols = s->cols;
@@ -321,19 +399,20 @@ StepArgs base_args(const rdcnn_sim* s, int in_buf, int out_buf) {
   a.periodic = s->slab ? 0 : 1;
   a.ghost = s->slab ? s->ghost : 0;
   a.batch = s->batch;
-  a.shared = s->h_params;
-  a.params = s->d_params;
+  a.shared = s->shared_params<T>();
+  a.params = static_cast<const ParamsT<T>*>(s->d_params);
   a.params_stride = s->params_stride;
   a.flags = s->d_flags;
   return a;
 }
 
-cudaError_t launch_range(rdcnn_sim* s, int k, StepArgs a, int row_begin, int row_end,
+template <class T>
+cudaError_t launch_range(rdcnn_sim* s, int k, StepArgsT<T> a, int row_begin, int row_end,
                          cudaStream_t st) {
-  const int w = width_for(s);
+  const int w = width_for<T>(s);
   const bool fast = s->mode == RDCNN_FAST;
   const bool per_grid = a.params_stride != 0;
-  const int rw = resident_blocks(k, w, fast, per_grid) * (kThreads / 32);
+  const int rw = resident_blocks<T>(k, w, fast, per_grid) * (kThreads / 32);
   Plan p = make_plan(s->cols, w, k, a.batch, row_begin, row_end, s->seg_rows, s->sm_count, rw);
   if (p.warps == 0) return cudaSuccess;
   a.row_begin = row_begin;
@@ -344,7 +423,7 @@ cudaError_t launch_range(rdcnn_sim* s, int k, StepArgs a, int row_begin, int row
   a.band_groups = p.band_groups;
   a.halo_groups = p.halo;
   ++s->launches;
-  return launch_stencil(k, w, fast, per_grid, a, p.warps, st);
+  return launch_stencil<T>(k, w, fast, per_grid, a, p.warps, st);
 }
 
 int alloc_common(rdcnn_sim* s) {
@@ -354,19 +433,23 @@ int alloc_common(rdcnn_sim* s) {
   RDCNN_CUDA_TRY(cudaEventCreate(&s->ev0));
   RDCNN_CUDA_TRY(cudaEventCreate(&s->ev1));
   for (int b = 0; b < 2; ++b) {
-    RDCNN_CUDA_TRY(cudaMalloc(&s->buf[b], s->buf_floats * sizeof(float)));
-    RDCNN_CUDA_TRY(cudaMemsetAsync(s->buf[b], 0, s->buf_floats * sizeof(float), s->stream));
+    RDCNN_CUDA_TRY(cudaMalloc(&s->buf[b], s->buf_elems * s->elem));
+    RDCNN_CUDA_TRY(cudaMemsetAsync(s->buf[b], 0, s->buf_elems * s->elem, s->stream));
   }
-  RDCNN_CUDA_TRY(cudaMalloc(&s->d_params, sizeof(Params) * (size_t)s->batch));
+  RDCNN_CUDA_TRY(cudaMalloc(&s->d_params, sizeof(ParamsT<double>) * (size_t)s->batch));
   RDCNN_CUDA_TRY(cudaMalloc(&s->d_flags, sizeof(unsigned) * ((size_t)s->batch + 1)));
   RDCNN_CUDA_TRY(cudaMemsetAsync(s->d_flags, 0, sizeof(unsigned) * ((size_t)s->batch + 1), s->stream));
   RDCNN_CUDA_TRY(cudaMallocHost(&s->h_flags, sizeof(unsigned) * ((size_t)s->batch + 1)));
   // Default gene (gene.hpp:13-24) until set_params is called.
-  double g7[7] = {0.1, -0.3, 1.3, -0.1, 1.0, 0.06, 1.0};
-  rdcnn_params_f32 p;
-  rdcnn_params_from_gene(g7, &p);
-  RDCNN_CUDA_TRY(cudaMemcpyAsync(s->d_params, &p, sizeof(Params), cudaMemcpyHostToDevice, s->stream));
-  std::memcpy(&s->h_params, &p, sizeof(Params));
+  const double g7[7] = {0.1, -0.3, 1.3, -0.1, 1.0, 0.06, 1.0};
+  s->h_params_d = {g7[0], g7[1], g7[2], g7[3], g7[4], g7[5], g7[6]};
+  rdcnn_params_f32 pf;
+  rdcnn_params_from_gene(g7, &pf);
+  std::memcpy(&s->h_params_f, &pf, sizeof pf);
+  if (s->elem == 4)
+    RDCNN_CUDA_TRY(cudaMemcpyAsync(s->d_params, &s->h_params_f, sizeof s->h_params_f, cudaMemcpyHostToDevice, s->stream));
+  else
+    RDCNN_CUDA_TRY(cudaMemcpyAsync(s->d_params, &s->h_params_d, sizeof s->h_params_d, cudaMemcpyHostToDevice, s->stream));
   s->params_stride = 0;
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
   return RDCNN_OK;
@@ -418,40 +501,41 @@ Schedule make_schedule(long steps, int kmax) {
 
 // Re-runs one block of grid g level by level from its preserved input to
 // find the first non-finite iteration.  Leaves the post-blow-up state in
-// buffer `final_buf`.  Returns the 1-based level (1..k) or a negative error.
+// buffer `final_buf`.  Returns the 1-based level (1..k) in *level_out.
+template <class T>
 int replay_grid(rdcnn_sim* s, int g, int in_buf, int k, int final_buf, int* level_out) {
   unsigned* scratch = s->d_flags + s->batch;
   int a_buf = in_buf;
+  const size_t off = (size_t)g * (size_t)s->grid_stride;
   for (int m = 1; m <= k; ++m) {
     RDCNN_CUDA_TRY(cudaMemsetAsync(scratch, 0, sizeof(unsigned), s->stream));
-    StepArgs a = base_args(s, a_buf, a_buf ^ 1);
-    const size_t off = (size_t)g * (size_t)s->grid_stride;
+    StepArgsT<T> a = base_args<T>(s, a_buf, a_buf ^ 1);
     a.u_in += off;
     a.v_in += off;
     a.u_out += off;
     a.v_out += off;
     a.batch = 1;
-    a.params = s->d_params + (size_t)g * s->params_stride;
+    a.params = static_cast<const ParamsT<T>*>(s->d_params) + (size_t)g * s->params_stride;
     a.flags = scratch;
+    a.tag = 1;
     if (s->params_stride != 0) {
       // One grid: run it on the shared-gene instance with its own gene.
-      RDCNN_CUDA_TRY(cudaMemcpyAsync(&a.shared, a.params, sizeof(Params), cudaMemcpyDeviceToHost, s->stream));
+      RDCNN_CUDA_TRY(cudaMemcpyAsync(&a.shared, a.params, sizeof(ParamsT<T>), cudaMemcpyDeviceToHost, s->stream));
       RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
       a.params_stride = 0;
     }
-    a.tag = 1;
-    RDCNN_CUDA_TRY(launch_range(s, 1, a, 0, s->rows, s->stream));
+    RDCNN_CUDA_TRY(launch_range<T>(s, 1, a, 0, s->rows, s->stream));
     unsigned hv = 0;
     RDCNN_CUDA_TRY(cudaMemcpyAsync(&hv, scratch, sizeof hv, cudaMemcpyDeviceToHost, s->stream));
     RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
     a_buf ^= 1;
     if (hv != 0) {
       if (a_buf != final_buf) {
-        const size_t plane = (size_t)s->rows * s->cols;
-        RDCNN_CUDA_TRY(cudaMemcpyAsync(s->u_ptr(final_buf) + off, s->u_ptr(a_buf) + off,
-                                       plane * sizeof(float), cudaMemcpyDeviceToDevice, s->stream));
-        RDCNN_CUDA_TRY(cudaMemcpyAsync(s->v_ptr(final_buf) + off, s->v_ptr(a_buf) + off,
-                                       plane * sizeof(float), cudaMemcpyDeviceToDevice, s->stream));
+        const size_t plane = (size_t)s->rows * s->cols * sizeof(T);
+        RDCNN_CUDA_TRY(cudaMemcpyAsync(s->u_ptr<T>(final_buf) + off, s->u_ptr<T>(a_buf) + off, plane,
+                                       cudaMemcpyDeviceToDevice, s->stream));
+        RDCNN_CUDA_TRY(cudaMemcpyAsync(s->v_ptr<T>(final_buf) + off, s->v_ptr<T>(a_buf) + off, plane,
+                                       cudaMemcpyDeviceToDevice, s->stream));
         RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
       }
       *level_out = m;
@@ -459,6 +543,217 @@ int replay_grid(rdcnn_sim* s, int g, int in_buf, int k, int final_buf, int* leve
     }
   }
   return fail(RDCNN_ECUDA, "blow-up flagged for grid %d but not reproduced by replay", g);
+}
+
+template <class T>
+int advance_impl(rdcnn_sim* s, long steps, long* first_bad) {
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  s->launches = 0;
+  if (first_bad)
+    for (int g = 0; g < s->batch; ++g) first_bad[g] = 0;
+  RDCNN_CUDA_TRY(cudaMemsetAsync(s->d_flags, 0, sizeof(unsigned) * (size_t)s->batch, s->stream));
+  const Schedule sched = make_schedule(steps, s->max_levels);
+  const int cur0 = s->cur;
+  RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
+  const long nl = sched.count();
+  for (long n = 0; n < nl; ++n) {
+    StepArgsT<T> a = base_args<T>(s, s->cur, s->cur ^ 1);
+    a.tag = (unsigned)(n + 1);
+    RDCNN_CUDA_TRY(launch_range<T>(s, sched.depth(n), a, 0, s->rows, s->stream));
+    s->cur ^= 1;
+  }
+  RDCNN_CUDA_TRY(cudaEventRecord(s->ev1, s->stream));
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(s->h_flags, s->d_flags, sizeof(unsigned) * (size_t)s->batch,
+                                 cudaMemcpyDeviceToHost, s->stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  float ms = 0;
+  RDCNN_CUDA_TRY(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+  s->last_ms = ms;
+  bool any = false;
+  for (int g = 0; g < s->batch; ++g) {
+    const unsigned tag = s->h_flags[g];
+    if (tag == 0) continue;
+    any = true;
+    const long n = (long)tag - 1;
+    const int in_buf = cur0 ^ int(n & 1);
+    int level = 0;
+    RDCNN_TRY(replay_grid<T>(s, g, in_buf, sched.depth(n), s->cur, &level));
+    if (first_bad) first_bad[g] = sched.start(n) + level;
+  }
+  if (any) return fail(RDCNN_EBLOWUP, "blow-up: non-finite state");
+  return RDCNN_OK;
+}
+
+int copy_state(rdcnn_sim* s, void* u, void* v, bool upload) {
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  const size_t e = (size_t)s->elem;
+  char* du = static_cast<char*>(s->buf[s->cur]);
+  char* dv = du + (s->slab ? (size_t)s->plane_off * e : (size_t)s->rows * s->cols * s->batch * e);
+  if (!s->slab) {
+    const size_t bytes = (size_t)s->rows * s->cols * s->batch * e;
+    const cudaMemcpyKind kind = upload ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    RDCNN_CUDA_TRY(cudaMemcpyAsync(upload ? (void*)du : u, upload ? u : (void*)du, bytes, kind, s->stream));
+    RDCNN_CUDA_TRY(cudaMemcpyAsync(upload ? (void*)dv : v, upload ? v : (void*)dv, bytes, kind, s->stream));
+  } else {
+    // Slab phases run on caller streams: drain them before touching the state.
+    RDCNN_CUDA_TRY(cudaDeviceSynchronize());
+    const size_t row0 = (size_t)s->ghost * s->pitch * e;
+    const size_t dpitch = (size_t)s->pitch * e, w = (size_t)s->cols * e;
+    if (upload) {
+      RDCNN_CUDA_TRY(cudaMemcpy2DAsync(du + row0, dpitch, u, w, w, s->rows, cudaMemcpyHostToDevice, s->stream));
+      RDCNN_CUDA_TRY(cudaMemcpy2DAsync(dv + row0, dpitch, v, w, w, s->rows, cudaMemcpyHostToDevice, s->stream));
+    } else {
+      RDCNN_CUDA_TRY(cudaMemcpy2DAsync(u, w, du + row0, dpitch, w, s->rows, cudaMemcpyDeviceToHost, s->stream));
+      RDCNN_CUDA_TRY(cudaMemcpy2DAsync(v, w, dv + row0, dpitch, w, s->rows, cudaMemcpyDeviceToHost, s->stream));
+    }
+  }
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RDCNN_OK;
+}
+
+int create_impl(int rows, int cols, int batch, int device, int mode, int elem, rdcnn_sim_t* out) {
+  if (!out) return fail(RDCNN_EINVAL, "null output handle");
+  *out = nullptr;
+  if (rows < 3 || cols < 3) return fail(RDCNN_EINVAL, "grid must be at least 3x3, got %dx%d", rows, cols);
+  if (batch < 1) return fail(RDCNN_EINVAL, "batch must be >= 1, got %d", batch);
+  if (mode != RDCNN_STRICT && mode != RDCNN_FAST) return fail(RDCNN_EINVAL, "unknown mode %d", mode);
+  if (elem != 4 && elem != 8) return fail(RDCNN_EINVAL, "element size must be 4 or 8 bytes, got %d", elem);
+  if (elem == 8 && mode == RDCNN_FAST) return fail(RDCNN_EINVAL, "fast mode is fp32 only");
+  auto* s = new (std::nothrow) rdcnn_sim();
+  if (!s) return fail(RDCNN_EINVAL, "out of host memory");
+  s->rows = rows;
+  s->cols = cols;
+  s->batch = batch;
+  s->device = device;
+  s->mode = mode;
+  s->elem = elem;
+  s->pitch = cols;
+  s->grid_stride = (long long)rows * cols;
+  s->buf_elems = (size_t)rows * cols * batch * 2;
+  s->max_levels = 4;
+  int rc = alloc_common(s);
+  if (rc != RDCNN_OK) {
+    std::string msg = g_last_error;
+    free_all(s);
+    g_last_error = msg;
+    return rc;
+  }
+  *out = s;
+  return RDCNN_OK;
+}
+
+template <class T>
+int init_impl(rdcnn_sim* s, int typ, uint64_t seed, int global_rows, int row_offset) {
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  const size_t row0 = s->slab ? (size_t)s->ghost * s->pitch : 0;
+  init_kernel<T><<<4 * s->sm_count, 256, 0, s->stream>>>(
+      s->u_ptr<T>(s->cur) + row0, s->v_ptr<T>(s->cur) + row0, s->pitch, s->grid_stride,
+      s->slab ? 1 : s->batch, s->rows, s->cols, global_rows, row_offset, typ, seed);
+  RDCNN_CUDA_TRY(cudaGetLastError());
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RDCNN_OK;
+}
+
+template <class T>
+int image_impl(rdcnn_sim* s, const uint8_t* px, double ka) {
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  T lut[256];
+  const T k = (T)ka;
+  for (int p = 0; p < 256; ++p) lut[p] = k * (T)(p / 255.0);  // init.hpp:58, image.hpp:283
+  const size_t n = (size_t)s->rows * s->cols;
+  uint8_t* d_px = nullptr;
+  T* d_lut = nullptr;
+  RDCNN_CUDA_TRY(cudaMallocAsync(&d_px, n, s->stream));
+  RDCNN_CUDA_TRY(cudaMallocAsync(&d_lut, sizeof lut, s->stream));
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(d_px, px, n, cudaMemcpyHostToDevice, s->stream));
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(d_lut, lut, sizeof lut, cudaMemcpyHostToDevice, s->stream));
+  image_kernel<T><<<4 * s->sm_count, 256, 0, s->stream>>>(s->u_ptr<T>(s->cur), s->v_ptr<T>(s->cur),
+                                                           s->pitch, s->grid_stride, s->batch,
+                                                           s->rows, s->cols, d_px, d_lut);
+  RDCNN_CUDA_TRY(cudaGetLastError());
+  RDCNN_CUDA_TRY(cudaFreeAsync(d_px, s->stream));
+  RDCNN_CUDA_TRY(cudaFreeAsync(d_lut, s->stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RDCNN_OK;
+}
+
+template <class T>
+int set_params_impl(rdcnn_sim* s, const ParamsT<T>* p, int n) {
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(s->d_params, p, sizeof(ParamsT<T>) * (size_t)n, cudaMemcpyHostToDevice, s->stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  s->params_stride = (n == 1) ? 0 : 1;
+  if (n == 1) {
+    if constexpr (sizeof(T) == 4) s->h_params_f = *p;
+    else s->h_params_d = *p;
+  }
+  return RDCNN_OK;
+}
+
+template <class T>
+int slab_step_impl(rdcnn_sim* s, int k, cudaStream_t st, bool boundary) {
+  StepArgsT<T> a = base_args<T>(s, s->cur, s->cur ^ 1);
+  if (boundary) ++s->slab_tag;
+  a.tag = s->slab_tag;
+  const int gh = s->ghost;
+  if (boundary) {
+    RDCNN_CUDA_TRY(launch_range<T>(s, k, a, 0, gh, st));
+    RDCNN_CUDA_TRY(launch_range<T>(s, k, a, s->rows - gh, s->rows, st));
+  } else {
+    RDCNN_CUDA_TRY(launch_range<T>(s, k, a, gh, s->rows - gh, st));
+  }
+  return RDCNN_OK;
+}
+
+int need_elem(rdcnn_sim* s, int elem) {
+  if (!s) return fail(RDCNN_EINVAL, "null handle");
+  if (s->elem != elem)
+    return fail(RDCNN_EINVAL, "handle holds fp%d values; this entry point is fp%d", 8 * s->elem, 8 * elem);
+  return RDCNN_OK;
+}
+
+template <class T>
+void host_unit(uint64_t& st, T& x) {
+  uint64_t z = (st += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  if constexpr (sizeof(T) == 4) x = (float)(z >> 40) * 0x1.0p-24f;
+  else x = (double)(z >> 11) * 0x1.0p-53;
+}
+
+template <class T>
+int host_full_random(int rows, int cols, uint64_t seed, T* u, T* v) {
+  if (rows < 3 || cols < 3 || !u || !v) return fail(RDCNN_EINVAL, "bad arguments");
+  uint64_t st = seed;
+  const size_t n = (size_t)rows * cols;
+  for (size_t k = 0; k < n; ++k) host_unit(st, u[k]);
+  for (size_t k = 0; k < n; ++k) host_unit(st, v[k]);
+  return RDCNN_OK;
+}
+
+template <class T>
+int host_center_square(int rows, int cols, uint64_t seed, T* u, T* v) {
+  if (rows < 11 || cols < 11 || !u || !v)
+    return fail(RDCNN_EINVAL, "typ=1 needs a grid of at least 11x11, got %dx%d", rows, cols);
+  const size_t n = (size_t)rows * cols;
+  std::fill(u, u + n, T(0));
+  std::fill(v, v + n, T(0));
+  const int i0 = (rows - 11) / 2, j0 = (cols - 11) / 2;
+  uint64_t st = seed;
+  for (T* plane : {u, v})
+    for (int i = i0; i < i0 + 11; ++i)
+      for (int j = j0; j < j0 + 11; ++j) host_unit(st, plane[(size_t)i * cols + j]);
+  return RDCNN_OK;
+}
+
+uint64_t fnv_planes(const void* u, const void* v, size_t bytes) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (const void* plane : {u, v}) {
+    const unsigned char* p = static_cast<const unsigned char*>(plane);
+    for (size_t i = 0; i < bytes; ++i) h = (h ^ p[i]) * 0x100000001b3ull;
+  }
+  return h;
 }
 
 }  // namespace
@@ -491,30 +786,16 @@ void rdcnn_params_from_gene(const double g[7], rdcnn_params_f32* out) {
 }
 
 int rdcnn_sim_create(int rows, int cols, int batch, int device, int mode, rdcnn_sim_t* out) {
-  if (!out) return fail(RDCNN_EINVAL, "null output handle");
-  *out = nullptr;
-  if (rows < 3 || cols < 3)
-    return fail(RDCNN_EINVAL, "grid must be at least 3x3, got %dx%d", rows, cols);
-  if (batch < 1) return fail(RDCNN_EINVAL, "batch must be >= 1, got %d", batch);
-  if (mode != RDCNN_STRICT && mode != RDCNN_FAST) return fail(RDCNN_EINVAL, "unknown mode %d", mode);
-  auto* s = new (std::nothrow) rdcnn_sim();
-  if (!s) return fail(RDCNN_EINVAL, "out of host memory");
-  s->rows = rows;
-  s->cols = cols;
-  s->batch = batch;
-  s->device = device;
-  s->mode = mode;
-  s->pitch = cols;
-  s->grid_stride = (long long)rows * cols;
-  s->buf_floats = (size_t)rows * cols * batch * 2;
-  int rc = alloc_common(s);
-  if (rc != RDCNN_OK) {
-    std::string msg = g_last_error;
-    free_all(s);
-    g_last_error = msg;
-    return rc;
-  }
-  *out = s;
+  return create_impl(rows, cols, batch, device, mode, 4, out);
+}
+
+int rdcnn_sim_create_f64(int rows, int cols, int batch, int device, rdcnn_sim_t* out) {
+  return create_impl(rows, cols, batch, device, RDCNN_STRICT, 8, out);
+}
+
+int rdcnn_sim_precision(rdcnn_sim_t s, int* bytes) {
+  if (!s || !bytes) return fail(RDCNN_EINVAL, "null argument");
+  *bytes = s->elem;
   return RDCNN_OK;
 }
 
@@ -525,6 +806,7 @@ int rdcnn_slab_create(int rows, int cols, int ghost, int device, int mode, rdcnn
   if (ghost != 1 && ghost != 2 && ghost != 4 && ghost != 8)
     return fail(RDCNN_EINVAL, "ghost depth must be 1, 2, 4 or 8, got %d", ghost);
   if (rows < 2 * ghost) return fail(RDCNN_EINVAL, "slab rows %d < 2*ghost %d", rows, 2 * ghost);
+  if (mode != RDCNN_STRICT && mode != RDCNN_FAST) return fail(RDCNN_EINVAL, "unknown mode %d", mode);
   auto* s = new (std::nothrow) rdcnn_sim();
   if (!s) return fail(RDCNN_EINVAL, "out of host memory");
   s->rows = rows;
@@ -532,12 +814,13 @@ int rdcnn_slab_create(int rows, int cols, int ghost, int device, int mode, rdcnn
   s->batch = 1;
   s->device = device;
   s->mode = mode;
+  s->elem = 4;
   s->slab = true;
   s->ghost = ghost;
   s->pitch = 2 * cols;
   s->plane_off = cols;
   s->grid_stride = 0;
-  s->buf_floats = (size_t)(rows + 2 * ghost) * 2 * cols;
+  s->buf_elems = (size_t)(rows + 2 * ghost) * 2 * cols;
   s->max_levels = ghost;
   int rc = alloc_common(s);
   if (rc != RDCNN_OK) {
@@ -546,29 +829,34 @@ int rdcnn_slab_create(int rows, int cols, int ghost, int device, int mode, rdcnn
     g_last_error = msg;
     return rc;
   }
-  // buf[b] points at the first ghost row; owned row 0 is `ghost` rows below.
-  *out = s;
+  *out = s;  // buf[b] points at the first ghost row; owned row 0 is `ghost` rows below
   return RDCNN_OK;
 }
 
 void rdcnn_sim_destroy(rdcnn_sim_t s) { free_all(s); }
 
 int rdcnn_sim_set_params(rdcnn_sim_t s, const rdcnn_params_f32* p, int n) {
-  if (!s || !p) return fail(RDCNN_EINVAL, "null argument");
+  RDCNN_TRY(need_elem(s, 4));
+  if (!p) return fail(RDCNN_EINVAL, "null argument");
   if (n != 1 && n != s->batch) return fail(RDCNN_EINVAL, "params count %d must be 1 or batch %d", n, s->batch);
-  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
-  static_assert(sizeof(Params) == sizeof(rdcnn_params_f32), "layout");
-  RDCNN_CUDA_TRY(cudaMemcpyAsync(s->d_params, p, sizeof(Params) * (size_t)n, cudaMemcpyHostToDevice, s->stream));
-  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
-  s->params_stride = (n == 1) ? 0 : 1;
-  if (n == 1) std::memcpy(&s->h_params, p, sizeof(Params));
-  return RDCNN_OK;
+  static_assert(sizeof(ParamsT<float>) == sizeof(rdcnn_params_f32), "layout");
+  return set_params_impl<float>(s, reinterpret_cast<const ParamsT<float>*>(p), n);
+}
+
+int rdcnn_sim_set_params_f64(rdcnn_sim_t s, const rdcnn_params_f64* p, int n) {
+  RDCNN_TRY(need_elem(s, 8));
+  if (!p) return fail(RDCNN_EINVAL, "null argument");
+  if (n != 1 && n != s->batch) return fail(RDCNN_EINVAL, "params count %d must be 1 or batch %d", n, s->batch);
+  static_assert(sizeof(ParamsT<double>) == sizeof(rdcnn_params_f64), "layout");
+  return set_params_impl<double>(s, reinterpret_cast<const ParamsT<double>*>(p), n);
 }
 
 int rdcnn_sim_set_tuning(rdcnn_sim_t s, int max_levels, int seg_rows) {
   if (!s) return fail(RDCNN_EINVAL, "null handle");
   if (max_levels != 1 && max_levels != 2 && max_levels != 4 && max_levels != 8)
     return fail(RDCNN_EINVAL, "max_levels must be 1, 2, 4 or 8, got %d", max_levels);
+  if (s->elem == 8 && max_levels > Traits<double>::kMaxLevels)
+    return fail(RDCNN_EINVAL, "fp64 handles fuse at most %d levels", Traits<double>::kMaxLevels);
   if (s->slab && max_levels > s->ghost)
     return fail(RDCNN_EINVAL, "max_levels %d exceeds slab ghost depth %d", max_levels, s->ghost);
   if (seg_rows < 0) return fail(RDCNN_EINVAL, "seg_rows must be >= 0");
@@ -578,40 +866,27 @@ int rdcnn_sim_set_tuning(rdcnn_sim_t s, int max_levels, int seg_rows) {
 }
 
 int rdcnn_sim_upload(rdcnn_sim_t s, const float* u, const float* v) {
-  if (!s || !u || !v) return fail(RDCNN_EINVAL, "null argument");
-  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
-  // Slab phases run on caller streams: drain them before touching the state.
-  if (s->slab) RDCNN_CUDA_TRY(cudaDeviceSynchronize());
-  const size_t plane = (size_t)s->rows * s->cols;
-  if (!s->slab) {
-    RDCNN_CUDA_TRY(cudaMemcpyAsync(s->u_ptr(s->cur), u, plane * s->batch * sizeof(float), cudaMemcpyHostToDevice, s->stream));
-    RDCNN_CUDA_TRY(cudaMemcpyAsync(s->v_ptr(s->cur), v, plane * s->batch * sizeof(float), cudaMemcpyHostToDevice, s->stream));
-  } else {
-    const size_t row0 = (size_t)s->ghost * s->pitch;
-    const size_t dpitch = (size_t)s->pitch * sizeof(float), w = (size_t)s->cols * sizeof(float);
-    RDCNN_CUDA_TRY(cudaMemcpy2DAsync(s->u_ptr(s->cur) + row0, dpitch, u, w, w, s->rows, cudaMemcpyHostToDevice, s->stream));
-    RDCNN_CUDA_TRY(cudaMemcpy2DAsync(s->v_ptr(s->cur) + row0, dpitch, v, w, w, s->rows, cudaMemcpyHostToDevice, s->stream));
-  }
-  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
-  return RDCNN_OK;
+  RDCNN_TRY(need_elem(s, 4));
+  if (!u || !v) return fail(RDCNN_EINVAL, "null argument");
+  return copy_state(s, const_cast<float*>(u), const_cast<float*>(v), true);
 }
 
 int rdcnn_sim_download(rdcnn_sim_t s, float* u, float* v) {
-  if (!s || !u || !v) return fail(RDCNN_EINVAL, "null argument");
-  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
-  if (s->slab) RDCNN_CUDA_TRY(cudaDeviceSynchronize());
-  const size_t plane = (size_t)s->rows * s->cols;
-  if (!s->slab) {
-    RDCNN_CUDA_TRY(cudaMemcpyAsync(u, s->u_ptr(s->cur), plane * s->batch * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
-    RDCNN_CUDA_TRY(cudaMemcpyAsync(v, s->v_ptr(s->cur), plane * s->batch * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
-  } else {
-    const size_t row0 = (size_t)s->ghost * s->pitch;
-    const size_t spitch = (size_t)s->pitch * sizeof(float), w = (size_t)s->cols * sizeof(float);
-    RDCNN_CUDA_TRY(cudaMemcpy2DAsync(u, w, s->u_ptr(s->cur) + row0, spitch, w, s->rows, cudaMemcpyDeviceToHost, s->stream));
-    RDCNN_CUDA_TRY(cudaMemcpy2DAsync(v, w, s->v_ptr(s->cur) + row0, spitch, w, s->rows, cudaMemcpyDeviceToHost, s->stream));
-  }
-  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
-  return RDCNN_OK;
+  RDCNN_TRY(need_elem(s, 4));
+  if (!u || !v) return fail(RDCNN_EINVAL, "null argument");
+  return copy_state(s, u, v, false);
+}
+
+int rdcnn_sim_upload_f64(rdcnn_sim_t s, const double* u, const double* v) {
+  RDCNN_TRY(need_elem(s, 8));
+  if (!u || !v) return fail(RDCNN_EINVAL, "null argument");
+  return copy_state(s, const_cast<double*>(u), const_cast<double*>(v), true);
+}
+
+int rdcnn_sim_download_f64(rdcnn_sim_t s, double* u, double* v) {
+  RDCNN_TRY(need_elem(s, 8));
+  if (!u || !v) return fail(RDCNN_EINVAL, "null argument");
+  return copy_state(s, u, v, false);
 }
 
 int rdcnn_sim_init(rdcnn_sim_t s, int typ, uint64_t seed) {
@@ -620,16 +895,9 @@ int rdcnn_sim_init(rdcnn_sim_t s, int typ, uint64_t seed) {
   if (s->slab) return fail(RDCNN_EINVAL, "slab handles initialise through rdcnn_slab_init");
   if (typ == 1 && (s->rows < 11 || s->cols < 11))
     return fail(RDCNN_EINVAL, "typ=1 needs a grid of at least 11x11, got %dx%d", s->rows, s->cols);
-  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
-  init_kernel<<<4 * s->sm_count, 256, 0, s->stream>>>(s->u_ptr(s->cur), s->v_ptr(s->cur), s->pitch,
-                                                       s->grid_stride, s->batch, s->rows, s->cols,
-                                                       s->rows, 0, typ, seed);
-  RDCNN_CUDA_TRY(cudaGetLastError());
-  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
-  return RDCNN_OK;
+  return s->elem == 4 ? init_impl<float>(s, typ, seed, s->rows, 0) : init_impl<double>(s, typ, seed, s->rows, 0);
 }
 
-// Slab of a global_rows x cols torus starting at global row row_offset.
 int rdcnn_slab_init(rdcnn_sim_t s, int typ, uint64_t seed, int global_rows, int row_offset) {
   if (!s || !s->slab) return fail(RDCNN_EINVAL, "not a slab handle");
   if (typ != 1 && typ != 2) return fail(RDCNN_EINVAL, "typ must be 1 or 2");
@@ -638,80 +906,20 @@ int rdcnn_slab_init(rdcnn_sim_t s, int typ, uint64_t seed, int global_rows, int 
   if (row_offset < 0 || row_offset + s->rows > global_rows)
     return fail(RDCNN_EINVAL, "slab rows [%d,%d) outside the %d-row lattice", row_offset,
                 row_offset + s->rows, global_rows);
-  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
-  const size_t row0 = (size_t)s->ghost * s->pitch;
-  init_kernel<<<4 * s->sm_count, 256, 0, s->stream>>>(s->u_ptr(s->cur) + row0, s->v_ptr(s->cur) + row0,
-                                                       s->pitch, 0, 1, s->rows, s->cols, global_rows,
-                                                       row_offset, typ, seed);
-  RDCNN_CUDA_TRY(cudaGetLastError());
-  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
-  return RDCNN_OK;
+  return init_impl<float>(s, typ, seed, global_rows, row_offset);
 }
 
 int rdcnn_sim_init_image(rdcnn_sim_t s, const uint8_t* px, double ka) {
   if (!s || !px) return fail(RDCNN_EINVAL, "null argument");
   if (s->slab) return fail(RDCNN_EINVAL, "image init is for periodic handles");
-  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
-  float lut[256];
-  const float k = (float)ka;
-  for (int p = 0; p < 256; ++p) lut[p] = k * (float)(p / 255.0);  // init.hpp:58, image.hpp:283
-  const size_t n = (size_t)s->rows * s->cols;
-  uint8_t* d_px = nullptr;
-  float* d_lut = nullptr;
-  RDCNN_CUDA_TRY(cudaMallocAsync(&d_px, n, s->stream));
-  RDCNN_CUDA_TRY(cudaMallocAsync(&d_lut, sizeof lut, s->stream));
-  RDCNN_CUDA_TRY(cudaMemcpyAsync(d_px, px, n, cudaMemcpyHostToDevice, s->stream));
-  RDCNN_CUDA_TRY(cudaMemcpyAsync(d_lut, lut, sizeof lut, cudaMemcpyHostToDevice, s->stream));
-  image_kernel<<<4 * s->sm_count, 256, 0, s->stream>>>(s->u_ptr(s->cur), s->v_ptr(s->cur), s->pitch,
-                                                        s->grid_stride, s->batch, s->rows, s->cols,
-                                                        d_px, d_lut);
-  RDCNN_CUDA_TRY(cudaGetLastError());
-  RDCNN_CUDA_TRY(cudaFreeAsync(d_px, s->stream));
-  RDCNN_CUDA_TRY(cudaFreeAsync(d_lut, s->stream));
-  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
-  return RDCNN_OK;
+  return s->elem == 4 ? image_impl<float>(s, px, ka) : image_impl<double>(s, px, ka);
 }
 
 int rdcnn_sim_advance(rdcnn_sim_t s, long steps, long* first_bad) {
   if (!s) return fail(RDCNN_EINVAL, "null handle");
   if (s->slab) return fail(RDCNN_EINVAL, "slab handles advance through rdcnn_slab_step_*");
   if (steps < 0) return fail(RDCNN_EINVAL, "steps must be >= 0, got %ld", steps);
-  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
-  s->launches = 0;
-  if (first_bad)
-    for (int g = 0; g < s->batch; ++g) first_bad[g] = 0;
-  RDCNN_CUDA_TRY(cudaMemsetAsync(s->d_flags, 0, sizeof(unsigned) * (size_t)s->batch, s->stream));
-  const Schedule sched = make_schedule(steps, s->max_levels);
-  const int cur0 = s->cur;
-  RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
-  const long nl = sched.count();
-  for (long n = 0; n < nl; ++n) {
-    StepArgs a = base_args(s, s->cur, s->cur ^ 1);
-    a.tag = (unsigned)(n + 1);
-    RDCNN_CUDA_TRY(launch_range(s, sched.depth(n), a, 0, s->rows, s->stream));
-    s->cur ^= 1;
-  }
-  RDCNN_CUDA_TRY(cudaEventRecord(s->ev1, s->stream));
-  RDCNN_CUDA_TRY(cudaMemcpyAsync(s->h_flags, s->d_flags, sizeof(unsigned) * (size_t)s->batch,
-                                 cudaMemcpyDeviceToHost, s->stream));
-  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
-  float ms = 0;
-  RDCNN_CUDA_TRY(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
-  s->last_ms = ms;
-  bool any = false;
-  for (int g = 0; g < s->batch; ++g) {
-    const unsigned tag = s->h_flags[g];
-    if (tag == 0) continue;
-    any = true;
-    const long n = (long)tag - 1;
-    const int in_buf = cur0 ^ int(n & 1);
-    int level = 0;
-    int rc = replay_grid(s, g, in_buf, sched.depth(n), s->cur, &level);
-    if (rc != RDCNN_OK) return rc;
-    if (first_bad) first_bad[g] = sched.start(n) + level;
-  }
-  if (any) return fail(RDCNN_EBLOWUP, "blow-up: non-finite state");
-  return RDCNN_OK;
+  return s->elem == 4 ? advance_impl<float>(s, steps, first_bad) : advance_impl<double>(s, steps, first_bad);
 }
 
 int rdcnn_sim_elapsed_ms(rdcnn_sim_t s, double* ms) {
@@ -732,11 +940,13 @@ int rdcnn_sim_stream(rdcnn_sim_t s, void** stream) {
   return RDCNN_OK;
 }
 
-int rdcnn_sim_device_state(rdcnn_sim_t s, float** u, float** v) {
+int rdcnn_sim_device_state(rdcnn_sim_t s, void** u, void** v) {
   if (!s || !u || !v) return fail(RDCNN_EINVAL, "null argument");
-  const size_t row0 = s->slab ? (size_t)s->ghost * s->pitch : 0;
-  *u = s->u_ptr(s->cur) + row0;
-  *v = s->v_ptr(s->cur) + row0;
+  const size_t e = (size_t)s->elem;
+  char* base = static_cast<char*>(s->buf[s->cur]);
+  const size_t row0 = s->slab ? (size_t)s->ghost * s->pitch * e : 0;
+  *u = base + row0;
+  *v = base + row0 + (s->slab ? (size_t)s->plane_off * e : (size_t)s->rows * s->cols * s->batch * e);
   return RDCNN_OK;
 }
 
@@ -749,18 +959,7 @@ static int slab_step(rdcnn_sim_t s, int k, void* stream, bool boundary) {
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   // The stream is taken literally: 0 is the legacy default stream (what
   // torch.cuda.current_stream() reports by default), not the handle's stream.
-  cudaStream_t st = (cudaStream_t)stream;
-  StepArgs a = base_args(s, s->cur, s->cur ^ 1);
-  if (boundary) ++s->slab_tag;
-  a.tag = s->slab_tag;
-  const int gh = s->ghost;
-  if (boundary) {
-    RDCNN_CUDA_TRY(launch_range(s, k, a, 0, gh, st));
-    RDCNN_CUDA_TRY(launch_range(s, k, a, s->rows - gh, s->rows, st));
-  } else {
-    RDCNN_CUDA_TRY(launch_range(s, k, a, gh, s->rows - gh, st));
-  }
-  return RDCNN_OK;
+  return slab_step_impl<float>(s, k, (cudaStream_t)stream, boundary);
 }
 
 int rdcnn_slab_step_boundary(rdcnn_sim_t s, int k, void* stream) { return slab_step(s, k, stream, true); }
@@ -776,8 +975,8 @@ int rdcnn_slab_rows_ptr(rdcnn_sim_t s, int which, float** first_row, float** fir
   if (!s || !s->slab || !first_row || !first_ghost) return fail(RDCNN_EINVAL, "bad argument");
   if (which != 0 && which != 1) return fail(RDCNN_EINVAL, "which must be 0 (front) or 1 (back)");
   const int b = which == 0 ? s->cur : s->cur ^ 1;
-  *first_ghost = s->buf[b];
-  *first_row = s->buf[b] + (size_t)s->ghost * s->pitch;
+  *first_ghost = s->u_ptr<float>(b);
+  *first_row = s->u_ptr<float>(b) + (size_t)s->ghost * s->pitch;
   return RDCNN_OK;
 }
 
@@ -794,48 +993,24 @@ int rdcnn_slab_poll_blowup(rdcnn_sim_t s, int* bad, unsigned* tag) {
 
 // ---- host helpers ------------------------------------------------------------
 
-static uint64_t host_mix(uint64_t& st) {
-  uint64_t z = (st += 0x9E3779B97F4A7C15ull);
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
-}
-static float host_unit(uint64_t& st) { return (float)(host_mix(st) >> 40) * 0x1.0p-24f; }
-
 int rdcnn_init_full_random_host(int rows, int cols, uint64_t seed, float* u, float* v) {
-  if (rows < 3 || cols < 3 || !u || !v) return fail(RDCNN_EINVAL, "bad arguments");
-  uint64_t st = seed;
-  const size_t n = (size_t)rows * cols;
-  for (size_t k = 0; k < n; ++k) u[k] = host_unit(st);
-  for (size_t k = 0; k < n; ++k) v[k] = host_unit(st);
-  return RDCNN_OK;
+  return host_full_random<float>(rows, cols, seed, u, v);
 }
-
 int rdcnn_init_center_square_host(int rows, int cols, uint64_t seed, float* u, float* v) {
-  if (rows < 11 || cols < 11 || !u || !v)
-    return fail(RDCNN_EINVAL, "typ=1 needs a grid of at least 11x11, got %dx%d", rows, cols);
-  const size_t n = (size_t)rows * cols;
-  std::memset(u, 0, n * sizeof(float));
-  std::memset(v, 0, n * sizeof(float));
-  const int i0 = (rows - 11) / 2, j0 = (cols - 11) / 2;
-  uint64_t st = seed;
-  for (int i = i0; i < i0 + 11; ++i)
-    for (int j = j0; j < j0 + 11; ++j) u[(size_t)i * cols + j] = host_unit(st);
-  for (int i = i0; i < i0 + 11; ++i)
-    for (int j = j0; j < j0 + 11; ++j) v[(size_t)i * cols + j] = host_unit(st);
-  return RDCNN_OK;
+  return host_center_square<float>(rows, cols, seed, u, v);
+}
+int rdcnn_init_full_random_host_f64(int rows, int cols, uint64_t seed, double* u, double* v) {
+  return host_full_random<double>(rows, cols, seed, u, v);
+}
+int rdcnn_init_center_square_host_f64(int rows, int cols, uint64_t seed, double* u, double* v) {
+  return host_center_square<double>(rows, cols, seed, u, v);
 }
 
 uint64_t rdcnn_checksum_f32(const float* u, const float* v, size_t cells) {
-  uint64_t h = 0xcbf29ce484222325ull;
-  const unsigned char* planes[2] = {reinterpret_cast<const unsigned char*>(u),
-                                    reinterpret_cast<const unsigned char*>(v)};
-  for (const unsigned char* p : planes)
-    for (size_t i = 0; i < cells * sizeof(float); ++i) {
-      h ^= p[i];
-      h *= 0x100000001b3ull;
-    }
-  return h;
+  return fnv_planes(u, v, cells * sizeof(float));
+}
+uint64_t rdcnn_checksum_f64(const double* u, const double* v, size_t cells) {
+  return fnv_planes(u, v, cells * sizeof(double));
 }
 
 int rdcnn_selftest_div3(int device, int domain, uint64_t* mismatches, uint32_t* first_bad) {
@@ -852,6 +1027,26 @@ int rdcnn_selftest_div3(int device, int domain, uint64_t* mismatches, uint32_t* 
   RDCNN_CUDA_TRY(cudaGetLastError());
   unsigned long long c = 0;
   unsigned f = 0;
+  RDCNN_CUDA_TRY(cudaMemcpy(&c, d_count, sizeof c, cudaMemcpyDeviceToHost));
+  RDCNN_CUDA_TRY(cudaMemcpy(&f, d_first, sizeof f, cudaMemcpyDeviceToHost));
+  cudaFree(d_count);
+  cudaFree(d_first);
+  *mismatches = c;
+  *first_bad = f;
+  return RDCNN_OK;
+}
+
+int rdcnn_selftest_div3_f64(int device, uint64_t samples, uint64_t* mismatches, uint64_t* first_bad) {
+  if (!mismatches || !first_bad) return fail(RDCNN_EINVAL, "bad arguments");
+  RDCNN_CUDA_TRY(cudaSetDevice(device));
+  unsigned long long *d_count = nullptr, *d_first = nullptr;
+  RDCNN_CUDA_TRY(cudaMalloc(&d_count, sizeof *d_count));
+  RDCNN_CUDA_TRY(cudaMalloc(&d_first, sizeof *d_first));
+  RDCNN_CUDA_TRY(cudaMemset(d_count, 0, sizeof *d_count));
+  RDCNN_CUDA_TRY(cudaMemset(d_first, 0xFF, sizeof *d_first));
+  div3_selftest_f64_kernel<<<sm_count_for(device) * 8, 256>>>(samples, d_count, d_first);
+  RDCNN_CUDA_TRY(cudaGetLastError());
+  unsigned long long c = 0, f = 0;
   RDCNN_CUDA_TRY(cudaMemcpy(&c, d_count, sizeof c, cudaMemcpyDeviceToHost));
   RDCNN_CUDA_TRY(cudaMemcpy(&f, d_first, sizeof f, cudaMemcpyDeviceToHost));
   cudaFree(d_count);

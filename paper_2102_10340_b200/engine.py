@@ -34,7 +34,9 @@ from typing import Callable, List, Optional, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import RDCNN_EBLOWUP, RDCNN_FAST, RDCNN_STRICT, ParamsF32, check, load
+from ._lib import RDCNN_EBLOWUP, RDCNN_FAST, RDCNN_STRICT, ParamsF32, ParamsF64, check, load
+
+DTYPES = {"single": np.float32, "double": np.float64}
 
 __all__ = [
     "Gene", "GridState", "Backend", "make_backend", "StepBuffers", "step", "run",
@@ -73,8 +75,10 @@ def gene_valid(g: Gene) -> bool:
     return all(np.isfinite(vals)) and g.dt >= 0 and g.Du >= 0 and g.Dv >= 0
 
 
-def params_from_gene(g: Gene) -> ParamsF32:
-    """make_params<float> (model.hpp:24-32), narrowed by the C-ABI."""
+def params_from_gene(g: Gene, precision: str = "single"):
+    """make_params<T> (model.hpp:24-32): narrowed to fp32 by the C-ABI, or fp64 as is."""
+    if precision == "double":
+        return ParamsF64(*[float(x) for x in g.to_vector()])
     lib = load()
     arr = (ctypes.c_double * 7)(*g.to_vector())
     out = ParamsF32()
@@ -85,24 +89,34 @@ def params_from_gene(g: Gene) -> ParamsF32:
 class GridState:
     """The paired u/v layers of a rows x cols toroidal lattice (grid.hpp:31-53)."""
 
-    def __init__(self, rows: int, cols: int, u=None, v=None):
+    def __init__(self, rows: int, cols: int, u=None, v=None, dtype=None):
         if rows < 3 or cols < 3:
             raise ValueError("grid must be at least 3x3")
         self.rows, self.cols = int(rows), int(cols)
         n = self.rows * self.cols
-        self.u = np.zeros(n, np.float32) if u is None else np.ascontiguousarray(u, np.float32).reshape(n)
-        self.v = np.zeros(n, np.float32) if v is None else np.ascontiguousarray(v, np.float32).reshape(n)
+        if dtype is None:
+            dtype = u.dtype if isinstance(u, np.ndarray) and u.dtype == np.float64 else np.float32
+        self.dtype = np.dtype(dtype)
+        self.u = np.zeros(n, dtype) if u is None else np.ascontiguousarray(u, dtype).reshape(n)
+        self.v = np.zeros(n, dtype) if v is None else np.ascontiguousarray(v, dtype).reshape(n)
+
+    @property
+    def precision(self) -> str:
+        return "double" if self.dtype == np.float64 else "single"
 
     def cells(self) -> int:
         return self.rows * self.cols
 
     def copy(self) -> "GridState":
-        return GridState(self.rows, self.cols, self.u.copy(), self.v.copy())
+        return GridState(self.rows, self.cols, self.u.copy(), self.v.copy(), self.dtype)
 
     def __eq__(self, other) -> bool:  # bitwise, like the defaulted operator==
-        return (isinstance(other, GridState) and self.rows == other.rows and self.cols == other.cols
-                and np.array_equal(self.u.view(np.uint32), other.u.view(np.uint32))
-                and np.array_equal(self.v.view(np.uint32), other.v.view(np.uint32)))
+        if not (isinstance(other, GridState) and self.rows == other.rows and self.cols == other.cols
+                and self.dtype == other.dtype):
+            return False
+        it = np.uint32 if self.dtype == np.float32 else np.uint64
+        return (np.array_equal(self.u.view(it), other.u.view(it))
+                and np.array_equal(self.v.view(it), other.v.view(it)))
 
 
 class BlowUpError(RuntimeError):
@@ -173,17 +187,29 @@ class Simulator:
     """Owner of one device state (C-ABI handle): batch x rows x cols, two planes."""
 
     def __init__(self, rows: int, cols: int, batch: int = 1, device: int = 0, mode: str = "strict",
-                 levels: int = 4, seg_rows: int = 0):
+                 levels: int = 4, seg_rows: int = 0, precision: str = "single"):
         self._lib = load()
         self.rows, self.cols, self.batch, self.device = int(rows), int(cols), int(batch), int(device)
         self.mode = mode
+        if precision not in DTYPES:
+            raise ValueError(f"unknown precision {precision} (expected single|double)")
+        self.precision = precision
+        self.dtype = np.dtype(DTYPES[precision])
+        self._f64 = precision == "double"
         h = ctypes.c_void_p()
         m = RDCNN_FAST if mode == "fast" else RDCNN_STRICT
         if mode not in ("strict", "fast"):
             raise ValueError(f"unknown mode {mode}")
-        check(self._lib.rdcnn_sim_create(self.rows, self.cols, self.batch, self.device, m, ctypes.byref(h)))
+        if self._f64:
+            check(self._lib.rdcnn_sim_create_f64(self.rows, self.cols, self.batch, self.device, ctypes.byref(h)))
+            levels = min(levels, 4)
+        else:
+            check(self._lib.rdcnn_sim_create(self.rows, self.cols, self.batch, self.device, m, ctypes.byref(h)))
         self._h = h
         self.set_tuning(levels, seg_rows)
+        L = self._lib
+        self._up = L.rdcnn_sim_upload_f64 if self._f64 else L.rdcnn_sim_upload
+        self._down = L.rdcnn_sim_download_f64 if self._f64 else L.rdcnn_sim_download
 
     # lifetime
     def close(self):
@@ -209,35 +235,37 @@ class Simulator:
         self.levels = int(levels)
 
     def set_params(self, genes):
-        genes = [genes] if isinstance(genes, (Gene, ParamsF32)) else list(genes)
-        arr = (ParamsF32 * len(genes))()
+        kind = ParamsF64 if self._f64 else ParamsF32
+        genes = [genes] if isinstance(genes, (Gene, ParamsF32, ParamsF64)) else list(genes)
+        arr = (kind * len(genes))()
         for k, g in enumerate(genes):
-            arr[k] = g if isinstance(g, ParamsF32) else params_from_gene(g)
-        check(self._lib.rdcnn_sim_set_params(self._h, arr, len(genes)))
+            arr[k] = g if isinstance(g, kind) else params_from_gene(g, self.precision)
+        fn = self._lib.rdcnn_sim_set_params_f64 if self._f64 else self._lib.rdcnn_sim_set_params
+        check(fn(self._h, arr, len(genes)))
 
     # state transfer
     def _shape_n(self) -> int:
         return self.batch * self.rows * self.cols
 
     def upload(self, u: np.ndarray, v: np.ndarray):
-        u = np.ascontiguousarray(u, np.float32)
-        v = np.ascontiguousarray(v, np.float32)
+        u = np.ascontiguousarray(u, self.dtype)
+        v = np.ascontiguousarray(v, self.dtype)
         if u.size != self._shape_n() or v.size != self._shape_n():
             raise ValueError("upload size does not match batch*rows*cols")
-        check(self._lib.rdcnn_sim_upload(self._h, _ptr(u), _ptr(v)))
+        check(self._up(self._h, _ptr(u), _ptr(v)))
 
     def upload_ptr(self, u_ptr: int, v_ptr: int):
-        check(self._lib.rdcnn_sim_upload(self._h, ctypes.c_void_p(u_ptr), ctypes.c_void_p(v_ptr)))
+        check(self._up(self._h, ctypes.c_void_p(u_ptr), ctypes.c_void_p(v_ptr)))
 
     def download(self, u: Optional[np.ndarray] = None, v: Optional[np.ndarray] = None):
         n = self._shape_n()
-        u = np.empty(n, np.float32) if u is None else u
-        v = np.empty(n, np.float32) if v is None else v
-        check(self._lib.rdcnn_sim_download(self._h, _ptr(u), _ptr(v)))
+        u = np.empty(n, self.dtype) if u is None else u
+        v = np.empty(n, self.dtype) if v is None else v
+        check(self._down(self._h, _ptr(u), _ptr(v)))
         return u, v
 
     def download_ptr(self, u_ptr: int, v_ptr: int):
-        check(self._lib.rdcnn_sim_download(self._h, ctypes.c_void_p(u_ptr), ctypes.c_void_p(v_ptr)))
+        check(self._down(self._h, ctypes.c_void_p(u_ptr), ctypes.c_void_p(v_ptr)))
 
     def init(self, typ: int, seed: int):
         check(self._lib.rdcnn_sim_init(self._h, int(typ), ctypes.c_uint64(seed)))
@@ -290,7 +318,8 @@ class StepBuffers:
     def __init__(self, initial: GridState, backend: Optional[Backend] = None):
         be = backend or Backend()
         self.backend = be
-        self.sim = Simulator(initial.rows, initial.cols, 1, be.device, be.mode, be.levels)
+        self.sim = Simulator(initial.rows, initial.cols, 1, be.device, be.mode, be.levels,
+                             precision=initial.precision)
         self.sim.upload(initial.u, initial.v)
         self._rows, self._cols = initial.rows, initial.cols
         self._gene_key = None
@@ -304,7 +333,7 @@ class StepBuffers:
     @property
     def front(self) -> GridState:
         u, v = self.sim.download()
-        return GridState(self._rows, self._cols, u, v)
+        return GridState(self._rows, self._cols, u, v, self.sim.dtype)
 
     def set_front(self, state: GridState):
         self.sim.upload(state.u, state.v)
@@ -404,8 +433,10 @@ class RunOutput:
 def run(cfg: RunConfig, gene: Gene, initial: GridState,
         on_snapshot: Optional[Callable[[int, float], None]] = None) -> RunOutput:
     """engine.hpp:54-94 on the device: state stays resident between snapshots."""
-    if precision_is_double(cfg):
-        raise NotImplementedError("precision=double is not implemented on the cuda backend yet")
+    if cfg.precision not in DTYPES:
+        raise ValueError(f"unknown precision: {cfg.precision}")
+    if (cfg.precision == "double") != (initial.dtype == np.float64):
+        raise ValueError(f"initial state dtype {initial.dtype} does not match precision={cfg.precision}")
     if initial.rows != cfg.nn or initial.cols != cfg.nm:
         raise ValueError("initial state shape does not match config")
     if cfg.nssp < 1 or cfg.nssp > cfg.iter_max or cfg.iter_max % cfg.nssp != 0:
@@ -436,58 +467,62 @@ def run(cfg: RunConfig, gene: Gene, initial: GridState,
         if on_snapshot:
             on_snapshot(done, elapsed)
     out.wall_seconds = time.perf_counter() - t0
-    out.final_state = GridState(cfg.nn, cfg.nm, snaps.frames_u[-1].copy(), snaps.frames_v[-1].copy())
+    out.final_state = GridState(cfg.nn, cfg.nm, snaps.frames_u[-1].copy(), snaps.frames_v[-1].copy(),
+                                initial.dtype)
     return out
-
-
-def precision_is_double(cfg: RunConfig) -> bool:
-    return cfg.precision == "double"
 
 
 # ---------------------------------------------------------------------------
 # Initial states and digest
 # ---------------------------------------------------------------------------
 
-def init_center_square(rows: int, cols: int, seed: int) -> GridState:
-    """typ=1 (init.hpp:34-48)."""
+def init_center_square(rows: int, cols: int, seed: int, precision: str = "single") -> GridState:
+    """typ=1 (init.hpp:34-48), init_center_square<float|double>."""
     if rows < 11 or cols < 11:
         raise ValueError(f"typ=1 needs a grid of at least 11x11, got {rows}x{cols}")
-    s = GridState(rows, cols)
-    check(load().rdcnn_init_center_square_host(rows, cols, ctypes.c_uint64(seed), _ptr(s.u), _ptr(s.v)))
+    s = GridState(rows, cols, dtype=DTYPES[precision])
+    L = load()
+    fn = L.rdcnn_init_center_square_host_f64 if precision == "double" else L.rdcnn_init_center_square_host
+    check(fn(rows, cols, ctypes.c_uint64(seed), _ptr(s.u), _ptr(s.v)))
     return s
 
 
-def init_full_random(rows: int, cols: int, seed: int) -> GridState:
-    """typ=2 (init.hpp:23-30)."""
-    s = GridState(rows, cols)
-    check(load().rdcnn_init_full_random_host(rows, cols, ctypes.c_uint64(seed), _ptr(s.u), _ptr(s.v)))
+def init_full_random(rows: int, cols: int, seed: int, precision: str = "single") -> GridState:
+    """typ=2 (init.hpp:23-30), init_full_random<float|double>."""
+    s = GridState(rows, cols, dtype=DTYPES[precision])
+    L = load()
+    fn = L.rdcnn_init_full_random_host_f64 if precision == "double" else L.rdcnn_init_full_random_host
+    check(fn(rows, cols, ctypes.c_uint64(seed), _ptr(s.u), _ptr(s.v)))
     return s
 
 
-def init_from_image(px: np.ndarray, gene: Gene) -> GridState:
-    """typ=3 (init.hpp:51-64): u = v = float(ka) * float(px/255.0)."""
+def init_from_image(px: np.ndarray, gene: Gene, precision: str = "single") -> GridState:
+    """typ=3 (init.hpp:51-64): u = v = T(ka) * T(px/255.0)."""
     px = np.asarray(px, np.uint8)
     if px.ndim != 2 or px.shape[0] < 3 or px.shape[1] < 3:
         raise ValueError("image must be at least 3x3")
-    x = np.float32(gene.ka) * (px.astype(np.float64) / 255.0).astype(np.float32)
-    return GridState(px.shape[0], px.shape[1], x.reshape(-1), x.reshape(-1).copy())
+    t = DTYPES[precision]
+    x = t(gene.ka) * (px.astype(np.float64) / 255.0).astype(t)
+    return GridState(px.shape[0], px.shape[1], x.reshape(-1), x.reshape(-1).copy(), t)
 
 
 def initial_state(cfg: RunConfig, gene: Gene, image: Optional[np.ndarray] = None) -> GridState:
     if cfg.init_mode == 1:
-        return init_center_square(cfg.nn, cfg.nm, cfg.seed)
+        return init_center_square(cfg.nn, cfg.nm, cfg.seed, cfg.precision)
     if cfg.init_mode == 2:
-        return init_full_random(cfg.nn, cfg.nm, cfg.seed)
+        return init_full_random(cfg.nn, cfg.nm, cfg.seed, cfg.precision)
     if cfg.init_mode == 3:
         if image is None:
             raise ValueError("typ=3 requires an image")
-        return init_from_image(image, gene)
+        return init_from_image(image, gene, cfg.precision)
     raise ValueError("typ must be 1, 2 or 3")
 
 
 def checksum(state: GridState) -> int:
     """FNV-1a 64 over u then v raw bytes (grid.hpp:101-116)."""
-    return int(load().rdcnn_checksum_f32(_ptr(state.u), _ptr(state.v), state.cells()))
+    L = load()
+    fn = L.rdcnn_checksum_f64 if state.dtype == np.float64 else L.rdcnn_checksum_f32
+    return int(fn(_ptr(state.u), _ptr(state.v), state.cells()))
 
 
 def checksum_hex(x: int) -> str:

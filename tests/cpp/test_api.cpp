@@ -268,9 +268,34 @@ void gene_and_metric() {
   CHECK(validate_config(RunConfig{}, Gene{}).empty());
 }
 
+// GridState<double> through the same API (grid.hpp:13-28); digest from the
+// reference itself (tests/golden/golden.json, f64_rand_32x48_s1001_25).
+void double_precision() {
+  auto s = init_full_random<double>(32, 48, 1001);
+  RunConfig cfg;
+  cfg.nn = 32;
+  cfg.nm = 48;
+  cfg.iter_max = 25;
+  cfg.nssp = 5;
+  cfg.precision = Precision::Double;
+  cfg.backend = kCuda;
+  auto out = run(cfg, Gene{}, s);
+  CHECK(checksum_hex(checksum(out.final_state)) == "954a15579afc6def");
+  StepBuffers<double> bufs(s);
+  for (int k = 0; k < 25; ++k) step(bufs, Gene{}, kCuda);
+  CHECK(checksum(bufs.front) == checksum(out.final_state));
+  Gene g;
+  g.dt = 100;
+  long it = 0;
+  StepBuffers<double> b2(init_center_square<double>(16, 16, 42));
+  CHECK(throws_blowup([&] { run_timed(b2, g, kCuda, 1000); }, &it));
+  CHECK(it == 6);  // golden f64_blowup_16_dt100
+}
+
 }  // namespace
 
 int main() {
+  double_precision();
   gene_and_metric();
   kat_criterion1();
   kat_criterion10();

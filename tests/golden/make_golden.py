@@ -44,6 +44,16 @@ CASES = [
 ]
 
 
+CASES_F64 = [
+    ("f64_rand_32x48_s1001_25", 32, 48, 2, 1001, DEFAULT_GENE7, 25),          # test_kernels.cpp:152-156
+    ("f64_kat_256_typ1_s42_1000", 256, 256, 1, 42, DEFAULT_GENE7, 1000),
+    ("f64_rand_17x23_s91_20", 17, 23, 2, 91, DEFAULT_GENE7, 20),
+    ("f64_rand_128_s11_10", 128, 128, 2, 11, DEFAULT_GENE7, 10),              # acceptance 3 (double)
+    ("f64_slow_300x200_typ1_s9_777", 300, 200, 1, 9, SLOW_GROWTH, 777),
+    ("f64_blowup_16_dt100", 16, 16, 1, 42, BLOWUP, 1000),
+]
+
+
 def main():
     ref = Reference()
     out = []
@@ -56,10 +66,20 @@ def main():
                         iters=iters, init_checksum=f"{init_ck:016x}", checksum=f"{ck:016x}",
                         bad_iter=bad, finite=bool(np.isfinite(fu).all() and np.isfinite(fv).all())))
         print(name, out[-1]["checksum"], bad)
+    out64 = []
+    for name, rows, cols, typ, seed, gene, iters in CASES_F64:
+        u, v = ref.init_f64(typ, rows, cols, seed)
+        init_ck = ref.checksum(rows, cols, u, v)
+        fu, fv, bad, _ = ref.run_timed_f64(rows, cols, u, v, iters, gene, backend="reference")
+        ck = ref.checksum(rows, cols, fu, fv)
+        out64.append(dict(name=name, rows=rows, cols=cols, typ=typ, seed=seed, gene7=list(gene),
+                          iters=iters, init_checksum=f"{init_ck:016x}", checksum=f"{ck:016x}",
+                          bad_iter=bad, precision="double"))
+        print(name, out64[-1]["checksum"], bad)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as f:
         json.dump({"generator": "tests/golden/make_golden.py via oracle/_ref (reference headers)",
-                   "cases": out}, f, indent=1)
+                   "cases": out, "cases_f64": out64}, f, indent=1)
 
 
 if __name__ == "__main__":

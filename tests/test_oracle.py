@@ -55,6 +55,21 @@ def test_golden_cases(oracle, golden):
             assert f"{oracle.checksum(u, v):016x}" == c["checksum"], c["name"]
 
 
+def test_golden_cases_f64(oracle):
+    """fp64 digests from the reference (make_params<double>, no narrowing)."""
+    import json
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with open(os.path.join(root, "tests", "golden", "golden.json")) as f:
+        cases = json.load(f)["cases_f64"]
+    for c in cases:
+        u, v = oracle.init_f64(c["typ"], c["rows"], c["cols"], c["seed"])
+        assert f"{oracle.checksum(u, v):016x}" == c["init_checksum"], c["name"]
+        u, v, bad = oracle.run_f64(c["rows"], c["cols"], u, v, c["iters"], c["gene7"])
+        assert bad == c["bad_iter"], c["name"]
+        if bad == 0:
+            assert f"{oracle.checksum(u, v):016x}" == c["checksum"], c["name"]
+
+
 @pytest.mark.skipif(not HAVE_REF, reason="oracle/_ref not built (reference tree absent)")
 def test_oracle_equals_reference_code():
     """The C restatement and the reference headers agree bit for bit, including
