@@ -155,6 +155,27 @@ int rdcnn_slab_rows_ptr(rdcnn_sim_t sim, int which, float** first_row,
 /* Any non-finite value stored so far (1) or not (0); *tag = launch tag. */
 int rdcnn_slab_poll_blowup(rdcnn_sim_t sim, int* bad, unsigned* tag);
 
+/* ---- snapshot store and analysis (batched sweeps, frames) ----------------
+ * Replaces the host-side post-processing of sweep.hpp:48-112 and
+ * frame.hpp:28-66 for device-resident runs.  A handle reserves `nframes`
+ * slots of its u planes (all grids); rdcnn_sim_frame_capture copies the
+ * current u planes into a slot (device to device).  Statistics are per grid
+ * of the batch and exact: min/max, and the median as std::nth_element picks
+ * it (rank floor(n/2)); counts of |double(x) - median| > threshold. */
+int rdcnn_sim_frames_reserve(rdcnn_sim_t sim, int nframes);
+int rdcnn_sim_frame_capture(rdcnn_sim_t sim, int slot);
+/* u planes of all grids of one slot (float or double per precision). */
+int rdcnn_sim_frame_download(rdcnn_sim_t sim, int slot, void* u);
+int rdcnn_sim_frame_stats(rdcnn_sim_t sim, int slot, double* mins, double* maxs,
+                          double* medians);
+int rdcnn_sim_frame_active(rdcnn_sim_t sim, int slot, const double* medians,
+                           const double* thresholds, long long* counts);
+/* normalize_frame(_fixed): 8-bit rows*cols image of grid `grid`'s u plane in
+ * `slot` (slot < 0: the current state), mapping [lo, hi] to 0..255 with
+ * lround and clamping; 128 everywhere when hi <= lo. */
+int rdcnn_sim_frame_normalize(rdcnn_sim_t sim, int slot, int grid, double lo,
+                              double hi, uint8_t* out);
+
 /* ---- host helpers (reference-identical, no device needed) --------------- */
 int rdcnn_init_center_square_host(int rows, int cols, uint64_t seed, float* u,
                                   float* v);

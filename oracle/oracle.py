@@ -196,6 +196,31 @@ class Reference:
             return int(f(rows, cols, _p(np.ascontiguousarray(u)), _p(np.ascontiguousarray(v))))
         return int(self.L.ref_checksum_f32(rows, cols, _p(np.ascontiguousarray(u)), _p(np.ascontiguousarray(v))))
 
+    def sweep_labels(self, x_param, xs, y_param, ys, gene7=DEFAULT_GENE7, ka=1.0, typ=1, nn=32, nm=32,
+                     iter_max=100, nssp=5, seed=42, per_cell_seed=False) -> str:
+        """The reference's sweep_grid labels CSV (sweep.hpp:227-247)."""
+        f = self.L.ref_sweep_labels_f32
+        f.restype = c_int
+        f.argtypes = [ctypes.c_char_p, c_void_p, c_int, ctypes.c_char_p, c_void_p, c_int, c_void_p, c_int,
+                      c_int, c_int, c_long, c_int, c_uint64, c_int, ctypes.c_char_p, c_size_t]
+        xa = np.asarray(xs, np.float64)
+        ya = np.asarray(ys, np.float64)
+        g8 = np.asarray(list(gene7) + [ka], np.float64)
+        buf = ctypes.create_string_buffer(1 << 20)
+        rc = f(x_param.encode(), _p(xa), len(xa), y_param.encode(), _p(ya), len(ya), _p(g8), typ, nn, nm,
+               iter_max, nssp, seed, int(per_cell_seed), buf, len(buf))
+        if rc != 0:
+            raise ValueError("reference sweep_grid rejected the spec")
+        return buf.value.decode()
+
+    def format_double(self, x: float) -> str:
+        f = self.L.ref_format_double
+        f.restype = c_int
+        f.argtypes = [c_double, ctypes.c_char_p, c_size_t]
+        buf = ctypes.create_string_buffer(64)
+        f(x, buf, 64)
+        return buf.value.decode()
+
     def init_f64(self, typ: int, rows: int, cols: int, seed: int):
         u = np.zeros(rows * cols, np.float64)
         v = np.zeros(rows * cols, np.float64)

@@ -16,6 +16,7 @@
 
 #include "rdcnn/engine.hpp"
 #include "rdcnn/init.hpp"
+#include "rdcnn/sweep.hpp"
 
 using namespace rdcnn;
 
@@ -133,6 +134,46 @@ uint64_t ref_checksum_f32(int rows, int cols, const float* u, const float* v) {
 }
 uint64_t ref_checksum_f64(int rows, int cols, const double* u, const double* v) {
   return checksum(make_state<double>(rows, cols, u, v));
+}
+
+// sweep_grid (sweep.hpp:255-326) on a typ 1/2 base config; writes the
+// labels CSV (sweep.hpp:227-247) into out (NUL-terminated).  Returns 0, or
+// 1 on invalid arguments / short buffer.
+int ref_sweep_labels_f32(const char* x_param, const double* xs, int nx, const char* y_param,
+                         const double* ys, int ny, const double g8[8], int typ, int nn, int nm,
+                         long iter_max, int nssp, uint64_t seed, int per_cell_seed, char* out,
+                         size_t cap) {
+  try {
+    SweepSpec spec;
+    spec.x_param = x_param;
+    spec.y_param = y_param;
+    spec.x_values.assign(xs, xs + nx);
+    spec.y_values.assign(ys, ys + ny);
+    spec.base_gene = gene_from(g8);
+    spec.base_config.init_mode = parse_init_mode(typ);
+    spec.base_config.nn = nn;
+    spec.base_config.nm = nm;
+    spec.base_config.iter_max = iter_max;
+    spec.base_config.nssp = nssp;
+    spec.base_config.seed = seed;
+    spec.base_config.backend = make_backend("parallel");
+    spec.per_cell_seed = per_cell_seed != 0;
+    auto res = sweep_grid<float>(spec);
+    if (res.labels_csv.size() + 1 > cap) return 1;
+    std::memcpy(out, res.labels_csv.c_str(), res.labels_csv.size() + 1);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+// std::to_chars shortest form (config.hpp:103-107), for checking the
+// product's labels formatting.
+int ref_format_double(double x, char* out, size_t cap) {
+  std::string s = format_double(x);
+  if (s.size() + 1 > cap) return 1;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return 0;
 }
 
 int ref_max_threads(void) {

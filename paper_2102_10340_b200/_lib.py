@@ -70,6 +70,12 @@ SIGNATURES = {
     "rdcnn_slab_swap": (c_int, [c_void_p]),
     "rdcnn_slab_rows_ptr": (c_int, [c_void_p, c_int, POINTER(c_void_p), POINTER(c_void_p)]),
     "rdcnn_slab_poll_blowup": (c_int, [c_void_p, POINTER(c_int), POINTER(c_uint)]),
+    "rdcnn_sim_frames_reserve": (c_int, [c_void_p, c_int]),
+    "rdcnn_sim_frame_capture": (c_int, [c_void_p, c_int]),
+    "rdcnn_sim_frame_download": (c_int, [c_void_p, c_int, c_void_p]),
+    "rdcnn_sim_frame_stats": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "rdcnn_sim_frame_active": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "rdcnn_sim_frame_normalize": (c_int, [c_void_p, c_int, c_int, c_double, c_double, c_void_p]),
     "rdcnn_init_center_square_host": (c_int, [c_int, c_int, c_uint64, c_void_p, c_void_p]),
     "rdcnn_init_full_random_host": (c_int, [c_int, c_int, c_uint64, c_void_p, c_void_p]),
     "rdcnn_checksum_f32": (c_uint64, [c_void_p, c_void_p, c_size_t]),

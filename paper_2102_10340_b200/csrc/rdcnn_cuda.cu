@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "analysis.cuh"
 #include "fhn_stencil.cuh"
 #include "rdcnn_cuda.h"
 
@@ -359,6 +360,10 @@ struct rdcnn_sim {
   int seg_rows = 0;
   int sm_count = 148;
   unsigned slab_tag = 0;
+  void* frames = nullptr;   // snapshot store: n_frames x batch u-planes
+  int n_frames = 0;
+  double* d_stats = nullptr;        // 3*batch doubles (min, max, median) + batch thresholds
+  long long* d_counts = nullptr;    // batch counts
 
   template <class T>
   T* u_ptr(int b) {
@@ -466,6 +471,9 @@ void free_all(rdcnn_sim* s) {
   if (s->h_flags) cudaFreeHost(s->h_flags);
   if (s->ev0) cudaEventDestroy(s->ev0);
   if (s->ev1) cudaEventDestroy(s->ev1);
+  if (s->frames) cudaFree(s->frames);
+  if (s->d_stats) cudaFree(s->d_stats);
+  if (s->d_counts) cudaFree(s->d_counts);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
 }
@@ -747,6 +755,70 @@ int host_center_square(int rows, int cols, uint64_t seed, T* u, T* v) {
   return RDCNN_OK;
 }
 
+// normalize_frame / normalize_frame_fixed (frame.hpp:28-66): lround of
+// (x - lo) * (255 / (hi - lo)) in double, clamped to 0..255; 128 when hi <= lo.
+template <class T>
+__global__ void normalize_kernel(const T* __restrict__ x, long long n, double lo, double hi,
+                                 uint8_t* __restrict__ out) {
+  const bool flat = !(hi > lo);
+  const double scale = flat ? 0.0 : 255.0 / (hi - lo);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (flat) {
+      out[i] = 128;
+    } else {
+      long long p = llround(__dmul_rn(__dsub_rn((double)x[i], lo), scale));
+      out[i] = (uint8_t)(p < 0 ? 0 : (p > 255 ? 255 : p));
+    }
+  }
+}
+
+template <class T>
+int frame_stats_impl(rdcnn_sim* s, int slot, double* mn, double* mx, double* med) {
+  const long long n = (long long)s->rows * s->cols;
+  const T* base = static_cast<const T*>(s->frames) + (size_t)slot * s->batch * n;
+  double* d = s->d_stats;
+  rdcnn_dev::frame_stats_kernel<T><<<s->batch, rdcnn_dev::kStatThreads, 0, s->stream>>>(
+      base, n, d, d + s->batch, d + 2 * s->batch);
+  RDCNN_CUDA_TRY(cudaGetLastError());
+  const size_t b = sizeof(double) * (size_t)s->batch;
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(mn, d, b, cudaMemcpyDeviceToHost, s->stream));
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(mx, d + s->batch, b, cudaMemcpyDeviceToHost, s->stream));
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(med, d + 2 * s->batch, b, cudaMemcpyDeviceToHost, s->stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RDCNN_OK;
+}
+
+template <class T>
+int frame_active_impl(rdcnn_sim* s, int slot, const double* med, const double* thr, long long* counts) {
+  const long long n = (long long)s->rows * s->cols;
+  const T* base = static_cast<const T*>(s->frames) + (size_t)slot * s->batch * n;
+  double* d = s->d_stats;
+  const size_t b = sizeof(double) * (size_t)s->batch;
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(d + 2 * s->batch, med, b, cudaMemcpyHostToDevice, s->stream));
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(d + 3 * s->batch, thr, b, cudaMemcpyHostToDevice, s->stream));
+  rdcnn_dev::frame_active_kernel<T><<<s->batch, rdcnn_dev::kStatThreads, 0, s->stream>>>(
+      base, n, d + 2 * s->batch, d + 3 * s->batch, s->d_counts);
+  RDCNN_CUDA_TRY(cudaGetLastError());
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(counts, s->d_counts, sizeof(long long) * (size_t)s->batch,
+                                 cudaMemcpyDeviceToHost, s->stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RDCNN_OK;
+}
+
+template <class T>
+int normalize_impl(rdcnn_sim* s, const void* src_dev, double lo, double hi, uint8_t* out) {
+  const long long n = (long long)s->rows * s->cols;
+  uint8_t* d_out = nullptr;
+  RDCNN_CUDA_TRY(cudaMallocAsync(&d_out, (size_t)n, s->stream));
+  normalize_kernel<T><<<4 * s->sm_count, 256, 0, s->stream>>>(static_cast<const T*>(src_dev), n, lo, hi, d_out);
+  RDCNN_CUDA_TRY(cudaGetLastError());
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(out, d_out, (size_t)n, cudaMemcpyDeviceToHost, s->stream));
+  RDCNN_CUDA_TRY(cudaFreeAsync(d_out, s->stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RDCNN_OK;
+}
+
 uint64_t fnv_planes(const void* u, const void* v, size_t bytes) {
   uint64_t h = 0xcbf29ce484222325ull;
   for (const void* plane : {u, v}) {
@@ -989,6 +1061,82 @@ int rdcnn_slab_poll_blowup(rdcnn_sim_t s, int* bad, unsigned* tag) {
   *bad = hv != 0;
   if (tag) *tag = hv;
   return RDCNN_OK;
+}
+
+// ---- snapshot store and analysis (sweep.hpp:48-112, frame.hpp:28-66) ------
+
+int rdcnn_sim_frames_reserve(rdcnn_sim_t s, int nframes) {
+  if (!s || s->slab) return fail(RDCNN_EINVAL, "not a periodic handle");
+  if (nframes < 1) return fail(RDCNN_EINVAL, "nframes must be >= 1");
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  if (s->frames) RDCNN_CUDA_TRY(cudaFree(s->frames));
+  s->frames = nullptr;
+  s->n_frames = 0;
+  const size_t bytes = (size_t)nframes * s->batch * s->rows * s->cols * s->elem;
+  RDCNN_CUDA_TRY(cudaMalloc(&s->frames, bytes));
+  if (!s->d_stats) RDCNN_CUDA_TRY(cudaMalloc(&s->d_stats, sizeof(double) * 4 * (size_t)s->batch));
+  if (!s->d_counts) RDCNN_CUDA_TRY(cudaMalloc(&s->d_counts, sizeof(long long) * (size_t)s->batch));
+  s->n_frames = nframes;
+  return RDCNN_OK;
+}
+
+static int frame_slot_ok(rdcnn_sim_t s, int slot) {
+  if (!s) return fail(RDCNN_EINVAL, "null handle");
+  if (slot < 0 || slot >= s->n_frames)
+    return fail(RDCNN_EINVAL, "frame slot %d outside [0,%d) (rdcnn_sim_frames_reserve)", slot, s->n_frames);
+  return RDCNN_OK;
+}
+
+int rdcnn_sim_frame_capture(rdcnn_sim_t s, int slot) {
+  RDCNN_TRY(frame_slot_ok(s, slot));
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  const size_t bytes = (size_t)s->batch * s->rows * s->cols * s->elem;
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(s->frames) + (size_t)slot * bytes, s->buf[s->cur],
+                                 bytes, cudaMemcpyDeviceToDevice, s->stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RDCNN_OK;
+}
+
+int rdcnn_sim_frame_download(rdcnn_sim_t s, int slot, void* u) {
+  RDCNN_TRY(frame_slot_ok(s, slot));
+  if (!u) return fail(RDCNN_EINVAL, "null argument");
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  const size_t bytes = (size_t)s->batch * s->rows * s->cols * s->elem;
+  RDCNN_CUDA_TRY(cudaMemcpy(u, static_cast<char*>(s->frames) + (size_t)slot * bytes, bytes, cudaMemcpyDeviceToHost));
+  return RDCNN_OK;
+}
+
+int rdcnn_sim_frame_stats(rdcnn_sim_t s, int slot, double* mins, double* maxs, double* medians) {
+  RDCNN_TRY(frame_slot_ok(s, slot));
+  if (!mins || !maxs || !medians) return fail(RDCNN_EINVAL, "null argument");
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  return s->elem == 4 ? frame_stats_impl<float>(s, slot, mins, maxs, medians)
+                      : frame_stats_impl<double>(s, slot, mins, maxs, medians);
+}
+
+int rdcnn_sim_frame_active(rdcnn_sim_t s, int slot, const double* medians, const double* thresholds,
+                           long long* counts) {
+  RDCNN_TRY(frame_slot_ok(s, slot));
+  if (!medians || !thresholds || !counts) return fail(RDCNN_EINVAL, "null argument");
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  return s->elem == 4 ? frame_active_impl<float>(s, slot, medians, thresholds, counts)
+                      : frame_active_impl<double>(s, slot, medians, thresholds, counts);
+}
+
+int rdcnn_sim_frame_normalize(rdcnn_sim_t s, int slot, int grid, double lo, double hi, uint8_t* out) {
+  if (!s || !out) return fail(RDCNN_EINVAL, "null argument");
+  if (grid < 0 || grid >= s->batch) return fail(RDCNN_EINVAL, "grid %d outside the batch", grid);
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  const size_t plane = (size_t)s->rows * s->cols * s->elem;
+  const void* src;
+  if (slot < 0) {  // the current state's u plane
+    if (s->slab) return fail(RDCNN_EINVAL, "not a periodic handle");
+    src = static_cast<const char*>(s->buf[s->cur]) + (size_t)grid * plane;
+  } else {
+    RDCNN_TRY(frame_slot_ok(s, slot));
+    src = static_cast<const char*>(s->frames) + ((size_t)slot * s->batch + grid) * plane;
+  }
+  return s->elem == 4 ? normalize_impl<float>(s, src, lo, hi, out) : normalize_impl<double>(s, src, lo, hi, out);
 }
 
 // ---- host helpers ------------------------------------------------------------

@@ -298,6 +298,38 @@ class Simulator:
         check(self._lib.rdcnn_sim_stream(self._h, ctypes.byref(s)))
         return s.value or 0
 
+    # snapshot store (device-resident frames for batched analysis)
+    def frames_reserve(self, nframes: int):
+        check(self._lib.rdcnn_sim_frames_reserve(self._h, int(nframes)))
+
+    def frame_capture(self, slot: int):
+        check(self._lib.rdcnn_sim_frame_capture(self._h, int(slot)))
+
+    def frame_download(self, slot: int) -> np.ndarray:
+        u = np.empty(self._shape_n(), self.dtype)
+        check(self._lib.rdcnn_sim_frame_download(self._h, int(slot), _ptr(u)))
+        return u
+
+    def frame_stats(self, slot: int):
+        """Per grid: (min, max, median) of the u plane in `slot` (nth_element(n/2))."""
+        mn, mx, med = (np.empty(self.batch, np.float64) for _ in range(3))
+        check(self._lib.rdcnn_sim_frame_stats(self._h, int(slot), _ptr(mn), _ptr(mx), _ptr(med)))
+        return mn, mx, med
+
+    def frame_active(self, slot: int, medians: np.ndarray, thresholds: np.ndarray) -> np.ndarray:
+        med = np.ascontiguousarray(medians, np.float64)
+        thr = np.ascontiguousarray(thresholds, np.float64)
+        out = np.empty(self.batch, np.int64)
+        check(self._lib.rdcnn_sim_frame_active(self._h, int(slot), _ptr(med), _ptr(thr), _ptr(out)))
+        return out
+
+    def frame_normalize(self, slot: int, grid: int, lo: float, hi: float) -> np.ndarray:
+        """normalize_frame(_fixed) on the device; slot < 0 = the current state."""
+        out = np.empty(self.rows * self.cols, np.uint8)
+        check(self._lib.rdcnn_sim_frame_normalize(self._h, int(slot), int(grid), float(lo), float(hi),
+                                                  _ptr(out)))
+        return out.reshape(self.rows, self.cols)
+
     def device_state(self):
         u, v = ctypes.c_void_p(), ctypes.c_void_p()
         check(self._lib.rdcnn_sim_device_state(self._h, ctypes.byref(u), ctypes.byref(v)))

@@ -54,6 +54,16 @@ CASES_F64 = [
 ]
 
 
+# sweep_grid specs (sweep.hpp:255-326); the labels CSV is the golden output.
+SWEEPS = [
+    dict(x_param="du", xs=[0.02, 0.3], y_param="dv", ys=[0.5, 1.0, 5.0], nn=32, nm=32, iter_max=200, nssp=5),
+    dict(x_param="du", xs=[0.3, 0.5, 0.7], y_param="dv", ys=[0.8, 1.0], nn=64, nm=64, iter_max=2000, nssp=5),
+    dict(x_param="a", xs=[-0.3, -0.05], y_param="eps", ys=[-0.1, -0.05], typ=2, nn=40, nm=48, iter_max=100,
+         nssp=4, seed=7, per_cell_seed=True),
+    dict(x_param="a", xs=[-0.05, -0.3], y_param="c", ys=[1.0], nn=128, nm=128, iter_max=3000, nssp=5),
+]
+
+
 def main():
     ref = Reference()
     out = []
@@ -76,10 +86,15 @@ def main():
                           iters=iters, init_checksum=f"{init_ck:016x}", checksum=f"{ck:016x}",
                           bad_iter=bad, precision="double"))
         print(name, out64[-1]["checksum"], bad)
+    sweeps = []
+    for spec in SWEEPS:
+        csv = ref.sweep_labels(**spec)
+        sweeps.append(dict(spec=spec, labels_csv=csv))
+        print("sweep", spec["x_param"], spec["y_param"], csv.count("\n") - 1, "cells")
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as f:
         json.dump({"generator": "tests/golden/make_golden.py via oracle/_ref (reference headers)",
-                   "cases": out, "cases_f64": out64}, f, indent=1)
+                   "cases": out, "cases_f64": out64, "sweeps": sweeps}, f, indent=1)
 
 
 if __name__ == "__main__":
