@@ -29,7 +29,15 @@ def spec_from(d):
 
 def test_format_double_matches_to_chars_examples():
     assert [format_double(x) for x in (0.0, 1.0, 0.02, 0.3, 5.0, -0.05, 1e-5, 1e21, 0.0001, 123456.0)] == \
-        ["0", "1", "0.02", "0.3", "5", "-0.05", "1e-05", "1e+21", "0.0001", "123456"]
+        ["0", "1", "0.02", "0.3", "5", "-0.05", "1e-05", "1e+21", "1e-04", "123456"]
+    try:
+        from oracle.oracle import Reference
+        ref = Reference()
+    except (OSError, FileNotFoundError):
+        return
+    rng = np.random.default_rng(1)
+    vals = list(10.0 ** rng.uniform(-40, 40, 2000)) + list(rng.uniform(-1e3, 1e3, 500))
+    assert [format_double(x) for x in vals] == [ref.format_double(x) for x in vals]
 
 
 def test_sweep_spec_validation():
