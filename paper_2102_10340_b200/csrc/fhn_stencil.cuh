@@ -311,11 +311,19 @@ struct RowCursor {
   }
 };
 
-// Resident CTAs per SM the register budget is capped for (128 threads each):
-// 4 CTAs = 16 warps (<= 128 registers) for fp32 K <= 4 and fp64 K <= 2.
+// One warp per CTA: every per-warp quantity (grid, band, segment, row range,
+// tick count) derives from blockIdx and kernel parameters only, so ptxas can
+// keep the loop control on the uniform datapath.  The warps of a CTA never
+// cooperate, so nothing is lost by not grouping them.
+constexpr int kWarpsPerCta = 1;
+constexpr int kCtaThreads = 32 * kWarpsPerCta;
+
+// Resident warps per SM the register budget is capped for: 16 warps
+// (<= 128 registers) for fp32 K <= 4 and fp64 K <= 2, else 8.
 template <int K, class T>
 struct MinBlocks {
-  static constexpr int value = (sizeof(T) == 4 ? K <= 4 : K <= 2) ? 4 : 2;
+  static constexpr int kWarps = (sizeof(T) == 4 ? K <= 4 : K <= 2) ? 16 : 8;
+  static constexpr int value = kWarps / kWarpsPerCta;
 };
 
 // K levels per launch, W columns per lane, element type T.
@@ -334,12 +342,12 @@ struct MinBlocks {
 // slot j % 3); the tick loop is unrolled by 3 so every slot index is a
 // compile-time constant and no register is copied to advance a window.
 template <int K, int W, class T, bool kFast, bool kPerGrid>
-__global__ void __launch_bounds__(128, MinBlocks<K, T>::value)
+__global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
     fhn_wavefront_kernel(const StepArgsT<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const long long warp_id = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  const int wib = kWarpsPerCta == 1 ? 0 : int(threadIdx.x >> 5);
+  const long long warp_id = (long long)blockIdx.x * kWarpsPerCta + wib;
   const long long per_grid = (long long)a.n_segs * a.n_bands;
   if (warp_id >= per_grid * a.batch) return;
   const int g = int(warp_id / per_grid);

@@ -49,7 +49,7 @@ int fail(int code, const char* fmt, ...) {
     if (rc_ != RDCNN_OK) return rc_; \
   } while (0)
 
-constexpr int kThreads = 128;  // 4 warps per CTA
+constexpr int kThreads = rdcnn_dev::kCtaThreads;  // threads per stencil CTA
 
 // ---------------------------------------------------------------------------
 // Kernel dispatch over the compiled instances.
