@@ -229,12 +229,12 @@ __device__ __forceinline__ int wrap_index(int x, int n) {
 }
 
 // Level-0 rows are staged through a per-warp shared-memory ring with
-// cp.async (LDGSTS; 16-byte copies bypass L1): kStage slots, prefetch
-// distance kStage - 3 ticks.  Each lane copies and later reads back only its
+// cp.async (LDGSTS; 16-byte copies bypass L1): kStage = 6 slots, prefetch
+// distance 3 ticks (thousands of cycles at 16 warps/SM).  Each lane copies and later reads back only its
 // own W columns of each plane, so no cross-lane synchronisation is needed
 // beyond the lane's own cp.async.wait_group.
-constexpr int kStage = 8;
-constexpr int kPrefetch = kStage - 3;
+constexpr int kStage = 6;
+constexpr int kPrefetch = 3;
 
 template <int W, class T>
 __device__ __forceinline__ void stage_row(uint32_t dst, const T* __restrict__ u,
@@ -298,17 +298,6 @@ struct Int {
 template <bool V>
 struct Bool {
   static constexpr bool value = V;
-};
-
-// Running row offset on the torus (periodic) or in the ghosted slab buffer.
-struct RowCursor {
-  size_t off;   // element offset of the current row (row * pitch)
-  size_t step;  // pitch
-  size_t end;   // rows * pitch (periodic) or SIZE_MAX (ghosted: never wraps)
-  __device__ __forceinline__ void next() {
-    off += step;
-    if (off == end) off = 0;
-  }
 };
 
 // One warp per CTA: every per-warp quantity (grid, band, segment, row range,
@@ -387,9 +376,22 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
   const int n_load = h + 2 * K;       // level-0 rows x_0 .. x_{n_load-1}
   const int nt = h + 3 * K - 1;       // ticks until level K has produced h rows
 
-  RowCursor cur{(size_t)(a.periodic ? wrap_index(r0 - K, a.rows) : r0 - K + a.ghost) * pitch, pitch,
-                a.periodic ? (size_t)a.rows * pitch : ~size_t(0)};
-  size_t out_off = (size_t)(a.periodic ? r0 : r0 + a.ghost) * pitch;
+  // Running source row (wraps on the torus; never in ghosted slabs) and
+  // running destination row: pointer increments, no per-tick index math.
+  const int r_first = a.periodic ? wrap_index(r0 - K, a.rows) : r0 - K + a.ghost;
+  const T* su = uin + (size_t)r_first * pitch;
+  const ptrdiff_t vdelta = vin - uin;
+  int rows_left = a.periodic ? a.rows - r_first : 0x7FFFFFFF;
+  const size_t span = (size_t)a.rows * pitch;
+  auto src_next = [&]() {
+    su += pitch;
+    if (--rows_left == 0) {
+      su -= span;
+      rows_left = a.rows;
+    }
+  };
+  T* du = uout + (size_t)(a.periodic ? r0 : r0 + a.ghost) * pitch;
+  const ptrdiff_t vout_delta = vout - uout;
 
   constexpr uint32_t kLaneBytes = uint32_t(sizeof(T)) * W;
   constexpr uint32_t kSlot = 2 * 32 * kLaneBytes;  // bytes of one staged row (u,v)
@@ -400,23 +402,23 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
 #pragma unroll
   for (int d = 0; d < kPrefetch; ++d) {
     if (d < n_load) {
-      stage_row<W, T>(ring + d * kSlot, uin, vin, cur.off);
-      cur.next();
+      stage_row<W, T>(ring + d * kSlot, su, su + vdelta, 0);
+      src_next();
     }
     stage_commit();
   }
 
   Row<W, T> win[K > 1 ? K - 1 : 1][3];
   Finite<T> fin;
-  const uint32_t ring_end = ring + kStage * kSlot;
-  uint32_t at_now = ring;                     // staging slot of tick j
-  uint32_t at_pre = ring + kPrefetch * kSlot; // staging slot of tick j + kPrefetch
-  auto prev_slot = [&](uint32_t x) { return x == ring ? ring_end - kSlot : x - kSlot; };
   const bool store = owner && frozen == 0u;
+  // The 6-slot ring is two halves of 3: tick j lives in slot j % 6, i.e.
+  // slot ph of the half the current 3-tick group uses; the prefetch of tick
+  // j+3 goes to slot ph of the other half.  Both half bases swap once per
+  // group, so every slot address is a base plus a compile-time offset.
+  uint32_t half_now = ring, half_other = ring + 3 * kSlot;
 
   // One tick.  PH = j % 3 (compile-time ring slot); kSteady = every level is
-  // active in this tick, so the validity tests (and the divergence guards
-  // ptxas puts around shuffles under a branch) disappear.
+  // active in this tick, so the validity tests disappear.
   auto tick = [&](auto ph_c, auto steady_c, int j) {
     constexpr int ph = decltype(ph_c)::value;
     constexpr bool kSteady = decltype(steady_c)::value;
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
     // slot ph with its tick-j row.
 #pragma unroll
     for (int t = K; t >= 2; --t) {
-      if (kSteady || (j >= 3 * t - 1 && j < h + 2 * K + t - 1)) {
+      if (kSteady || (j >= 3 * t - 1 && j - (h + 2 * K - 1) < t)) {
         const Row<W, T>& up = win[t - 2][ph];
         const Row<W, T>& ce = win[t - 2][(ph + 1) % 3];
         const Row<W, T>& dn = win[t - 2][(ph + 2) % 3];
@@ -435,42 +437,39 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
           Row<W, T> o;
           level_row<W, T, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
           if (store) {
-            store_row<W, T>(uout, vout, out_off, o);
+            store_row<W, T>(du, du + vout_delta, 0, o);
             fold_finite<W, T>(fin, o);
           }
-          out_off += pitch;
+          du += pitch;
         }
       }
     }
-    // Stage the row of tick j + kPrefetch (an empty group past the end keeps
-    // the wait_group accounting uniform).
+    // Stage the row of tick j + kPrefetch into the slot of tick j - 3 (an
+    // empty group past the end keeps the wait_group accounting uniform).
     if (j + kPrefetch < n_load) {
-      stage_row<W, T>(at_pre, uin, vin, cur.off);
-      cur.next();
+      stage_row<W, T>(half_other + ph * kSlot, su, su + vdelta, 0);
+      src_next();
     }
     stage_commit();
-    at_pre = (at_pre + kSlot == ring_end) ? ring : at_pre + kSlot;
     // Level 1 from the level-0 rows of ticks j-2, j-1, j.
     if (kSteady || (j >= 2 && j < n_load)) {
       stage_wait<kPrefetch>();  // the row of tick j has landed
       Row<W, T> up, ce, dn;
-      const uint32_t at1 = prev_slot(at_now);
-      read_staged<W, T>(prev_slot(at1), up);
-      read_staged<W, T>(at1, ce);
-      read_staged<W, T>(at_now, dn);
+      read_staged<W, T>(ph >= 2 ? half_now + (ph - 2) * kSlot : half_other + (ph + 1) * kSlot, up);
+      read_staged<W, T>(ph >= 1 ? half_now + (ph - 1) * kSlot : half_other + 2 * kSlot, ce);
+      read_staged<W, T>(half_now + ph * kSlot, dn);
       if constexpr (K == 1) {
         Row<W, T> o;
         level_row<W, T, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
         if (store) {
-          store_row<W, T>(uout, vout, out_off, o);
+          store_row<W, T>(du, du + vout_delta, 0, o);
           fold_finite<W, T>(fin, o);
         }
-        out_off += pitch;
+        du += pitch;
       } else {
         level_row<W, T, kFast>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
       }
     }
-    at_now = (at_now + kSlot == ring_end) ? ring : at_now + kSlot;
   };
 
   // Steady ticks: every level active, j in [3K-1, n_load).
@@ -489,6 +488,9 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
       if (j0 + 1 < nt) tick(Int<1>{}, Bool<false>{}, j0 + 1);
       if (j0 + 2 < nt) tick(Int<2>{}, Bool<false>{}, j0 + 2);
     }
+    const uint32_t t_half = half_now;
+    half_now = half_other;
+    half_other = t_half;
   }
   stage_wait<0>();
 
