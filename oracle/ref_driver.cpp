@@ -176,6 +176,53 @@ int ref_format_double(double x, char* out, size_t cap) {
   return 0;
 }
 
+// manifest_text (config.hpp:109-134) for a typ 1/2 config on a named backend.
+int ref_manifest_text(const double g8[8], int typ, int nn, int nm, long iter_max, int nssp,
+                      uint64_t seed, const char* backend, int precision_double, char* out,
+                      size_t cap) {
+  try {
+    RunConfig cfg;
+    cfg.init_mode = parse_init_mode(typ);
+    cfg.nn = nn;
+    cfg.nm = nm;
+    cfg.iter_max = iter_max;
+    cfg.nssp = nssp;
+    cfg.seed = seed;
+    cfg.backend = make_backend(backend);
+    cfg.precision = precision_double ? Precision::Double : Precision::Single;
+    std::string s = manifest_text(gene_from(g8), cfg);
+    if (s.size() + 1 > cap) return 1;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+// write_png / write_pgm (image.hpp:96-174) of a rows x cols 8-bit raster.
+int ref_write_image(const char* path, int rows, int cols, const uint8_t* px, int png) {
+  try {
+    Image8 img{rows, cols, std::vector<uint8_t>(px, px + size_t(rows) * cols)};
+    if (png)
+      write_png(path, img);
+    else
+      write_pgm(path, img);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+// normalize_frame<float> (frame.hpp:28-44) into out; lo/hi returned.
+int ref_normalize_frame_f32(const float* layer, int rows, int cols, uint8_t* out, double* lo,
+                            double* hi) {
+  Frame8 f = normalize_frame(std::span<const float>(layer, size_t(rows) * cols), rows, cols);
+  std::memcpy(out, f.px.data(), f.px.size());
+  *lo = f.lo;
+  *hi = f.hi;
+  return 0;
+}
+
 int ref_max_threads(void) {
 #if defined(_OPENMP)
   return omp_get_max_threads();
