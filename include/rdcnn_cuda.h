@@ -155,6 +155,23 @@ int rdcnn_slab_rows_ptr(rdcnn_sim_t sim, int which, float** first_row,
 /* Any non-finite value stored so far (1) or not (0); *tag = launch tag. */
 int rdcnn_slab_poll_blowup(rdcnn_sim_t sim, int* bad, unsigned* tag);
 
+/* Native ring (no host work per block).  Rank 0 calls rdcnn_nccl_unique_id
+ * and shares the 128 bytes with every rank (e.g. a torch.distributed
+ * broadcast); each rank then attaches its slab.  world == 1 closes the ring
+ * on itself (the torus row wrap as two device copies, no NCCL).  NCCL is
+ * resolved at run time from the libnccl.so.2 already in the process. */
+int rdcnn_nccl_unique_id(uint8_t id[128]);
+int rdcnn_slab_attach_ring(rdcnn_sim_t sim, const uint8_t id[128], int rank,
+                           int world);
+/* Exchange the front buffer's edge rows into the ring's ghosts (once, after
+ * initialising the slabs). */
+int rdcnn_slab_fill_ghosts(rdcnn_sim_t sim);
+/* Advance by `steps`: per block of k <= ghost levels, boundary kernel ->
+ * NCCL ring exchange on a comm stream overlapped with the interior kernel.
+ * On a non-finite value returns RDCNN_EBLOWUP with *first_bad = the first
+ * iteration of the first bad block (block granularity). */
+int rdcnn_slab_advance(rdcnn_sim_t sim, long steps, long* first_bad);
+
 /* ---- snapshot store and analysis (batched sweeps, frames) ----------------
  * Replaces the host-side post-processing of sweep.hpp:48-112 and
  * frame.hpp:28-66 for device-resident runs.  A handle reserves `nframes`

@@ -70,6 +70,10 @@ SIGNATURES = {
     "rdcnn_slab_swap": (c_int, [c_void_p]),
     "rdcnn_slab_rows_ptr": (c_int, [c_void_p, c_int, POINTER(c_void_p), POINTER(c_void_p)]),
     "rdcnn_slab_poll_blowup": (c_int, [c_void_p, POINTER(c_int), POINTER(c_uint)]),
+    "rdcnn_nccl_unique_id": (c_int, [c_void_p]),
+    "rdcnn_slab_attach_ring": (c_int, [c_void_p, c_void_p, c_int, c_int]),
+    "rdcnn_slab_fill_ghosts": (c_int, [c_void_p]),
+    "rdcnn_slab_advance": (c_int, [c_void_p, c_long, POINTER(c_long)]),
     "rdcnn_sim_frames_reserve": (c_int, [c_void_p, c_int]),
     "rdcnn_sim_frame_capture": (c_int, [c_void_p, c_int]),
     "rdcnn_sim_frame_download": (c_int, [c_void_p, c_int, c_void_p]),

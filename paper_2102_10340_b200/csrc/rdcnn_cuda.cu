@@ -15,6 +15,9 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "analysis.cuh"
 #include "fhn_stencil.cuh"
 #include "rdcnn_cuda.h"
@@ -323,6 +326,49 @@ __global__ void div3_selftest_f64_kernel(unsigned long long samples, unsigned lo
   }
 }
 
+// NCCL, resolved at run time from whichever libnccl.so.2 the process already
+// has (torch's) or the system one, so the library carries no link-time NCCL
+// dependency and single-GPU users never load it.
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_unique_id = (decltype(a.get_unique_id))dlsym(h, "ncclGetUniqueId");
+    a.comm_init_rank = (decltype(a.comm_init_rank))dlsym(h, "ncclCommInitRank");
+    a.comm_destroy = (decltype(a.comm_destroy))dlsym(h, "ncclCommDestroy");
+    a.send = (decltype(a.send))dlsym(h, "ncclSend");
+    a.recv = (decltype(a.recv))dlsym(h, "ncclRecv");
+    a.group_start = (decltype(a.group_start))dlsym(h, "ncclGroupStart");
+    a.group_end = (decltype(a.group_end))dlsym(h, "ncclGroupEnd");
+    a.error_string = (decltype(a.error_string))dlsym(h, "ncclGetErrorString");
+    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.send && a.recv && a.group_start &&
+           a.group_end && a.error_string;
+    return a;
+  }();
+  return api;
+}
+
+#define RDCNN_NCCL_TRY(expr)                                                          \
+  do {                                                                                \
+    ncclResult_t r_ = (expr);                                                         \
+    if (r_ != ncclSuccess)                                                            \
+      return fail(RDCNN_ECUDA, "%s failed: %s", #expr, nccl().error_string(r_));     \
+  } while (0)
+
 int sm_count_for(int device) {
   int n = 0;
   if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) n = 148;
@@ -360,6 +406,11 @@ struct rdcnn_sim {
   int seg_rows = 0;
   int sm_count = 148;
   unsigned slab_tag = 0;
+  // slab ring (native multi-GPU path)
+  ncclComm_t comm = nullptr;
+  int ring_rank = 0, ring_world = 1;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_bnd = nullptr, ev_xchg = nullptr;
   void* frames = nullptr;   // snapshot store: n_frames x batch u-planes
   int n_frames = 0;
   double* d_stats = nullptr;        // 3*batch doubles (min, max, median) + batch thresholds
@@ -471,6 +522,10 @@ void free_all(rdcnn_sim* s) {
   if (s->h_flags) cudaFreeHost(s->h_flags);
   if (s->ev0) cudaEventDestroy(s->ev0);
   if (s->ev1) cudaEventDestroy(s->ev1);
+  if (s->comm) nccl().comm_destroy(s->comm);
+  if (s->comm_stream) cudaStreamDestroy(s->comm_stream);
+  if (s->ev_bnd) cudaEventDestroy(s->ev_bnd);
+  if (s->ev_xchg) cudaEventDestroy(s->ev_xchg);
   if (s->frames) cudaFree(s->frames);
   if (s->d_stats) cudaFree(s->d_stats);
   if (s->d_counts) cudaFree(s->d_counts);
@@ -1060,6 +1115,120 @@ int rdcnn_slab_poll_blowup(rdcnn_sim_t s, int* bad, unsigned* tag) {
   RDCNN_CUDA_TRY(cudaMemcpy(&hv, s->d_flags, sizeof hv, cudaMemcpyDeviceToHost));
   *bad = hv != 0;
   if (tag) *tag = hv;
+  return RDCNN_OK;
+}
+
+// ---- native slab ring: NCCL halo exchange overlapped with the interior -------
+
+int rdcnn_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return fail(RDCNN_EINVAL, "null argument");
+  if (!nccl().ok) return fail(RDCNN_ECUDA, "libnccl.so.2 not loadable");
+  ncclUniqueId uid;
+  RDCNN_NCCL_TRY(nccl().get_unique_id(&uid));
+  std::memcpy(id, &uid, sizeof uid);
+  return RDCNN_OK;
+}
+
+int rdcnn_slab_attach_ring(rdcnn_sim_t s, const uint8_t id[128], int rank, int world) {
+  if (!s || !s->slab) return fail(RDCNN_EINVAL, "not a slab handle");
+  if (world < 1 || rank < 0 || rank >= world) return fail(RDCNN_EINVAL, "bad rank %d / world %d", rank, world);
+  if (s->comm_stream) return fail(RDCNN_EINVAL, "ring already attached");
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  RDCNN_CUDA_TRY(cudaStreamCreateWithFlags(&s->comm_stream, cudaStreamNonBlocking));
+  RDCNN_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_bnd, cudaEventDisableTiming));
+  RDCNN_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_xchg, cudaEventDisableTiming));
+  s->ring_rank = rank;
+  s->ring_world = world;
+  if (world > 1) {
+    if (!id) return fail(RDCNN_EINVAL, "null NCCL id");
+    if (!nccl().ok) return fail(RDCNN_ECUDA, "libnccl.so.2 not loadable");
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof uid);
+    RDCNN_NCCL_TRY(nccl().comm_init_rank(&s->comm, world, uid, rank));
+  }
+  return RDCNN_OK;
+}
+
+// The ring exchange of buffer `b`: its first `ghost` owned rows go to the
+// previous rank (its bottom ghosts), its last `ghost` rows to the next rank
+// (its top ghosts).  Issue order matches paper_2102_10340_b200/slab.py
+// exchange_ops (tested with gloo): send last -> next, send first -> prev,
+// recv top <- prev, recv bottom <- next, so sends and receives between one
+// pair pair up in order even when prev == next (world 2).  World 1 closes the
+// ring on itself: the torus row wrap is two device copies.
+static int ring_exchange(rdcnn_sim* s, int b, cudaStream_t st) {
+  float* base = s->u_ptr<float>(b);  // first top-ghost row
+  const size_t row = (size_t)s->pitch, g = (size_t)s->ghost, S = (size_t)s->rows;
+  float* first = base + g * row;
+  float* last = base + S * row;  // owned rows [S-g, S)
+  float* top = base;
+  float* bottom = base + (g + S) * row;
+  const size_t count = g * row;
+  if (s->ring_world == 1) {
+    RDCNN_CUDA_TRY(cudaMemcpyAsync(top, last, count * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    RDCNN_CUDA_TRY(cudaMemcpyAsync(bottom, first, count * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    return RDCNN_OK;
+  }
+  const int prev = (s->ring_rank + s->ring_world - 1) % s->ring_world;
+  const int next = (s->ring_rank + 1) % s->ring_world;
+  RDCNN_NCCL_TRY(nccl().group_start());
+  RDCNN_NCCL_TRY(nccl().send(last, count, ncclFloat32, next, s->comm, st));
+  RDCNN_NCCL_TRY(nccl().send(first, count, ncclFloat32, prev, s->comm, st));
+  RDCNN_NCCL_TRY(nccl().recv(top, count, ncclFloat32, prev, s->comm, st));
+  RDCNN_NCCL_TRY(nccl().recv(bottom, count, ncclFloat32, next, s->comm, st));
+  RDCNN_NCCL_TRY(nccl().group_end());
+  return RDCNN_OK;
+}
+
+int rdcnn_slab_fill_ghosts(rdcnn_sim_t s) {
+  if (!s || !s->slab || !s->comm_stream) return fail(RDCNN_EINVAL, "slab ring not attached");
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  RDCNN_TRY(ring_exchange(s, s->cur, s->comm_stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->comm_stream));
+  return RDCNN_OK;
+}
+
+// Per block of k <= ghost levels: boundary rows (they read the ghosts) on the
+// compute stream; the ring exchange of those rows on the comm stream, which
+// waits only for the boundary launch; the interior on the compute stream at
+// the same time; then the compute stream waits for the exchange and the
+// buffers swap.  No host synchronisation inside the loop.
+int rdcnn_slab_advance(rdcnn_sim_t s, long steps, long* first_bad) {
+  if (!s || !s->slab || !s->comm_stream) return fail(RDCNN_EINVAL, "slab ring not attached");
+  if (steps < 0) return fail(RDCNN_EINVAL, "steps must be >= 0");
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  if (first_bad) *first_bad = 0;
+  s->launches = 0;
+  s->slab_tag = 0;
+  RDCNN_CUDA_TRY(cudaMemsetAsync(s->d_flags, 0, sizeof(unsigned), s->stream));
+  const Schedule sched = make_schedule(steps, s->max_levels);
+  RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
+  for (long n = 0; n < sched.count(); ++n) {
+    const int k = sched.depth(n);
+    RDCNN_TRY(slab_step_impl<float>(s, k, s->stream, true));
+    RDCNN_CUDA_TRY(cudaEventRecord(s->ev_bnd, s->stream));
+    RDCNN_CUDA_TRY(cudaStreamWaitEvent(s->comm_stream, s->ev_bnd, 0));
+    RDCNN_TRY(ring_exchange(s, s->cur ^ 1, s->comm_stream));
+    RDCNN_TRY(slab_step_impl<float>(s, k, s->stream, false));
+    RDCNN_CUDA_TRY(cudaEventRecord(s->ev_xchg, s->comm_stream));
+    RDCNN_CUDA_TRY(cudaStreamWaitEvent(s->stream, s->ev_xchg, 0));
+    s->cur ^= 1;
+  }
+  RDCNN_CUDA_TRY(cudaEventRecord(s->ev1, s->stream));
+  unsigned tag = 0;
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(s->h_flags, s->d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, s->stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  tag = s->h_flags[0];
+  float ms = 0;
+  RDCNN_CUDA_TRY(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+  s->last_ms = ms;
+  if (tag != 0) {
+    // Block granularity: a slab cannot replay alone (its neighbours moved on),
+    // so the report is the first iteration of the first bad block.
+    if (first_bad) *first_bad = sched.start((long)tag - 1) + 1;
+    return fail(RDCNN_EBLOWUP, "blow-up: non-finite state in block %u", tag);
+  }
   return RDCNN_OK;
 }
 

@@ -76,7 +76,11 @@ class SlabStepper:
 
     def __init__(self, global_rows: int, cols: int, rank: int, world: int, ghost: int = 4,
                  device: int = 0, mode: str = "strict",
-                 exchange: Optional[Callable] = None, seg_rows: int = 0):
+                 exchange: Optional[Callable] = None, seg_rows: int = 0, native: Optional[bool] = None):
+        """``native`` (default: True unless a Python ``exchange`` is given)
+        runs the whole block loop in the C-ABI (rdcnn_slab_advance: NCCL ring
+        on a comm stream, no host work per block); otherwise each block is
+        driven from Python with ``exchange`` (the gloo-testable path)."""
         if global_rows % world:
             raise ValueError(f"global rows {global_rows} not divisible by world size {world}")
         self._lib = load()
@@ -84,6 +88,7 @@ class SlabStepper:
         self.rows = global_rows // world
         self.ghost = ghost
         self.device = device
+        self.native = (exchange is None) if native is None else native
         self.exchange = exchange or exchange_halos
         h = ctypes.c_void_p()
         m = RDCNN_FAST if mode == "fast" else RDCNN_STRICT
@@ -91,6 +96,30 @@ class SlabStepper:
         self._h = h
         check(self._lib.rdcnn_sim_set_tuning(self._h, ghost, seg_rows))
         self.launches = 0
+        if self.native:
+            self._attach_ring()
+
+    def _attach_ring(self):
+        """NCCL communicator for the ring (id from rank 0, shared through
+        torch.distributed); world 1 needs none."""
+        uid = (ctypes.c_uint8 * 128)()
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            if self.rank == 0:
+                check(self._lib.rdcnn_nccl_unique_id(uid))
+            on_gpu = dist.get_backend() == "nccl"
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8,
+                             device=f"cuda:{self.device}" if on_gpu else "cpu")
+            dist.broadcast(t, src=0)
+            for k, b in enumerate(t.cpu().tolist()):
+                uid[k] = b
+        check(self._lib.rdcnn_slab_attach_ring(self._h, uid, self.rank, self.world))
+
+    def elapsed_ms(self) -> float:
+        ms = ctypes.c_double()
+        check(self._lib.rdcnn_sim_elapsed_ms(self._h, ctypes.byref(ms)))
+        return ms.value
 
     def close(self):
         if getattr(self, "_h", None):
@@ -147,15 +176,27 @@ class SlabStepper:
         """Exchange the front buffer's edge rows (before the first block)."""
         import torch
 
+        if self.native:
+            check(self._lib.rdcnn_slab_fill_ghosts(self._h))
+            return
         works = self.exchange(*self._views(0), self.rank, self.world)
         for w in works:
             w.wait()
         torch.cuda.current_stream(self.device).synchronize()
 
     def advance(self, steps: int, stream=None):
-        """Advance by `steps` iterations in blocks of <= ghost levels."""
+        """Advance by `steps` iterations in blocks of <= ghost levels.
+        Returns the first iteration of the first block that produced a
+        non-finite value (0 = none; native path only)."""
         import torch
 
+        if self.native:
+            bad = ctypes.c_long()
+            check(self._lib.rdcnn_slab_advance(self._h, int(steps), ctypes.byref(bad)))
+            n = ctypes.c_long()
+            check(self._lib.rdcnn_sim_launch_count(self._h, ctypes.byref(n)))
+            self.launches += n.value
+            return bad.value
         st = stream or torch.cuda.current_stream(self.device)
         sp = ctypes.c_void_p(st.cuda_stream)
         done = 0
