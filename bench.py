@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="budget of the cpu_baseline sample on rank 0")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slab", action="store_true",
+                    help="run the multi-GPU slab path even at N=1 (a world-1 ring)")
     return ap.parse_args()
 
 
@@ -226,7 +228,7 @@ def bench_ours(args, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     launches = 0
-    if world == 1:
+    if world == 1 and not args.slab:
         sim = fhn.Simulator(n, n, device=local_rank, mode=args.mode, levels=args.levels,
                             seg_rows=args.seg_rows)
         sim.set_params(gene)
@@ -262,24 +264,27 @@ def bench_ours(args, rank, world, local_rank):
         for _ in range(args.warmup):
             slab.advance(S)
         torch.cuda.synchronize()
-        dist.barrier()
+        if dist is not None:
+            dist.barrier()
         with ClockSampler(local_rank) as clocks:
             ev0 = torch.cuda.Event(enable_timing=True)
             ev1 = torch.cuda.Event(enable_timing=True)
             l0 = slab.launches
             ev0.record(stream)
+            bad = 0
             for _ in range(args.steps):
-                slab.advance(S)
+                bad = bad or slab.advance(S)
             ev1.record(stream)
             torch.cuda.synchronize()
             launches = slab.launches - l0
-        dist.barrier()
         t = torch.tensor([ev0.elapsed_time(ev1)], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if dist is not None:
+            dist.barrier()
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
         cells_global = rows_global * n
-        if slab.blew_up():
-            raise RuntimeError("blow-up in slab run")
+        if bad:
+            raise RuntimeError(f"blow-up in slab run near iteration {bad}")
 
     total_updates = cells_global * S * args.steps
     value = total_updates / (t_ms / 1e3) / 1e6
@@ -316,7 +321,7 @@ def bench_ours(args, rank, world, local_rank):
 
     # ---- end to end through the public API with host buffers (N=1 only) ----
     e2e = None
-    if world == 1:
+    if world == 1 and not args.slab:
         u_h = torch.empty(n * n, dtype=torch.float32).pin_memory()
         v_h = torch.empty(n * n, dtype=torch.float32).pin_memory()
         sim.download_ptr(u_h.data_ptr(), v_h.data_ptr())
