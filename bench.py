@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slab", action="store_true",
                     help="run the multi-GPU slab path even at N=1 (a world-1 ring)")
+    ap.add_argument("--transport", default="p2p", choices=("p2p", "nccl"),
+                    help="slab halo exchange: fused peer stores in the step kernel, or NCCL")
     return ap.parse_args()
 
 
@@ -254,7 +256,7 @@ def bench_ours(args, rank, world, local_rank):
         from paper_2102_10340_b200.slab import SlabStepper
         rows_global = n * world
         slab = SlabStepper(rows_global, n, rank, world, ghost=args.levels, device=local_rank,
-                           mode=args.mode, seg_rows=args.seg_rows)
+                           mode=args.mode, seg_rows=args.seg_rows, transport=args.transport)
         slab.set_params(gene)
         slab.init(1, 42)
         slab.fill_ghosts()
@@ -294,7 +296,7 @@ def bench_ours(args, rank, world, local_rank):
     peaks, peak_kind = measured_peaks()
     per_rank_cells = n * n
     launches_per_rank = max(launches, 1)
-    if world > 1:
+    if (world > 1 or args.slab) and args.transport == "nccl":
         # 3 launches per block (two boundary strips + interior); the interior
         # carries ~all the work, so the per-block time is the launch figure
         launches_per_rank = max(launches // 3, 1)
@@ -343,6 +345,35 @@ def bench_ours(args, rank, world, local_rank):
         un = u_h.numpy()
         if not np.isfinite(un).all():
             raise RuntimeError("non-finite state after e2e")
+    else:
+        # Slab path: every rank uploads its slab from pinned host memory,
+        # refills the ring's ghosts, advances, downloads; max over ranks.
+        lib = fhn.load()
+        cells = slab.rows * n
+        u_h = torch.empty(cells, dtype=torch.float32).pin_memory()
+        v_h = torch.empty(cells, dtype=torch.float32).pin_memory()
+        fhn._lib.check(lib.rdcnn_sim_download(slab._h, u_h.data_ptr(), v_h.data_ptr()))
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            fhn._lib.check(lib.rdcnn_sim_upload(slab._h, u_h.data_ptr(), v_h.data_ptr()))
+            slab.fill_ghosts()
+            bad = slab.advance(S)
+            fhn._lib.check(lib.rdcnn_sim_download(slab._h, u_h.data_ptr(), v_h.data_ptr()))
+            if bad:
+                raise RuntimeError(f"blow-up in e2e slab run near iteration {bad}")
+        torch.cuda.synchronize()
+        te = torch.tensor([time.perf_counter() - t0], device="cuda")
+        if dist is not None:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        e2e = {"value": round(cells * world * S * args.e2e_steps / e2e_s / 1e6, 2),
+               "unit": "Mcell-updates/s", "h2d_bytes_per_step": 2 * 4 * cells * world,
+               "d2h_bytes_per_step": 2 * 4 * cells * world,
+               "path": "per rank: rdcnn_sim_upload (pinned host) -> rdcnn_slab_fill_ghosts -> "
+                       "rdcnn_slab_advance -> rdcnn_sim_download; max wall time over ranks",
+               "steps": args.e2e_steps}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -361,11 +392,14 @@ def bench_ours(args, rank, world, local_rank):
             "config": {
                 "workload": (f"cfg2: FHN RD-CNN {n}x{n} fp32 torus per GPU, typ=1 seed 42, "
                              f"slow-growth gene a=-0.05, {S} iterations per step"
-                             + (f"; global {n * world}x{n} row-slabbed, NCCL halo exchange"
-                                if world > 1 else "")),
+                             + (f"; global {n * world}x{n} row-slabbed, halo exchange: "
+                                + ("fused peer stores in the step kernel" if args.transport == "p2p"
+                                   else "NCCL send/recv overlapped with the interior kernel")
+                                if world > 1 or args.slab else "")),
                 "rows": n * world, "cols": n, "iterations_per_step": S, "levels_per_launch": levels,
                 "mode": args.mode, "l2": "state 256 MiB/GPU > 126 MB L2 (no flush needed)",
-                "parallelism": f"slab{world}" if world > 1 else "single",
+                "parallelism": f"slab{world}" if world > 1 or args.slab else "single",
+                **({"transport": args.transport} if world > 1 or args.slab else {}),
             },
             "roofline": roofline,
             "cpu_baseline": cpu,

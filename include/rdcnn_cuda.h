@@ -164,13 +164,45 @@ int rdcnn_nccl_unique_id(uint8_t id[128]);
 int rdcnn_slab_attach_ring(rdcnn_sim_t sim, const uint8_t id[128], int rank,
                            int world);
 /* Exchange the front buffer's edge rows into the ring's ghosts (once, after
- * initialising the slabs). */
+ * initialising the slabs; NCCL ring or peer ring). */
 int rdcnn_slab_fill_ghosts(rdcnn_sim_t sim);
-/* Advance by `steps`: per block of k <= ghost levels, boundary kernel ->
- * NCCL ring exchange on a comm stream overlapped with the interior kernel.
+/* Advance by `steps`.  Peer ring: one fused launch per block of k <= ghost
+ * levels.  NCCL ring: per block, boundary kernel -> NCCL ring exchange on a
+ * comm stream overlapped with the interior kernel.
  * On a non-finite value returns RDCNN_EBLOWUP with *first_bad = the first
  * iteration of the first bad block (block granularity). */
 int rdcnn_slab_advance(rdcnn_sim_t sim, long steps, long* first_bad);
+
+/* Fused peer ring (the default multi-GPU transport): the halo exchange runs
+ * INSIDE the step kernel.  Per block, one launch computes every owned row;
+ * the warps producing the first/last `ghost` rows also store them straight
+ * into the ring neighbours' ghost rows (peer memory: CUDA IPC mappings over
+ * NVLink, or plain pointers when the neighbour lives in the same process),
+ * then publish a per-direction "delivered" word with a release store; the
+ * neighbours' edge warps acquire it before reading their ghosts.  No NCCL,
+ * no exchange copies, no host work per block.
+ *
+ * Protocol: every rank exports its descriptor, the descriptors are shared
+ * (e.g. torch.distributed all_gather_object), every rank attaches with its
+ * ring neighbours' descriptors (prev = rank-1, next = rank+1 mod world; world
+ * 1 passes its own), calls rdcnn_slab_fill_ghosts, and the ranks barrier once
+ * before the first block.  All ranks must then run the same blocks.  Destroy
+ * only after a barrier (neighbours write into this slab's ghost rows). */
+typedef struct {
+  uint8_t ipc[3][64];   /* cudaIpcMemHandle_t: buffer 0, buffer 1, sync words */
+  uint64_t ptr[3];      /* the same allocations as device pointers (exporter's process) */
+  int64_t pid;          /* exporting process */
+  int32_t device, rows, cols, ghost;
+  int32_t ipc_ok;       /* 0: IPC export failed (in-process rings only) */
+} rdcnn_slab_peer_desc;
+int rdcnn_slab_peer_export(rdcnn_sim_t sim, rdcnn_slab_peer_desc* out);
+int rdcnn_slab_attach_peers(rdcnn_sim_t sim, int rank, int world,
+                            const rdcnn_slab_peer_desc* prev,
+                            const rdcnn_slab_peer_desc* next);
+/* One fused block of k levels on `stream` (NULL: the handle's stream); for
+ * drivers that interleave several in-process ranks on one stream.  The ring
+ * must have been filled (rdcnn_slab_fill_ghosts). */
+int rdcnn_slab_step_fused(rdcnn_sim_t sim, int k, void* stream);
 
 /* ---- snapshot store and analysis (batched sweeps, frames) ----------------
  * Replaces the host-side post-processing of sweep.hpp:48-112 and

@@ -5,7 +5,7 @@ include/rdcnn_cuda.h; this package is its Python host side (a mirror of the
 reference's C++ API, see :mod:`.engine`) plus the multi-GPU slab driver
 (:mod:`.slab`).
 """
-from ._lib import LIB_PATH, LibraryMissing, RdcnnError, load  # noqa: F401
+from ._lib import LIB_PATH, LibraryMissing, RdcnnError, last_error, load  # noqa: F401
 from .engine import (  # noqa: F401
     Backend, BlowUpError, Gene, GridState, RunConfig, RunOutput, ScheduleError, Simulator,
     SnapshotBuffer, StepBuffers, checksum, checksum_hex, gene_valid, init_center_square,

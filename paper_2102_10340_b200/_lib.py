@@ -35,6 +35,15 @@ class ParamsF64(ctypes.Structure):
     _fields_ = [(n, c_double) for n in ("dt", "a", "b", "eps", "c", "du", "dv")]
 
 
+class PeerDesc(ctypes.Structure):
+    """rdcnn_slab_peer_desc: one slab's exported peer memory (IPC handles +
+    in-process pointers) for the fused peer ring."""
+
+    _fields_ = [("ipc", (ctypes.c_uint8 * 64) * 3), ("ptr", c_uint64 * 3), ("pid", ctypes.c_int64),
+                ("device", ctypes.c_int32), ("rows", ctypes.c_int32), ("cols", ctypes.c_int32),
+                ("ghost", ctypes.c_int32), ("ipc_ok", ctypes.c_int32)]
+
+
 # name -> (restype, argtypes); exactly the symbols include/rdcnn_cuda.h declares.
 SIGNATURES = {
     "rdcnn_abi_version": (c_int, []),
@@ -74,6 +83,9 @@ SIGNATURES = {
     "rdcnn_slab_attach_ring": (c_int, [c_void_p, c_void_p, c_int, c_int]),
     "rdcnn_slab_fill_ghosts": (c_int, [c_void_p]),
     "rdcnn_slab_advance": (c_int, [c_void_p, c_long, POINTER(c_long)]),
+    "rdcnn_slab_peer_export": (c_int, [c_void_p, POINTER(PeerDesc)]),
+    "rdcnn_slab_attach_peers": (c_int, [c_void_p, c_int, c_int, POINTER(PeerDesc), POINTER(PeerDesc)]),
+    "rdcnn_slab_step_fused": (c_int, [c_void_p, c_int, c_void_p]),
     "rdcnn_sim_frames_reserve": (c_int, [c_void_p, c_int]),
     "rdcnn_sim_frame_capture": (c_int, [c_void_p, c_int]),
     "rdcnn_sim_frame_download": (c_int, [c_void_p, c_int, c_void_p]),

@@ -68,6 +68,19 @@ struct StepArgsT {
   int params_stride;      // 0: one gene for all grids; 1: one per grid
   unsigned* flags;        // per grid: 0 clean, else tag of the first bad launch
   unsigned tag;           // this launch's tag (launch index + 1)
+  // Fused peer halo exchange (kPeer instances, slab mode only).
+  // Level-K edge rows are also stored straight into the ring neighbours'
+  // ghost rows of THEIR output buffer (peer memory: CUDA IPC over NVLink, or
+  // the same device), and the edge warps signal completion with one release
+  // store per block and direction.
+  T* peer_top;            // prev rank's bottom ghost row 0 (receives owned row 0)
+  T* peer_bot;            // next rank's top ghost row 0 (receives owned row rows-ghost)
+  unsigned* edge_count;   // [2] this rank's completion counters: top / bottom edge warps
+  unsigned* sig_prev;     // prev rank's "bottom ghosts delivered" word
+  unsigned* sig_next;     // next rank's "top ghosts delivered" word
+  const unsigned* ready;  // [2] this rank's "top / bottom ghosts delivered" words
+  unsigned seq;           // block number: this block's ghosts are in when ready[] >= seq
+  int n_top, n_bot;       // warps whose segment touches the top / bottom `ghost` rows
 };
 using StepArgs = StepArgsT<float>;
 
@@ -285,6 +298,30 @@ __device__ __forceinline__ void read_staged(uint32_t src, Row<W, T>& r) {
   }
 }
 
+// ---- peer ring synchronisation (kPeer) --------------------------------------
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// Wait until *p >= seq (wrap-safe).  Every lane polls, so every lane's later
+// reads of the ghost rows are ordered after its own acquire.
+__device__ __forceinline__ void wait_ready(const unsigned* p, unsigned seq) {
+  while ((int)(ld_acquire_sys(p) - seq) < 0) __nanosleep(128);
+}
+// Called by lane 0 of an edge warp after every lane's peer stores were
+// fenced: the last of `n` warps resets the counter and publishes `val`.
+__device__ __forceinline__ void edge_done(unsigned* count, int n, unsigned* sig, unsigned val) {
+  if (atomicAdd(count, 1u) == unsigned(n - 1)) {
+    atomicExch(count, 0u);
+    __threadfence_system();
+    st_release_sys(sig, val);
+  }
+}
+
 // Shared memory per CTA of the wavefront kernel.
 template <int W, class T>
 constexpr int wavefront_smem_bytes(int warps) {
@@ -330,7 +367,12 @@ struct MinBlocks {
 // Register rotation: level-t rows (t = 1..K-1) live in rings of 3 (tick j ->
 // slot j % 3); the tick loop is unrolled by 3 so every slot index is a
 // compile-time constant and no register is copied to advance a window.
-template <int K, int W, class T, bool kFast, bool kPerGrid>
+//
+// kPeer (slab mode): the launch covers every owned row of the slab; warps
+// whose segment reads ghost rows first wait for the neighbour's "delivered"
+// word, store their edge rows into the neighbour's ghosts as well as locally,
+// and publish completion -- the halo exchange is fused into the step.
+template <int K, int W, class T, bool kFast, bool kPerGrid, bool kPeer = false>
 __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
     fhn_wavefront_kernel(const StepArgsT<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -375,6 +417,23 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
   const int h = min(a.seg_rows, a.row_end - r0);
   const int n_load = h + 2 * K;       // level-0 rows x_0 .. x_{n_load-1}
   const int nt = h + 3 * K - 1;       // ticks until level K has produced h rows
+
+  // Fused exchange: a warp reads top (bottom) ghosts iff it produces one of
+  // the first (last) `ghost` rows.  Wait until the neighbour has delivered
+  // this block's ghosts -- the same signal says it has finished reading the
+  // ghost rows of ours that this block's edge stores overwrite.
+  bool top_edge = false, bot_edge = false;
+  int orow = r0;
+  T* ptop = nullptr;
+  T* pbot = nullptr;
+  if constexpr (kPeer) {
+    top_edge = r0 < a.ghost;
+    bot_edge = r0 + h > a.rows - a.ghost;
+    if (top_edge) wait_ready(a.ready + 0, a.seq);
+    if (bot_edge) wait_ready(a.ready + 1, a.seq);
+    ptop = a.peer_top + (size_t)grp * W;
+    pbot = a.peer_bot + (size_t)grp * W - (size_t)(a.rows - a.ghost) * pitch;
+  }
 
   // Running source row (wraps on the torus; never in ghosted slabs) and
   // running destination row: pointer increments, no per-tick index math.
@@ -439,8 +498,15 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
           if (store) {
             store_row<W, T>(du, du + vout_delta, 0, o);
             fold_finite<W, T>(fin, o);
+            if constexpr (kPeer) {
+              if (orow < a.ghost)
+                store_row<W, T>(ptop, ptop + vout_delta, (size_t)orow * pitch, o);
+              else if (orow >= a.rows - a.ghost)
+                store_row<W, T>(pbot, pbot + vout_delta, (size_t)orow * pitch, o);
+            }
           }
           du += pitch;
+          if constexpr (kPeer) ++orow;
         }
       }
     }
@@ -464,8 +530,15 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
         if (store) {
           store_row<W, T>(du, du + vout_delta, 0, o);
           fold_finite<W, T>(fin, o);
+          if constexpr (kPeer) {
+            if (orow < a.ghost)
+              store_row<W, T>(ptop, ptop + vout_delta, (size_t)orow * pitch, o);
+            else if (orow >= a.rows - a.ghost)
+              store_row<W, T>(pbot, pbot + vout_delta, (size_t)orow * pitch, o);
+          }
         }
         du += pitch;
+        if constexpr (kPeer) ++orow;
       } else {
         level_row<W, T, kFast>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
       }
@@ -495,6 +568,17 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
   stage_wait<0>();
 
   if (fin.bad_in_warp() && lane == 0 && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);
+
+  if constexpr (kPeer) {
+    if (top_edge || bot_edge) {
+      __threadfence_system();  // this lane's peer stores before the count
+      __syncwarp();
+      if (lane == 0) {
+        if (top_edge) edge_done(a.edge_count + 0, a.n_top, a.sig_prev, a.seq + 1u);
+        if (bot_edge) edge_done(a.edge_count + 1, a.n_bot, a.sig_next, a.seq + 1u);
+      }
+    }
+  }
 }
 
 }  // namespace rdcnn_dev

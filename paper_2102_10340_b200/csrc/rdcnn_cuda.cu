@@ -16,6 +16,7 @@
 #include <vector>
 
 #include <dlfcn.h>
+#include <unistd.h>
 #include <nccl.h>
 
 #include "analysis.cuh"
@@ -133,6 +134,49 @@ int resident_blocks(int k, int w, bool fast, bool per_grid) {
     auto fn = t.fn[w > 1][k_index(k)][fast][per_grid];
     if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kThreads, smem_for<T>(w)) !=
                    cudaSuccess || n < 1)
+      n = 1;
+    r = n;
+  }
+  return r;
+}
+
+// Fused peer-exchange instances (fp32 slabs, shared gene): [wide][k][fast].
+struct PeerTable {
+  using Fn = void (*)(StepArgsT<float>);
+  Fn fn[2][4][2] = {};
+  int resident[2][4][2] = {};
+};
+
+template <int W, int KI, int FI>
+void fill_peer_one(PeerTable& t) {
+  t.fn[W > 1][KI][FI] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI == 1, false, true>;
+}
+
+template <int W>
+void fill_peer_w(PeerTable& t) {
+  fill_peer_one<W, 0, 0>(t); fill_peer_one<W, 0, 1>(t);
+  fill_peer_one<W, 1, 0>(t); fill_peer_one<W, 1, 1>(t);
+  fill_peer_one<W, 2, 0>(t); fill_peer_one<W, 2, 1>(t);
+  fill_peer_one<W, 3, 0>(t); fill_peer_one<W, 3, 1>(t);
+}
+
+PeerTable& peer_table() {
+  static PeerTable t = [] {
+    PeerTable x;
+    fill_peer_w<1>(x);
+    fill_peer_w<4>(x);
+    return x;
+  }();
+  return t;
+}
+
+int peer_resident_blocks(int k, int w, bool fast) {
+  PeerTable& t = peer_table();
+  int& r = t.resident[w > 1][k_index(k)][fast];
+  if (r == 0) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, t.fn[w > 1][k_index(k)][fast], kThreads,
+                                                      smem_for<float>(w)) != cudaSuccess || n < 1)
       n = 1;
     r = n;
   }
@@ -411,6 +455,15 @@ struct rdcnn_sim {
   int ring_rank = 0, ring_world = 1;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_bnd = nullptr, ev_xchg = nullptr;
+  // fused peer ring (rdcnn_slab_attach_peers): peer memory of the ring
+  // neighbours, opened from their IPC handles (or taken as is in-process)
+  bool p2p = false;
+  unsigned* p2p_words = nullptr;    // own: [0] top ready, [1] bottom ready, [2..3] edge counters
+  void* peer_buf[2][2] = {};        // [prev, next][buffer]
+  unsigned* peer_words[2] = {};     // [prev, next]
+  int peer_rows[2] = {0, 0};
+  unsigned p2p_seq = 0;             // blocks run since attach (equal on every rank)
+  std::vector<void*> ipc_opened;    // cudaIpcCloseMemHandle on destroy
   void* frames = nullptr;   // snapshot store: n_frames x batch u-planes
   int n_frames = 0;
   double* d_stats = nullptr;        // 3*batch doubles (min, max, median) + batch thresholds
@@ -526,6 +579,8 @@ void free_all(rdcnn_sim* s) {
   if (s->comm_stream) cudaStreamDestroy(s->comm_stream);
   if (s->ev_bnd) cudaEventDestroy(s->ev_bnd);
   if (s->ev_xchg) cudaEventDestroy(s->ev_xchg);
+  for (void* p : s->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (s->p2p_words) cudaFree(s->p2p_words);
   if (s->frames) cudaFree(s->frames);
   if (s->d_stats) cudaFree(s->d_stats);
   if (s->d_counts) cudaFree(s->d_counts);
@@ -765,6 +820,46 @@ int slab_step_impl(rdcnn_sim* s, int k, cudaStream_t st, bool boundary) {
   } else {
     RDCNN_CUDA_TRY(launch_range<T>(s, k, a, gh, s->rows - gh, st));
   }
+  return RDCNN_OK;
+}
+
+// One block of the fused peer ring (rdcnn_slab_attach_peers): every owned row
+// in ONE launch of the kPeer instance, which also stores the edge rows into
+// the neighbours' ghost rows of the output buffer and signals them.  Stream
+// order alone covers the local dependencies (block n+1 reads what block n
+// wrote); the cross-rank ones are the in-kernel ready words.
+int peer_block(rdcnn_sim* s, int k, unsigned tag, cudaStream_t st) {
+  StepArgsT<float> a = base_args<float>(s, s->cur, s->cur ^ 1);
+  a.tag = tag;
+  const int ob = s->cur ^ 1;
+  const size_t pitch = (size_t)s->pitch;
+  a.peer_top = static_cast<float*>(s->peer_buf[0][ob]) + (size_t)(s->ghost + s->peer_rows[0]) * pitch;
+  a.peer_bot = static_cast<float*>(s->peer_buf[1][ob]);
+  a.edge_count = s->p2p_words + 2;
+  a.sig_prev = s->peer_words[0] + 1;
+  a.sig_next = s->peer_words[1] + 0;
+  a.ready = s->p2p_words;
+  a.seq = s->p2p_seq;
+  const int w = width_for<float>(s);
+  const bool fast = s->mode == RDCNN_FAST;
+  const int rw = peer_resident_blocks(k, w, fast) * (kThreads / 32);
+  const Plan p = make_plan(s->cols, w, k, 1, 0, s->rows, s->seg_rows, s->sm_count, rw);
+  a.row_begin = 0;
+  a.row_end = s->rows;
+  a.seg_rows = p.seg_rows;
+  a.n_segs = p.n_segs;
+  a.n_bands = p.n_bands;
+  a.band_groups = p.band_groups;
+  a.halo_groups = p.halo;
+  const int h = p.seg_rows, S = s->rows, g = s->ghost;
+  a.n_top = p.n_bands * std::min(p.n_segs, (g + h - 1) / h);  // segments with r0 < g
+  a.n_bot = p.n_bands * (p.n_segs - (S - g) / h);             // segments with r0 + h > S - g
+  auto fn = peer_table().fn[w > 1][k_index(k)][fast];
+  fn<<<dim3((unsigned)p.warps), dim3(kThreads), smem_for<float>(w), st>>>(a);
+  RDCNN_CUDA_TRY(cudaGetLastError());
+  ++s->launches;
+  ++s->p2p_seq;
+  s->cur ^= 1;
   return RDCNN_OK;
 }
 
@@ -1180,9 +1275,116 @@ static int ring_exchange(rdcnn_sim* s, int b, cudaStream_t st) {
   return RDCNN_OK;
 }
 
-int rdcnn_slab_fill_ghosts(rdcnn_sim_t s) {
-  if (!s || !s->slab || !s->comm_stream) return fail(RDCNN_EINVAL, "slab ring not attached");
+// ---- fused peer ring ----------------------------------------------------------
+
+int rdcnn_slab_peer_export(rdcnn_sim_t s, rdcnn_slab_peer_desc* out) {
+  if (!s || !s->slab || !out) return fail(RDCNN_EINVAL, "not a slab handle");
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  if (!s->p2p_words) {
+    RDCNN_CUDA_TRY(cudaMalloc(&s->p2p_words, 4 * sizeof(unsigned)));
+    RDCNN_CUDA_TRY(cudaMemset(s->p2p_words, 0, 4 * sizeof(unsigned)));
+  }
+  std::memset(out, 0, sizeof *out);
+  void* mem[3] = {s->buf[0], s->buf[1], s->p2p_words};
+  out->ipc_ok = 1;
+  for (int m = 0; m < 3; ++m) {
+    out->ptr[m] = (uint64_t)(uintptr_t)mem[m];
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, mem[m]) == cudaSuccess) {
+      std::memcpy(out->ipc[m], &h, sizeof h);
+    } else {
+      cudaGetLastError();  // in-process rings do not need IPC
+      out->ipc_ok = 0;
+    }
+  }
+  out->pid = (int64_t)getpid();
+  out->device = s->device;
+  out->rows = s->rows;
+  out->cols = s->cols;
+  out->ghost = s->ghost;
+  return RDCNN_OK;
+}
+
+static int open_peer(rdcnn_sim* s, const rdcnn_slab_peer_desc* d, void* mem[3]) {
+  if (d->pid == (int64_t)getpid()) {  // same process: the pointers are valid as they are
+    for (int m = 0; m < 3; ++m) mem[m] = (void*)(uintptr_t)d->ptr[m];
+    if (d->device != s->device) {
+      cudaError_t e = cudaDeviceEnablePeerAccess(d->device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else RDCNN_CUDA_TRY(e);
+    }
+    return RDCNN_OK;
+  }
+  if (!d->ipc_ok) return fail(RDCNN_ECUDA, "peer slab (pid %lld) could not export IPC handles", (long long)d->pid);
+  for (int m = 0; m < 3; ++m) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, d->ipc[m], sizeof h);
+    RDCNN_CUDA_TRY(cudaIpcOpenMemHandle(&mem[m], h, cudaIpcMemLazyEnablePeerAccess));
+    s->ipc_opened.push_back(mem[m]);
+  }
+  return RDCNN_OK;
+}
+
+int rdcnn_slab_attach_peers(rdcnn_sim_t s, int rank, int world, const rdcnn_slab_peer_desc* prev,
+                            const rdcnn_slab_peer_desc* next) {
+  if (!s || !s->slab || !prev || !next) return fail(RDCNN_EINVAL, "bad argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(RDCNN_EINVAL, "bad rank %d / world %d", rank, world);
+  if (s->p2p || s->comm_stream) return fail(RDCNN_EINVAL, "ring already attached");
+  if (!s->p2p_words) return fail(RDCNN_EINVAL, "export this slab (rdcnn_slab_peer_export) before attaching");
+  for (const rdcnn_slab_peer_desc* d : {prev, next})
+    if (d->cols != s->cols || d->ghost != s->ghost)
+      return fail(RDCNN_EINVAL, "peer slab %dx%d ghost %d does not match %dx%d ghost %d", d->rows, d->cols,
+                  d->ghost, s->rows, s->cols, s->ghost);
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  void* mp[3];
+  void* mn[3];
+  RDCNN_TRY(open_peer(s, prev, mp));
+  if (std::memcmp(prev, next, sizeof *prev) == 0) {  // world <= 2: one neighbour on both sides
+    std::memcpy(mn, mp, sizeof mp);
+  } else {
+    RDCNN_TRY(open_peer(s, next, mn));
+  }
+  for (int b = 0; b < 2; ++b) {
+    s->peer_buf[0][b] = mp[b];
+    s->peer_buf[1][b] = mn[b];
+  }
+  s->peer_words[0] = static_cast<unsigned*>(mp[2]);
+  s->peer_words[1] = static_cast<unsigned*>(mn[2]);
+  s->peer_rows[0] = prev->rows;
+  s->peer_rows[1] = next->rows;
+  s->ring_rank = rank;
+  s->ring_world = world;
+  s->p2p = true;
+  s->p2p_seq = 0;
+  RDCNN_CUDA_TRY(cudaMemset(s->p2p_words, 0, 4 * sizeof(unsigned)));
+  return RDCNN_OK;
+}
+
+int rdcnn_slab_step_fused(rdcnn_sim_t s, int k, void* stream) {
+  if (!s || !s->slab || !s->p2p) return fail(RDCNN_EINVAL, "peer ring not attached");
+  if (k != 1 && k != 2 && k != 4 && k != 8) return fail(RDCNN_EINVAL, "k must be 1, 2, 4 or 8");
+  if (k > s->ghost) return fail(RDCNN_EINVAL, "k=%d exceeds ghost depth %d", k, s->ghost);
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  return peer_block(s, k, s->p2p_seq + 1, stream ? (cudaStream_t)stream : s->stream);
+}
+
+int rdcnn_slab_fill_ghosts(rdcnn_sim_t s) {
+  if (!s || !s->slab || (!s->comm_stream && !s->p2p)) return fail(RDCNN_EINVAL, "slab ring not attached");
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  if (s->p2p) {
+    // Own edge rows of the front buffer into the neighbours' front ghosts
+    // (peer copies); the caller barriers the ranks before the first block.
+    const size_t pitch = (size_t)s->pitch, g = (size_t)s->ghost, S = (size_t)s->rows;
+    float* mine = s->u_ptr<float>(s->cur);
+    float* prev_bottom = static_cast<float*>(s->peer_buf[0][s->cur]) + (g + (size_t)s->peer_rows[0]) * pitch;
+    float* next_top = static_cast<float*>(s->peer_buf[1][s->cur]);
+    const size_t bytes = g * pitch * sizeof(float);
+    RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+    RDCNN_CUDA_TRY(cudaMemcpyAsync(prev_bottom, mine + g * pitch, bytes, cudaMemcpyDefault, s->stream));
+    RDCNN_CUDA_TRY(cudaMemcpyAsync(next_top, mine + S * pitch, bytes, cudaMemcpyDefault, s->stream));
+    RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return RDCNN_OK;
+  }
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
   RDCNN_TRY(ring_exchange(s, s->cur, s->comm_stream));
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->comm_stream));
@@ -1195,7 +1397,7 @@ int rdcnn_slab_fill_ghosts(rdcnn_sim_t s) {
 // the same time; then the compute stream waits for the exchange and the
 // buffers swap.  No host synchronisation inside the loop.
 int rdcnn_slab_advance(rdcnn_sim_t s, long steps, long* first_bad) {
-  if (!s || !s->slab || !s->comm_stream) return fail(RDCNN_EINVAL, "slab ring not attached");
+  if (!s || !s->slab || (!s->comm_stream && !s->p2p)) return fail(RDCNN_EINVAL, "slab ring not attached");
   if (steps < 0) return fail(RDCNN_EINVAL, "steps must be >= 0");
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   if (first_bad) *first_bad = 0;
@@ -1204,7 +1406,9 @@ int rdcnn_slab_advance(rdcnn_sim_t s, long steps, long* first_bad) {
   RDCNN_CUDA_TRY(cudaMemsetAsync(s->d_flags, 0, sizeof(unsigned), s->stream));
   const Schedule sched = make_schedule(steps, s->max_levels);
   RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
-  for (long n = 0; n < sched.count(); ++n) {
+  for (long n = 0; n < sched.count() && s->p2p; ++n)
+    RDCNN_TRY(peer_block(s, sched.depth(n), (unsigned)(n + 1), s->stream));
+  for (long n = 0; n < sched.count() && !s->p2p; ++n) {
     const int k = sched.depth(n);
     RDCNN_TRY(slab_step_impl<float>(s, k, s->stream, true));
     RDCNN_CUDA_TRY(cudaEventRecord(s->ev_bnd, s->stream));

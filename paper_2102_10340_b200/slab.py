@@ -1,22 +1,25 @@
 """Row-slab sharding of one large torus across GPUs (one process per GPU).
 
 Each rank owns ``rows // world`` consecutive rows of the global lattice
-(SURVEY.md §8e).  Per block of ``k`` time levels:
+(SURVEY.md §8e); rank r-1 is above, r+1 below, and the ring is periodic
+(rank 0's top ghosts are rank P-1's last rows: the torus row wrap of
+kernels.hpp:46-47).  Column wrap stays inside each slab.  Two native
+transports advance a block of ``k <= ghost`` time levels:
 
-1. ``boundary`` kernel: the ``ghost`` rows at each edge of the slab, which
-   need the neighbours' rows (held in the ghost rows from the last exchange);
-2. halo exchange of the freshly computed edge rows with the ring neighbours
-   (rank r-1 above, r+1 below, periodic: rank 0's top ghosts are rank P-1's
-   last rows, the torus row wrap of kernels.hpp:46-47), on the NCCL stream;
-3. ``interior`` kernel on the compute stream, overlapping the exchange;
-4. wait for the exchange, swap buffers.
+* ``p2p`` (default): ONE fused launch per block.  The warps that produce the
+  first/last ``ghost`` rows also store them straight into the neighbours'
+  ghost rows over peer memory (CUDA IPC mappings over NVLink; plain pointers
+  in-process) and publish a "delivered" word with a release store; the
+  neighbours' edge warps acquire it before reading their ghosts.  Interior
+  warps never wait, so the exchange overlaps the step tile by tile.
+* ``nccl``: boundary kernel -> NCCL send/recv of the edge rows on a comm
+  stream, overlapped with the interior kernel; wait; swap.
 
-Column wrap stays inside each slab.  Arithmetic per cell is unchanged, so
-the result is bit-identical to the single-GPU periodic run at any world size.
+Arithmetic per cell is unchanged, so the result is bit-identical to the
+single-GPU periodic run at any world size.
 
-The exchange is a plain function of four row blocks so it can be exercised on
-CPU tensors with the gloo backend (tests/test_slab_gloo.py) and on GPUs with
-NCCL (bench.py --gpus N).
+The Python-driven exchange is a plain function of four row blocks so it can
+be exercised on CPU tensors with the gloo backend (tests/test_slab_gloo.py).
 """
 from __future__ import annotations
 
@@ -76,11 +79,19 @@ class SlabStepper:
 
     def __init__(self, global_rows: int, cols: int, rank: int, world: int, ghost: int = 4,
                  device: int = 0, mode: str = "strict",
-                 exchange: Optional[Callable] = None, seg_rows: int = 0, native: Optional[bool] = None):
+                 exchange: Optional[Callable] = None, seg_rows: int = 0, native: Optional[bool] = None,
+                 transport: str = "p2p", attach: bool = True):
         """``native`` (default: True unless a Python ``exchange`` is given)
-        runs the whole block loop in the C-ABI (rdcnn_slab_advance: NCCL ring
-        on a comm stream, no host work per block); otherwise each block is
-        driven from Python with ``exchange`` (the gloo-testable path)."""
+        runs the whole block loop in the C-ABI (rdcnn_slab_advance, no host
+        work per block); otherwise each block is driven from Python with
+        ``exchange`` (the gloo-testable path).
+
+        ``transport`` (native only): ``"p2p"`` fuses the halo exchange into
+        the step kernel -- edge rows are stored straight into the neighbours'
+        ghost rows over peer memory (CUDA IPC) and signalled with release
+        stores, one launch per block; ``"nccl"`` runs boundary kernel ->
+        NCCL send/recv on a comm stream || interior kernel.  ``attach=False``
+        leaves the ring to the caller (in-process rings, see ``attach_peers``)."""
         if global_rows % world:
             raise ValueError(f"global rows {global_rows} not divisible by world size {world}")
         self._lib = load()
@@ -96,8 +107,41 @@ class SlabStepper:
         self._h = h
         check(self._lib.rdcnn_sim_set_tuning(self._h, ghost, seg_rows))
         self.launches = 0
-        if self.native:
-            self._attach_ring()
+        self._dist_ring = False
+        if transport not in ("p2p", "nccl"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport if self.native else "python"
+        if self.native and attach:
+            if transport == "p2p":
+                self._attach_peers()
+            else:
+                self._attach_ring()
+
+    # -- fused peer ring -------------------------------------------------------
+    def export_peer(self) -> "_lib.PeerDesc":
+        d = _lib.PeerDesc()
+        check(self._lib.rdcnn_slab_peer_export(self._h, ctypes.byref(d)))
+        return d
+
+    def attach_peers(self, prev: "_lib.PeerDesc", nxt: "_lib.PeerDesc"):
+        check(self._lib.rdcnn_slab_attach_peers(self._h, self.rank, self.world, ctypes.byref(prev),
+                                                ctypes.byref(nxt)))
+
+    def _attach_peers(self):
+        """Share every rank's peer descriptor (torch.distributed) and open
+        the ring neighbours' memory; world 1 closes the ring on itself."""
+        mine = self.export_peer()
+        if self.world == 1:
+            self.attach_peers(mine, mine)
+            return
+        import torch.distributed as dist
+
+        blobs = [None] * self.world
+        dist.all_gather_object(blobs, bytes(mine))
+        self._dist_ring = True
+        prev, nxt = ring_neighbours(self.rank, self.world)
+        self.attach_peers(_lib.PeerDesc.from_buffer_copy(blobs[prev]),
+                          _lib.PeerDesc.from_buffer_copy(blobs[nxt]))
 
     def _attach_ring(self):
         """NCCL communicator for the ring (id from rank 0, shared through
@@ -177,7 +221,13 @@ class SlabStepper:
         import torch
 
         if self.native:
+            p2p_ring = self._dist_ring  # ranks in separate processes
+            if p2p_ring:
+                import torch.distributed as dist
+                dist.barrier()  # no rank still reads the ghosts this overwrites
             check(self._lib.rdcnn_slab_fill_ghosts(self._h))
+            if p2p_ring:
+                dist.barrier()  # every ghost row is in before any rank's first block
             return
         works = self.exchange(*self._views(0), self.rank, self.world)
         for w in works:

@@ -295,16 +295,19 @@ def test_fast_mode_tolerance(oracle):
 # Slab (multi-GPU) kernels on one GPU: slab mode == periodic mode
 # --------------------------------------------------------------------------
 
+@pytest.mark.parametrize("transport", ("p2p", "nccl"))
 @pytest.mark.parametrize("ghost", (1, 2, 4, 8))
-def test_single_slab_ring_equals_periodic(oracle, ghost):
-    """world=1 ring (ghosts = own wrapped rows) reproduces the periodic run."""
+def test_single_slab_ring_equals_periodic(oracle, ghost, transport):
+    """world=1 ring (ghosts = own wrapped rows) reproduces the periodic run,
+    with the fused peer exchange (edge rows stored into the slab's own ghost
+    rows by the step kernel) and with the NCCL-ring block loop."""
     import torch
     from paper_2102_10340_b200.slab import SlabStepper
 
     rows, cols, iters = 64, 96, 37
     u0, v0 = oracle.init(2, rows, cols, 5)
     ou, ov, _ = oracle.run(rows, cols, u0, v0, iters)
-    s = SlabStepper(rows, cols, rank=0, world=1, ghost=ghost, device=0)
+    s = SlabStepper(rows, cols, rank=0, world=1, ghost=ghost, device=0, transport=transport)
     s.upload(u0, v0)
     s.fill_ghosts()
     s.advance(iters)
@@ -361,4 +364,117 @@ def test_multi_slab_emulated_ring(oracle, world):
     torch.cuda.synchronize()
     got_u = np.concatenate([s.download()[0] for s in slabs])
     got_v = np.concatenate([s.download()[1] for s in slabs])
+    assert np.array_equal(bits(got_u), bits(ou)) and np.array_equal(bits(got_v), bits(ov))
+
+
+def _peer_ring(world, rows, cols, ghost, seg_rows=0, mode="strict"):
+    """`world` in-process slabs on one GPU joined by the fused peer ring."""
+    from paper_2102_10340_b200.slab import SlabStepper
+
+    slabs = [SlabStepper(rows, cols, rank=r, world=world, ghost=ghost, device=0, seg_rows=seg_rows,
+                         mode=mode, attach=False) for r in range(world)]
+    descs = [s.export_peer() for s in slabs]
+    for r, s in enumerate(slabs):
+        s.attach_peers(descs[(r - 1) % world], descs[(r + 1) % world])
+    return slabs
+
+
+@pytest.mark.parametrize("world,ghost,seg_rows", [
+    (2, 4, 0), (3, 4, 0), (4, 4, 0), (2, 8, 0), (3, 1, 0), (3, 2, 0),
+    (2, 4, 3),    # edge rows spread over two segments: two warps per edge per band
+    (3, 4, 100),  # one segment holds the whole slab: each warp is both edges
+])
+def test_peer_ring_in_process(oracle, world, ghost, seg_rows):
+    """The fused peer exchange between `world` slabs on one GPU, blocks
+    interleaved rank by rank on one stream: the torus result is bit-identical
+    to the unsplit oracle run, including the k < ghost tail blocks."""
+    import ctypes
+
+    import torch
+
+    rows, cols, iters = 24 * world, 40, 29
+    u0, v0 = oracle.init(1, rows, cols, 42)
+    rng = np.random.default_rng(world * 10 + ghost)
+    u0 = u0 + rng.random(u0.size, dtype=np.float32) * 0.5
+    ou, ov, _ = oracle.run(rows, cols, u0, v0, iters)
+
+    slabs = _peer_ring(world, rows, cols, ghost, seg_rows)
+    S = rows // world
+    for r, s in enumerate(slabs):
+        s.upload(u0[r * S * cols:(r + 1) * S * cols], v0[r * S * cols:(r + 1) * S * cols])
+    for s in slabs:
+        s.fill_ghosts()
+    lib = fhn.load()
+    sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    done = 0
+    while done < iters:
+        k = ghost
+        while k > iters - done:
+            k //= 2
+        for s in slabs:
+            assert lib.rdcnn_slab_step_fused(s._h, k, sp) == 0, fhn.last_error()
+        done += k
+    torch.cuda.synchronize()
+    got_u = np.concatenate([s.download()[0] for s in slabs])
+    got_v = np.concatenate([s.download()[1] for s in slabs])
+    assert np.array_equal(bits(got_u), bits(ou)) and np.array_equal(bits(got_v), bits(ov))
+    for s in slabs:
+        s.close()
+
+
+def _ipc_rank(rank, world, port, rows, cols, iters, q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Oracle
+        from paper_2102_10340_b200.slab import SlabStepper
+
+        orc = Oracle()
+        u0, v0 = orc.init(2, rows, cols, 9)
+        S = rows // world
+        s = SlabStepper(rows, cols, rank=rank, world=world, ghost=4, device=0, transport="p2p")
+        s.upload(u0[rank * S * cols:(rank + 1) * S * cols], v0[rank * S * cols:(rank + 1) * S * cols])
+        s.fill_ghosts()
+        bad = s.advance(iters)
+        u, v = s.download()
+        dist.barrier()  # neighbours are done writing into this slab
+        s.close()
+        q.put((rank, bad, u.tobytes(), v.tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_ring_two_processes_ipc(oracle):
+    """Two processes (one slab each) on one GPU: the peer memory is opened
+    from CUDA IPC handles shared over torch.distributed, as on a multi-GPU
+    box; the result equals the unsplit oracle run."""
+    import multiprocessing as mp
+    import socket
+
+    rows, cols, iters, world = 48, 64, 21, 2
+    u0, v0 = oracle.init(2, rows, cols, 9)
+    ou, ov, _ = oracle.run(rows, cols, u0, v0, iters)
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_rank, args=(r, world, port, rows, cols, iters, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        res = sorted(q.get(timeout=240) for _ in range(world))
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    assert all(p.exitcode == 0 for p in procs)
+    got_u = np.concatenate([np.frombuffer(r[2], np.float32) for r in res])
+    got_v = np.concatenate([np.frombuffer(r[3], np.float32) for r in res])
+    assert [r[1] for r in res] == [0, 0]
     assert np.array_equal(bits(got_u), bits(ou)) and np.array_equal(bits(got_v), bits(ov))
