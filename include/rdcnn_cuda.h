@@ -204,6 +204,15 @@ int rdcnn_slab_attach_peers(rdcnn_sim_t sim, int rank, int world,
  * must have been filled (rdcnn_slab_fill_ghosts). */
 int rdcnn_slab_step_fused(rdcnn_sim_t sim, int k, void* stream);
 
+/* Exact blow-up iteration for slab runs (engine.hpp:79 BlowUpError(iter+1)).
+ * With the checkpoint on, every rdcnn_slab_advance first copies its input
+ * buffer (ghost rows included) aside; rdcnn_slab_restore puts it back as the
+ * front buffer.  The ranks then agree on the first bad block (min over
+ * ranks), restore, re-advance to that block's first iteration and step one
+ * level at a time until any rank flags -- see slab.py SlabStepper.advance. */
+int rdcnn_slab_checkpoint_enable(rdcnn_sim_t sim, int on);
+int rdcnn_slab_restore(rdcnn_sim_t sim);
+
 /* ---- snapshot store and analysis (batched sweeps, frames) ----------------
  * Replaces the host-side post-processing of sweep.hpp:48-112 and
  * frame.hpp:28-66 for device-resident runs.  A handle reserves `nframes`

@@ -86,6 +86,8 @@ SIGNATURES = {
     "rdcnn_slab_peer_export": (c_int, [c_void_p, POINTER(PeerDesc)]),
     "rdcnn_slab_attach_peers": (c_int, [c_void_p, c_int, c_int, POINTER(PeerDesc), POINTER(PeerDesc)]),
     "rdcnn_slab_step_fused": (c_int, [c_void_p, c_int, c_void_p]),
+    "rdcnn_slab_checkpoint_enable": (c_int, [c_void_p, c_int]),
+    "rdcnn_slab_restore": (c_int, [c_void_p]),
     "rdcnn_sim_frames_reserve": (c_int, [c_void_p, c_int]),
     "rdcnn_sim_frame_capture": (c_int, [c_void_p, c_int]),
     "rdcnn_sim_frame_download": (c_int, [c_void_p, c_int, c_void_p]),

@@ -388,8 +388,11 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
 
   // A grid that already blew up in an earlier launch of this advance stays
   // frozen (no stores), so the input of its first bad launch survives for
-  // the host-side replay.  The flag is only needed at the first store.
-  const unsigned frozen = a.flags != nullptr ? *(volatile unsigned*)(a.flags + g) : 0u;
+  // the host-side replay.  A flag carrying this launch's own tag was raised
+  // by a sibling warp (or, in slab mode, by the boundary launch of the same
+  // block) and does not freeze.  The flag is only needed at the first store.
+  const unsigned fl = a.flags != nullptr ? *(volatile unsigned*)(a.flags + g) : 0u;
+  const unsigned frozen = fl != 0u && fl != a.tag;
 
   // Shared gene: read straight from the kernel-parameter bank.  Per-grid
   // genes (sweeps) come from global memory once per warp.

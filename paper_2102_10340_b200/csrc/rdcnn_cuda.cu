@@ -463,6 +463,7 @@ struct rdcnn_sim {
   unsigned* peer_words[2] = {};     // [prev, next]
   int peer_rows[2] = {0, 0};
   unsigned p2p_seq = 0;             // blocks run since attach (equal on every rank)
+  void* ckpt = nullptr;             // slab: copy of the last advance's input buffer (ghosts included)
   std::vector<void*> ipc_opened;    // cudaIpcCloseMemHandle on destroy
   void* frames = nullptr;   // snapshot store: n_frames x batch u-planes
   int n_frames = 0;
@@ -581,6 +582,7 @@ void free_all(rdcnn_sim* s) {
   if (s->ev_xchg) cudaEventDestroy(s->ev_xchg);
   for (void* p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   if (s->p2p_words) cudaFree(s->p2p_words);
+  if (s->ckpt) cudaFree(s->ckpt);
   if (s->frames) cudaFree(s->frames);
   if (s->d_stats) cudaFree(s->d_stats);
   if (s->d_counts) cudaFree(s->d_counts);
@@ -1405,6 +1407,9 @@ int rdcnn_slab_advance(rdcnn_sim_t s, long steps, long* first_bad) {
   s->slab_tag = 0;
   RDCNN_CUDA_TRY(cudaMemsetAsync(s->d_flags, 0, sizeof(unsigned), s->stream));
   const Schedule sched = make_schedule(steps, s->max_levels);
+  if (s->ckpt)  // the input of this advance, for an exact blow-up replay
+    RDCNN_CUDA_TRY(cudaMemcpyAsync(s->ckpt, s->buf[s->cur], s->buf_elems * s->elem, cudaMemcpyDeviceToDevice,
+                                   s->stream));
   RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
   for (long n = 0; n < sched.count() && s->p2p; ++n)
     RDCNN_TRY(peer_block(s, sched.depth(n), (unsigned)(n + 1), s->stream));
@@ -1433,6 +1438,29 @@ int rdcnn_slab_advance(rdcnn_sim_t s, long steps, long* first_bad) {
     if (first_bad) *first_bad = sched.start((long)tag - 1) + 1;
     return fail(RDCNN_EBLOWUP, "blow-up: non-finite state in block %u", tag);
   }
+  return RDCNN_OK;
+}
+
+int rdcnn_slab_checkpoint_enable(rdcnn_sim_t s, int on) {
+  if (!s || !s->slab) return fail(RDCNN_EINVAL, "not a slab handle");
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  if (on && !s->ckpt) RDCNN_CUDA_TRY(cudaMalloc(&s->ckpt, s->buf_elems * s->elem));
+  if (!on && s->ckpt) {
+    RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+    RDCNN_CUDA_TRY(cudaFree(s->ckpt));
+    s->ckpt = nullptr;
+  }
+  return RDCNN_OK;
+}
+
+int rdcnn_slab_restore(rdcnn_sim_t s) {
+  if (!s || !s->slab) return fail(RDCNN_EINVAL, "not a slab handle");
+  if (!s->ckpt) return fail(RDCNN_EINVAL, "no checkpoint (rdcnn_slab_checkpoint_enable)");
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  RDCNN_CUDA_TRY(cudaDeviceSynchronize());
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(s->buf[s->cur], s->ckpt, s->buf_elems * s->elem, cudaMemcpyDeviceToDevice,
+                                 s->stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
   return RDCNN_OK;
 }
 

@@ -80,7 +80,7 @@ class SlabStepper:
     def __init__(self, global_rows: int, cols: int, rank: int, world: int, ghost: int = 4,
                  device: int = 0, mode: str = "strict",
                  exchange: Optional[Callable] = None, seg_rows: int = 0, native: Optional[bool] = None,
-                 transport: str = "p2p", attach: bool = True):
+                 transport: str = "p2p", attach: bool = True, exact_blowup: bool = True):
         """``native`` (default: True unless a Python ``exchange`` is given)
         runs the whole block loop in the C-ABI (rdcnn_slab_advance, no host
         work per block); otherwise each block is driven from Python with
@@ -91,7 +91,9 @@ class SlabStepper:
         ghost rows over peer memory (CUDA IPC) and signalled with release
         stores, one launch per block; ``"nccl"`` runs boundary kernel ->
         NCCL send/recv on a comm stream || interior kernel.  ``attach=False``
-        leaves the ring to the caller (in-process rings, see ``attach_peers``)."""
+        leaves the ring to the caller (in-process rings, see ``attach_peers``).
+        ``exact_blowup`` keeps a device copy of each advance's input so a
+        blow-up is reported at its exact iteration (see ``advance``)."""
         if global_rows % world:
             raise ValueError(f"global rows {global_rows} not divisible by world size {world}")
         self._lib = load()
@@ -108,6 +110,9 @@ class SlabStepper:
         check(self._lib.rdcnn_sim_set_tuning(self._h, ghost, seg_rows))
         self.launches = 0
         self._dist_ring = False
+        self.exact_blowup = bool(exact_blowup) and self.native
+        if self.exact_blowup:
+            check(self._lib.rdcnn_slab_checkpoint_enable(self._h, 1))
         if transport not in ("p2p", "nccl"):
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport if self.native else "python"
@@ -234,19 +239,63 @@ class SlabStepper:
             w.wait()
         torch.cuda.current_stream(self.device).synchronize()
 
+    # -- blow-up (engine.hpp:79, BlowUpError(iter + 1)) -----------------------
+    def _advance_native(self, steps: int) -> int:
+        """One native advance; the first iteration (1-based) of this rank's
+        first bad block, or 0."""
+        bad = ctypes.c_long()
+        rc = self._lib.rdcnn_slab_advance(self._h, int(steps), ctypes.byref(bad))
+        if rc != _lib.RDCNN_EBLOWUP:
+            check(rc)
+        n = ctypes.c_long()
+        check(self._lib.rdcnn_sim_launch_count(self._h, ctypes.byref(n)))
+        self.launches += n.value
+        return bad.value if rc == _lib.RDCNN_EBLOWUP else 0
+
+    def _agree(self, x: int, op: str) -> int:
+        """min over ranks of the non-zero values (0 = none), or max."""
+        if not self._dist_ring:
+            return x
+        import torch
+        import torch.distributed as dist
+
+        big = 1 << 62
+        dev = f"cuda:{self.device}" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([(x or big) if op == "min" else x], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN if op == "min" else dist.ReduceOp.MAX)
+        v = int(t.item())
+        return 0 if (op == "min" and v == big) else v
+
+    def _replay_exact(self, first_block_iter: int) -> int:
+        """Every rank: restore this advance's input, re-run to the first bad
+        block, then one level at a time until any rank flags.  Leaves the
+        post-blow-up state (as run_timed does, engine.hpp:103-104) and returns
+        the exact 1-based iteration."""
+        check(self._lib.rdcnn_slab_restore(self._h))
+        pre = first_block_iter - 1
+        if pre and self._agree(self._advance_native(pre), "min"):
+            raise RuntimeError("blow-up before the first flagged block on replay")
+        for m in range(1, self.ghost + 1):
+            if self._agree(1 if self._advance_native(1) else 0, "max"):
+                return pre + m
+        raise RuntimeError(f"blow-up flagged in the block at iteration {first_block_iter} "
+                           "was not reproduced by the replay")
+
     def advance(self, steps: int, stream=None):
         """Advance by `steps` iterations in blocks of <= ghost levels.
-        Returns the first iteration of the first block that produced a
-        non-finite value (0 = none; native path only)."""
+
+        Native path: returns 0, or the exact first iteration (1-based, as
+        BlowUpError.iteration) at which any rank's slab held a non-finite
+        value -- agreed over the ranks, found by replaying the first bad block
+        level by level from the advance's checkpointed input (block
+        granularity with ``exact_blowup=False``)."""
         import torch
 
         if self.native:
-            bad = ctypes.c_long()
-            check(self._lib.rdcnn_slab_advance(self._h, int(steps), ctypes.byref(bad)))
-            n = ctypes.c_long()
-            check(self._lib.rdcnn_sim_launch_count(self._h, ctypes.byref(n)))
-            self.launches += n.value
-            return bad.value
+            first = self._agree(self._advance_native(steps), "min")
+            if first == 0 or not self.exact_blowup:
+                return first
+            return self._replay_exact(first)
         st = stream or torch.cuda.current_stream(self.device)
         sp = ctypes.c_void_p(st.cuda_stream)
         done = 0

@@ -422,7 +422,36 @@ def test_peer_ring_in_process(oracle, world, ghost, seg_rows):
         s.close()
 
 
-def _ipc_rank(rank, world, port, rows, cols, iters, q):
+@pytest.mark.parametrize("transport", ("p2p", "nccl"))
+@pytest.mark.parametrize("ghost", (1, 2, 4, 8))
+def test_slab_blowup_exact_iteration(oracle, ghost, transport):
+    """A slab run reports the exact first non-finite iteration (engine.hpp:79)
+    -- replayed level by level from the advance's checkpointed input -- and
+    leaves the post-blow-up state, also when the advance is split."""
+    from paper_2102_10340_b200.slab import SlabStepper
+
+    g = fhn.Gene(Du=2.6)  # checkerboard instability: blows up at iteration 99
+    rows, cols = 32, 24
+    u0, v0 = oracle.init(2, rows, cols, 9)
+    _, _, want = oracle.run(rows, cols, u0, v0, 1000, g.to_vector())
+    assert want == 99
+    ou, ov, _ = oracle.run(rows, cols, u0, v0, want, g.to_vector())
+    for split in (0, 50):
+        s = SlabStepper(rows, cols, rank=0, world=1, ghost=ghost, device=0, transport=transport)
+        s.set_params(g)
+        s.upload(u0, v0)
+        s.fill_ghosts()
+        if split:
+            assert s.advance(split) == 0
+        assert s.advance(500) == want - split
+        u, v = s.download()
+        s.close()
+        assert np.array_equal(np.isfinite(u), np.isfinite(ou))
+        fin = np.isfinite(ou) & np.isfinite(ov)
+        assert np.array_equal(bits(u)[fin], bits(ou)[fin]) and np.array_equal(bits(v)[fin], bits(ov)[fin])
+
+
+def _ipc_rank(rank, world, port, rows, cols, iters, q, gene7=None):
     import os
 
     import torch.distributed as dist
@@ -437,6 +466,9 @@ def _ipc_rank(rank, world, port, rows, cols, iters, q):
         u0, v0 = orc.init(2, rows, cols, 9)
         S = rows // world
         s = SlabStepper(rows, cols, rank=rank, world=world, ghost=4, device=0, transport="p2p")
+        if gene7 is not None:
+            import paper_2102_10340_b200 as fhn_
+            s.set_params(fhn_.Gene(**gene7))
         s.upload(u0[rank * S * cols:(rank + 1) * S * cols], v0[rank * S * cols:(rank + 1) * S * cols])
         s.fill_ghosts()
         bad = s.advance(iters)
@@ -448,22 +480,31 @@ def _ipc_rank(rank, world, port, rows, cols, iters, q):
         dist.destroy_process_group()
 
 
-def test_peer_ring_two_processes_ipc(oracle):
+@pytest.mark.parametrize("blowup", (False, True))
+def test_peer_ring_two_processes_ipc(oracle, blowup):
     """Two processes (one slab each) on one GPU: the peer memory is opened
     from CUDA IPC handles shared over torch.distributed, as on a multi-GPU
-    box; the result equals the unsplit oracle run."""
+    box; the result equals the unsplit oracle run.  With an unstable gene
+    both ranks agree on the exact blow-up iteration and hold the oracle's
+    post-blow-up state."""
     import multiprocessing as mp
     import socket
 
-    rows, cols, iters, world = 48, 64, 21, 2
+    rows, cols, world = 48, 64, 2
+    gene = fhn.Gene(Du=2.6) if blowup else fhn.Gene()
+    iters = 400 if blowup else 21
     u0, v0 = oracle.init(2, rows, cols, 9)
-    ou, ov, _ = oracle.run(rows, cols, u0, v0, iters)
+    _, _, want = oracle.run(rows, cols, u0, v0, iters, gene.to_vector())
+    assert (want > 0) == blowup
+    ou, ov, _ = oracle.run(rows, cols, u0, v0, want or iters, gene.to_vector())
     with socket.socket() as so:
         so.bind(("127.0.0.1", 0))
         port = so.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_ipc_rank, args=(r, world, port, rows, cols, iters, q)) for r in range(world)]
+    g7 = dict(dt=gene.dt, a=gene.a, b=gene.b, eps=gene.eps, c=gene.c, Du=gene.Du, Dv=gene.Dv)
+    procs = [ctx.Process(target=_ipc_rank, args=(r, world, port, rows, cols, iters, q, g7))
+             for r in range(world)]
     for p in procs:
         p.start()
     try:
@@ -476,5 +517,7 @@ def test_peer_ring_two_processes_ipc(oracle):
     assert all(p.exitcode == 0 for p in procs)
     got_u = np.concatenate([np.frombuffer(r[2], np.float32) for r in res])
     got_v = np.concatenate([np.frombuffer(r[3], np.float32) for r in res])
-    assert [r[1] for r in res] == [0, 0]
-    assert np.array_equal(bits(got_u), bits(ou)) and np.array_equal(bits(got_v), bits(ov))
+    assert [r[1] for r in res] == [want, want]
+    fin = np.isfinite(ou) & np.isfinite(ov)
+    assert np.array_equal(np.isfinite(got_u), np.isfinite(ou))
+    assert np.array_equal(bits(got_u)[fin], bits(ou)[fin]) and np.array_equal(bits(got_v)[fin], bits(ov)[fin])
