@@ -118,6 +118,13 @@ int rdcnn_sim_launch_count(rdcnn_sim_t sim, long* n);
 /* Tuning: maximum time levels per launch (1, 2, 4 or 8; default 4) and the
  * rows per warp segment (0 = automatic). */
 int rdcnn_sim_set_tuning(rdcnn_sim_t sim, int max_levels, int seg_rows);
+/* Small single lattices (batch 1, fp32, cols 128 or 256, rows = C*R with
+ * C, R <= 16 -- e.g. the reference's 256x256 default) advance in ONE launch
+ * of a persistent 16-CTA thread-block cluster: state in registers, row
+ * halos through shared memory and DSMEM, one cluster barrier per step,
+ * exact per-step blow-up stop.  mode 0: automatic (default), 1: required
+ * (advance fails with RDCNN_EINVAL when the shape does not fit), -1: off. */
+int rdcnn_sim_set_persistent(rdcnn_sim_t sim, int mode);
 /* The handle's CUDA stream (cudaStream_t) for interop with other libraries. */
 int rdcnn_sim_stream(rdcnn_sim_t sim, void** stream);
 /* Device pointers of the current front planes (plane u, plane v; float or

@@ -70,6 +70,7 @@ SIGNATURES = {
     "rdcnn_sim_elapsed_ms": (c_int, [c_void_p, POINTER(c_double)]),
     "rdcnn_sim_launch_count": (c_int, [c_void_p, POINTER(c_long)]),
     "rdcnn_sim_set_tuning": (c_int, [c_void_p, c_int, c_int]),
+    "rdcnn_sim_set_persistent": (c_int, [c_void_p, c_int]),
     "rdcnn_sim_stream": (c_int, [c_void_p, POINTER(c_void_p)]),
     "rdcnn_sim_device_state": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p)]),
     "rdcnn_slab_create": (c_int, [c_int, c_int, c_int, c_int, c_int, POINTER(c_void_p)]),

@@ -1,0 +1,268 @@
+// fhn_cluster.cuh -- persistent thread-block-cluster kernel for small single
+// lattices (SURVEY.md §7 "launch-bound small grids"; cfg1 = 256^2 x 1000).
+//
+// The whole advance is ONE launch of ONE cluster of C CTAs (C <= 16,
+// non-portable size).  CTA c owns R = rows / C consecutive rows; each warp
+// owns RW consecutive rows and lane l owns W consecutive columns of them, so
+// the state lives in registers for all `steps` iterations.  Per step:
+//   1. each warp publishes its first and last row (u, v) into the CTA's
+//      shared exchange rows of this step's parity; the CTA's first/last row
+//      also goes into the previous/next CTA's halo row (DSMEM: mapa +
+//      st.shared::cluster), closing the torus ring across the cluster;
+//   2. cluster barrier ARRIVE (release); the warp's interior rows (1..RW-2)
+//      need only its own registers and are computed while the barrier
+//      completes; then WAIT (acquire);
+//   3. the edge rows: up/down rows from shared memory, left/right columns
+//      from warp shuffles (the row wraps around the warp: the torus column
+//      wrap), the reference cell update (fhn_cell, strict or fast).
+// Non-finite results set a per-parity flag word in EVERY CTA (remote stores,
+// only on blow-up); all CTAs read their local copy after the next barrier and
+// stop together, holding the post-blow-up state, so the exact iteration is
+// known without a replay (engine.hpp:79, BlowUpError(iter+1)).
+//
+// Shared memory layout per CTA: [flag0, flag1, pad, pad] then
+// X[2 parities][R + 2 rows][2 planes][W/4 chunks][32 lanes] float4 -- chunk-
+// major so each STS.128/LDS.128 of a warp is 512 contiguous bytes (no bank
+// conflicts).  Row 0 is the top halo, rows 1..R the CTA's own (only each
+// warp's first and last are written), row R+1 the bottom halo.
+#pragma once
+
+#include "fhn_stencil.cuh"
+
+namespace rdcnn_dev {
+
+struct ClusterArgs {
+  const float* u_in;
+  const float* v_in;
+  float* u_out;
+  float* v_out;
+  int rows, cols;
+  int R;                 // rows per CTA (= warps per CTA x rows per warp)
+  long long steps;
+  ParamsT<float> p;
+  long long* first_bad;  // 0, or the 1-based iteration whose output went non-finite
+};
+
+constexpr int kClusterMax = 16;
+
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_nctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, unsigned rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, unsigned v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ void lds_v4(uint32_t addr, float& a, float& b, float& c, float& d) {
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+               : "=f"(a), "=f"(b), "=f"(c), "=f"(d)
+               : "r"(addr)
+               : "memory");
+}
+
+// Bytes of dynamic shared memory for R rows per CTA.
+template <int W>
+constexpr int cluster_smem_bytes(int R) {
+  return 16 + 2 * (R + 2) * 2 * W * 32 * 4;
+}
+
+template <int W>
+__device__ __forceinline__ void publish_row(uint32_t addr, const float (&u)[W], const float (&v)[W]) {
+  constexpr uint32_t kPlane = W / 4 * 32 * 16;
+#pragma unroll
+  for (int c = 0; c < W / 4; ++c) {
+    sts_v4(addr + c * 512, u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
+    sts_v4(addr + c * 512 + kPlane, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  }
+}
+template <int W>
+__device__ __forceinline__ void publish_row_remote(uint32_t addr, const float (&u)[W], const float (&v)[W]) {
+  constexpr uint32_t kPlane = W / 4 * 32 * 16;
+#pragma unroll
+  for (int c = 0; c < W / 4; ++c) {
+    st_cluster_v4(addr + c * 512, u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
+    st_cluster_v4(addr + c * 512 + kPlane, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  }
+}
+template <int W>
+__device__ __forceinline__ void read_row(uint32_t addr, float (&u)[W], float (&v)[W]) {
+  constexpr uint32_t kPlane = W / 4 * 32 * 16;
+#pragma unroll
+  for (int c = 0; c < W / 4; ++c) {
+    lds_v4(addr + c * 512, u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
+    lds_v4(addr + c * 512 + kPlane, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  }
+}
+
+// One row of one step: left/right by shuffles (the warp is the whole row, so
+// lane 31's right neighbour is lane 0: the torus column wrap).
+template <int W, bool kFast>
+__device__ __forceinline__ void cluster_row(const float (&uu)[W], const float (&vu)[W], const float (&uc)[W],
+                                            const float (&vc)[W], const float (&ud)[W], const float (&vd)[W],
+                                            float (&un)[W], float (&vn)[W], const ParamsT<float>& p,
+                                            float neg_eps, int lane_l, int lane_r) {
+  const float ul = __shfl_sync(kFull, uc[W - 1], lane_l);
+  const float ur = __shfl_sync(kFull, uc[0], lane_r);
+  const float vl = __shfl_sync(kFull, vc[W - 1], lane_l);
+  const float vr = __shfl_sync(kFull, vc[0], lane_r);
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const float u_l = k > 0 ? uc[k - 1] : ul;
+    const float u_r = k < W - 1 ? uc[k + 1] : ur;
+    const float v_l = k > 0 ? vc[k - 1] : vl;
+    const float v_r = k < W - 1 ? vc[k + 1] : vr;
+    fhn_cell<float, kFast>(uc[k], vc[k], u_r, u_l, ud[k], uu[k], v_r, v_l, vd[k], vu[k], p, neg_eps, un[k],
+                           vn[k]);
+  }
+}
+
+// W columns per lane, RW consecutive rows per warp, R = warps * RW rows per CTA.
+template <int RW>
+struct ClusterThreads {  // launch bound: 4-row warps keep ~200 registers
+  static constexpr int value = RW >= 4 ? 256 : 512;
+};
+
+template <int W, int RW, bool kFast>
+__global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kernel(const ClusterArgs a) {
+  static_assert(W % 4 == 0, "W must be a multiple of 4 (float4 chunks)");
+  constexpr uint32_t kRow = 2 * (W / 4) * 32 * 16;  // bytes of one exchange row (u, v)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+
+  const unsigned crank = cluster_ctarank();
+  const unsigned C = cluster_nctarank();
+  const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+  const int nw = int(blockDim.x >> 5);
+  const int R = a.R;  // = nw * RW
+  const int grow0 = int(crank) * R + warp * RW;  // this warp's first lattice row
+  const ParamsT<float> p = a.p;
+  const float neg_eps = -p.eps;  // model.hpp:45 negates eps first
+  const int lane_l = (lane + 31) & 31, lane_r = (lane + 1) & 31;
+
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  const uint32_t flags = base;        // two u32 flags (step parity)
+  const uint32_t X = base + 16;       // exchange rows, local row i at X + i*kRow
+  const uint32_t par_bytes = (uint32_t)(R + 2) * kRow;
+  const uint32_t lane_off = (uint32_t)lane * 16;
+  const uint32_t my_first = X + (uint32_t)(1 + warp * RW) * kRow + lane_off;
+  const uint32_t my_last = my_first + (uint32_t)(RW - 1) * kRow;
+  const uint32_t above = my_first - kRow;  // the previous warp's last row (or the top halo)
+  const uint32_t below = my_last + kRow;   // the next warp's first row (or the bottom halo)
+  // Ring: the CTA's first row -> prev CTA's bottom halo (row R+1); its last
+  // row -> next CTA's top halo (row 0).
+  const unsigned prev = (crank + C - 1) % C, next = (crank + 1) % C;
+  const uint32_t to_prev = mapa_shared(X + (uint32_t)(R + 1) * kRow + lane_off, prev);
+  const uint32_t to_next = mapa_shared(X + lane_off, next);
+  const bool cta_first = warp == 0, cta_last = warp == nw - 1;
+
+  float u[RW][W], v[RW][W];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const size_t off = (size_t)(grow0 + r) * a.cols + (size_t)lane * W;
+#pragma unroll
+    for (int k = 0; k < W; k += 4) {
+      const float4 x = *reinterpret_cast<const float4*>(a.u_in + off + k);
+      const float4 y = *reinterpret_cast<const float4*>(a.v_in + off + k);
+      u[r][k] = x.x; u[r][k + 1] = x.y; u[r][k + 2] = x.z; u[r][k + 3] = x.w;
+      v[r][k] = y.x; v[r][k + 1] = y.y; v[r][k + 2] = y.z; v[r][k + 3] = y.w;
+    }
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %1};\n" ::"r"(flags), "r"(0u) : "memory");
+  }
+  cluster_barrier();  // flags zeroed and every CTA of the cluster running before any DSMEM store
+
+  Finite<float> fin;
+  long long done = 0;
+  for (; done < a.steps; ++done) {
+    const uint32_t par = (uint32_t)(done & 1) * par_bytes;
+    // 1. publish the warp's edge rows (the CTA's edge rows also to the ring neighbours)
+    publish_row<W>(my_first + par, u[0], v[0]);
+    if (RW > 1) publish_row<W>(my_last + par, u[RW - 1], v[RW - 1]);
+    if (cta_first) publish_row_remote<W>(to_prev + par, u[0], v[0]);
+    if (cta_last) publish_row_remote<W>(to_next + par, u[RW - 1], v[RW - 1]);
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    // 2. interior rows need only this warp's registers: overlap the barrier
+    float un[RW][W], vn[RW][W];
+#pragma unroll
+    for (int r = 1; r < RW - 1; ++r)
+      cluster_row<W, kFast>(u[r - 1], v[r - 1], u[r], v[r], u[r + 1], v[r + 1], un[r], vn[r], p, neg_eps, lane_l,
+                            lane_r);
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    // The previous step's blow-up flag: every CTA sees the same value here
+    // (written before this barrier's arrive; the next write to this parity
+    // comes after the next barrier).
+    if (done > 0) {
+      unsigned f;
+      asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(f) : "r"(flags + 4u * (uint32_t)((done - 1) & 1)) : "memory");
+      if (f) break;
+    }
+    // 3. edge rows with the neighbours' rows from shared memory
+    {
+      float ua[W], va[W], ub[W], vb[W];
+      read_row<W>(above + par, ua, va);
+      read_row<W>(below + par, ub, vb);
+      if constexpr (RW == 1) {
+        cluster_row<W, kFast>(ua, va, u[0], v[0], ub, vb, un[0], vn[0], p, neg_eps, lane_l, lane_r);
+      } else {
+        cluster_row<W, kFast>(ua, va, u[0], v[0], u[1], v[1], un[0], vn[0], p, neg_eps, lane_l, lane_r);
+        cluster_row<W, kFast>(u[RW - 2], v[RW - 2], u[RW - 1], v[RW - 1], ub, vb, un[RW - 1], vn[RW - 1], p,
+                              neg_eps, lane_l, lane_r);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        u[r][k] = un[r][k];
+        v[r][k] = vn[r][k];
+        fin.add(un[r][k], vn[r][k]);
+      }
+    if (fin.bad_in_warp() && lane == 0) {
+      const uint32_t fl = flags + 4u * (uint32_t)(done & 1);
+      for (unsigned c = 0; c < C; ++c) st_cluster_u32(mapa_shared(fl, c), 1u);
+    }
+  }
+  // The last computed step's flag (or the one that stopped the loop).
+  cluster_barrier();
+  if (done > 0 && threadIdx.x == 0 && crank == 0) {
+    unsigned f;
+    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(f) : "r"(flags + 4u * (uint32_t)((done - 1) & 1)) : "memory");
+    *a.first_bad = f ? done : 0;
+  }
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const size_t off = (size_t)(grow0 + r) * a.cols + (size_t)lane * W;
+#pragma unroll
+    for (int k = 0; k < W; k += 4) {
+      *reinterpret_cast<float4*>(a.u_out + off + k) = make_float4(u[r][k], u[r][k + 1], u[r][k + 2], u[r][k + 3]);
+      *reinterpret_cast<float4*>(a.v_out + off + k) = make_float4(v[r][k], v[r][k + 1], v[r][k + 2], v[r][k + 3]);
+    }
+  }
+  // No CTA exits while a peer could still store into its shared memory: the
+  // last DSMEM stores precede the barrier above.
+}
+
+}  // namespace rdcnn_dev

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -20,6 +21,7 @@
 #include <nccl.h>
 
 #include "analysis.cuh"
+#include "fhn_cluster.cuh"
 #include "fhn_stencil.cuh"
 #include "rdcnn_cuda.h"
 
@@ -448,6 +450,8 @@ struct rdcnn_sim {
   long launches = 0;
   int max_levels = 4;
   int seg_rows = 0;
+  int cluster_mode = 0;       // persistent cluster path: 0 auto, 1 required, -1 off
+  long long* d_first_bad = nullptr;  // cluster path result word
   int sm_count = 148;
   unsigned slab_tag = 0;
   // slab ring (native multi-GPU path)
@@ -582,6 +586,7 @@ void free_all(rdcnn_sim* s) {
   if (s->ev_xchg) cudaEventDestroy(s->ev_xchg);
   for (void* p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   if (s->p2p_words) cudaFree(s->p2p_words);
+  if (s->d_first_bad) cudaFree(s->d_first_bad);
   if (s->ckpt) cudaFree(s->ckpt);
   if (s->frames) cudaFree(s->frames);
   if (s->d_stats) cudaFree(s->d_stats);
@@ -665,9 +670,141 @@ int replay_grid(rdcnn_sim* s, int g, int in_buf, int k, int final_buf, int* leve
   return fail(RDCNN_ECUDA, "blow-up flagged for grid %d but not reproduced by replay", g);
 }
 
+// ---- persistent cluster path (small single lattices, fhn_cluster.cuh) -------
+
+struct ClusterPlan {
+  int C = 0, R = 0, W = 0, RW = 0;
+  size_t smem = 0;
+};
+
+using ClusterFn = void (*)(rdcnn_dev::ClusterArgs);
+
+template <int W, int RW>
+ClusterFn cluster_fn_wr(bool fast) {
+  return fast ? &rdcnn_dev::fhn_cluster_kernel<W, RW, true> : &rdcnn_dev::fhn_cluster_kernel<W, RW, false>;
+}
+
+ClusterFn cluster_fn(int w, int rw, bool fast) {
+  if (w == 4) return rw == 1 ? cluster_fn_wr<4, 1>(fast) : rw == 2 ? cluster_fn_wr<4, 2>(fast) : cluster_fn_wr<4, 4>(fast);
+  return rw == 1 ? cluster_fn_wr<8, 1>(fast) : rw == 2 ? cluster_fn_wr<8, 2>(fast) : cluster_fn_wr<8, 4>(fast);
+}
+
+int cluster_max_warps(int rw) { return (rw >= 4 ? 256 : 512) / 32; }
+
+// Rows per warp to try, best first (RDCNN_CLUSTER_RW pins one for tuning).
+std::vector<int> cluster_rw_order() {
+  if (const char* e = std::getenv("RDCNN_CLUSTER_RW")) {
+    const int r = std::atoi(e);
+    if (r == 1 || r == 2 || r == 4) return {r};
+  }
+  return {4, 2, 1};
+}
+
+// One cluster of C CTAs, each R = nw*RW rows (nw warps of RW rows), W =
+// cols/32 columns per lane (4 or 8): the most CTAs first.  Returns false
+// when the shape does not fit or the device cannot host the cluster (then
+// the wavefront kernel runs).
+bool cluster_plan_for(rdcnn_sim* s, ClusterPlan* out) {
+  if (s->slab || s->batch != 1 || s->elem != 4 || s->params_stride != 0 || s->cluster_mode < 0) return false;
+  if (s->cols % 128 != 0) return false;
+  const int w = s->cols / 32;
+  if (w != 4 && w != 8) return false;
+  const bool fast = s->mode == RDCNN_FAST;
+  for (int rw : cluster_rw_order()) {
+    int C = 0;
+    for (int c = rdcnn_dev::kClusterMax; c >= 1; --c)
+      if (s->rows % c == 0 && (s->rows / c) % rw == 0 && s->rows / c / rw <= cluster_max_warps(rw)) {
+        C = c;
+        break;
+      }
+    if (C == 0) continue;
+    ClusterPlan p;
+    p.C = C;
+    p.R = s->rows / C;
+    p.W = w;
+    p.RW = rw;
+    p.smem = (size_t)(w == 4 ? rdcnn_dev::cluster_smem_bytes<4>(p.R) : rdcnn_dev::cluster_smem_bytes<8>(p.R));
+    if (p.smem > 200 * 1024) continue;
+    static int checked[2][5][2][rdcnn_dev::kClusterMax + 1] = {};  // 1 ok, -1 not launchable
+    int& ok = checked[w == 8][rw][fast][C];
+    if (ok == 0) {
+      ClusterFn fn = cluster_fn(w, rw, fast);
+      ok = -1;
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)C);
+        cfg.blockDim = dim3(32u * (unsigned)cluster_max_warps(rw));
+        cfg.dynamicSmemBytes = 200 * 1024;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) == cudaSuccess && n >= 1) ok = 1;
+      }
+      cudaGetLastError();
+    }
+    if (ok != 1) continue;
+    *out = p;
+    return true;
+  }
+  return false;
+}
+
+int cluster_advance(rdcnn_sim* s, const ClusterPlan& pl, long steps, long* first_bad) {
+  if (!s->d_first_bad) RDCNN_CUDA_TRY(cudaMalloc(&s->d_first_bad, sizeof(long long)));
+  rdcnn_dev::ClusterArgs a{};
+  a.u_in = s->u_ptr<float>(s->cur);
+  a.v_in = s->v_ptr<float>(s->cur);
+  a.u_out = s->u_ptr<float>(s->cur ^ 1);
+  a.v_out = s->v_ptr<float>(s->cur ^ 1);
+  a.rows = s->rows;
+  a.cols = s->cols;
+  a.R = pl.R;
+  a.steps = steps;
+  a.p = s->h_params_f;
+  a.first_bad = s->d_first_bad;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)pl.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)pl.C);
+  cfg.blockDim = dim3(32u * (unsigned)(pl.R / pl.RW));
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = s->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
+  RDCNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, cluster_fn(pl.W, pl.RW, s->mode == RDCNN_FAST), a));
+  RDCNN_CUDA_TRY(cudaEventRecord(s->ev1, s->stream));
+  long long fb = 0;
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(&fb, s->d_first_bad, sizeof fb, cudaMemcpyDeviceToHost, s->stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  float ms = 0;
+  RDCNN_CUDA_TRY(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+  s->last_ms = ms;
+  s->launches = 1;
+  s->cur ^= 1;
+  if (first_bad) first_bad[0] = (long)fb;
+  if (fb) return fail(RDCNN_EBLOWUP, "blow-up: non-finite state");
+  return RDCNN_OK;
+}
+
 template <class T>
 int advance_impl(rdcnn_sim* s, long steps, long* first_bad) {
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  if constexpr (sizeof(T) == 4) {
+    ClusterPlan pl;
+    if (steps > 0 && cluster_plan_for(s, &pl)) return cluster_advance(s, pl, steps, first_bad);
+    if (s->cluster_mode > 0) return fail(RDCNN_EINVAL, "persistent cluster path required but %dx%d (batch %d) does not fit it",
+                                         s->rows, s->cols, s->batch);
+  }
   s->launches = 0;
   if (first_bad)
     for (int g = 0; g < s->batch; ++g) first_bad[g] = 0;
@@ -1086,6 +1223,13 @@ int rdcnn_sim_set_tuning(rdcnn_sim_t s, int max_levels, int seg_rows) {
   if (seg_rows < 0) return fail(RDCNN_EINVAL, "seg_rows must be >= 0");
   s->max_levels = max_levels;
   s->seg_rows = seg_rows;
+  return RDCNN_OK;
+}
+
+int rdcnn_sim_set_persistent(rdcnn_sim_t s, int mode) {
+  if (!s) return fail(RDCNN_EINVAL, "null handle");
+  if (mode < -1 || mode > 1) return fail(RDCNN_EINVAL, "mode must be -1, 0 or 1, got %d", mode);
+  s->cluster_mode = mode;
   return RDCNN_OK;
 }
 

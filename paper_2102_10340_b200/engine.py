@@ -187,7 +187,9 @@ class Simulator:
     """Owner of one device state (C-ABI handle): batch x rows x cols, two planes."""
 
     def __init__(self, rows: int, cols: int, batch: int = 1, device: int = 0, mode: str = "strict",
-                 levels: int = 4, seg_rows: int = 0, precision: str = "single"):
+                 levels: int = 4, seg_rows: int = 0, precision: str = "single", persistent: int = 0):
+        """``persistent``: the one-launch cluster path for small single fp32
+        lattices (rdcnn_sim_set_persistent): 0 automatic, 1 required, -1 off."""
         self._lib = load()
         self.rows, self.cols, self.batch, self.device = int(rows), int(cols), int(batch), int(device)
         self.mode = mode
@@ -207,6 +209,7 @@ class Simulator:
             check(self._lib.rdcnn_sim_create(self.rows, self.cols, self.batch, self.device, m, ctypes.byref(h)))
         self._h = h
         self.set_tuning(levels, seg_rows)
+        check(self._lib.rdcnn_sim_set_persistent(self._h, int(persistent)))
         L = self._lib
         self._up = L.rdcnn_sim_upload_f64 if self._f64 else L.rdcnn_sim_upload
         self._down = L.rdcnn_sim_download_f64 if self._f64 else L.rdcnn_sim_download

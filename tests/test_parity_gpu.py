@@ -52,7 +52,7 @@ def test_golden_cases(golden, levels):
     equivalence cases of test_kernels.cpp:141-213, at every fusion depth."""
     for case in golden:
         r, c = case["rows"], case["cols"]
-        with fhn.Simulator(r, c, levels=levels) as sim:
+        with fhn.Simulator(r, c, levels=levels, persistent=-1) as sim:
             sim.set_params(gene_from7(case["gene7"]))
             sim.init(case["typ"], case["seed"])
             u0, v0 = sim.download()
@@ -65,10 +65,34 @@ def test_golden_cases(golden, levels):
                 assert f"{got:016x}" == case["checksum"], (case["name"], levels)
 
 
+def test_golden_cases_persistent_cluster(golden):
+    """The same reference digests through the one-launch cluster path
+    (fhn_cluster.cuh) wherever the shape fits it (256^2, 128^2, ...)."""
+    used = 0
+    for case in golden:
+        r, c = case["rows"], case["cols"]
+        with fhn.Simulator(r, c) as sim:
+            sim.set_params(gene_from7(case["gene7"]))
+            sim.init(case["typ"], case["seed"])
+            bad = sim.advance(case["iters"])
+            assert int(bad[0]) == case["bad_iter"], case["name"]
+            used += sim.launch_count() == 1 and case["iters"] > 4
+            if case["bad_iter"] == 0:
+                u, v = sim.download()
+                assert f"{fhn.checksum(fhn.GridState(r, c, u, v)):016x}" == case["checksum"], case["name"]
+    assert used >= 3  # 256^2 x1000, 128^2 x500, 128^2 x10
+
+
 def test_golden_split_advances(golden):
     """Advancing in uneven chunks (snapshot-style) gives the same digest."""
     case = next(c for c in golden if c["name"] == "kat_crit1_256_typ1_s42_1000")
     with fhn.Simulator(256, 256, levels=8) as sim:
+        sim.init(1, 42)
+        for chunk in (1, 3, 7, 13, 200, 376, 400):
+            assert int(sim.advance(chunk)[0]) == 0
+        u, v = sim.download()
+    assert f"{fhn.checksum(fhn.GridState(256, 256, u, v)):016x}" == case["checksum"]
+    with fhn.Simulator(256, 256, levels=8, persistent=-1) as sim:
         sim.init(1, 42)
         for chunk in (1, 3, 7, 13, 200, 376, 400):
             assert int(sim.advance(chunk)[0]) == 0
@@ -83,6 +107,7 @@ def test_golden_split_advances(golden):
 SHAPES = [
     (3, 3), (3, 4), (4, 3), (5, 7), (11, 11), (17, 23), (32, 48), (9, 128), (128, 128),
     (64, 64), (33, 256), (40, 124), (31, 132), (61, 1000), (200, 36), (257, 120), (96, 512),
+    (256, 256), (100, 256), (3, 128), (7, 128), (48, 256), (13, 256),
 ]
 
 
@@ -94,12 +119,54 @@ def test_random_shapes_vs_oracle(oracle, rows, cols):
     assert obad == 0
     for levels in LEVELS:
         for seg in (0, 1, 5):
-            with fhn.Simulator(rows, cols, levels=levels, seg_rows=seg) as sim:
+            with fhn.Simulator(rows, cols, levels=levels, seg_rows=seg, persistent=-1) as sim:
                 sim.upload(u0, v0)
                 assert int(sim.advance(iters)[0]) == 0
                 u, v = sim.download()
             assert np.array_equal(bits(u), bits(ou)), (rows, cols, levels, seg)
             assert np.array_equal(bits(v), bits(ov)), (rows, cols, levels, seg)
+    # automatic path choice (the persistent cluster where the shape fits)
+    with fhn.Simulator(rows, cols) as sim:
+        sim.upload(u0, v0)
+        assert int(sim.advance(iters)[0]) == 0
+        u, v = sim.download()
+    assert np.array_equal(bits(u), bits(ou)) and np.array_equal(bits(v), bits(ov)), (rows, cols)
+
+
+@pytest.mark.parametrize("rows,cols", [(256, 256), (128, 128), (100, 256), (9, 128), (48, 256)])
+def test_persistent_cluster_path(oracle, rows, cols):
+    """The one-launch cluster path (required, so a silent fallback fails):
+    bit-exact against the oracle; fast mode within the reference's
+    tolerance-class bound; exact blow-up iteration and post-blow-up state."""
+    iters = 301
+    u0, v0 = oracle.init(2, rows, cols, 77 + rows)
+    ou, ov, _ = oracle.run(rows, cols, u0, v0, iters)
+    with fhn.Simulator(rows, cols, persistent=1) as sim:
+        sim.upload(u0, v0)
+        assert int(sim.advance(iters)[0]) == 0
+        assert sim.launch_count() == 1
+        u, v = sim.download()
+    assert np.array_equal(bits(u), bits(ou)) and np.array_equal(bits(v), bits(ov))
+    # blow-up: checkerboard instability, the exact iteration and the state right after it
+    g = fhn.Gene(Du=2.6)
+    _, _, want = oracle.run(rows, cols, u0, v0, 2000, g.to_vector())
+    assert want > 0
+    bu, bv, _ = oracle.run(rows, cols, u0, v0, want, g.to_vector())
+    with fhn.Simulator(rows, cols, persistent=1) as sim:
+        sim.set_params(g)
+        sim.upload(u0, v0)
+        assert int(sim.advance(17)[0]) == 0
+        assert int(sim.advance(5000)[0]) == want - 17
+        u, v = sim.download()
+    assert np.array_equal(np.isfinite(u), np.isfinite(bu))
+    fin = np.isfinite(bu) & np.isfinite(bv)
+    assert np.array_equal(bits(u)[fin], bits(bu)[fin]) and np.array_equal(bits(v)[fin], bits(bv)[fin])
+
+
+def test_persistent_cluster_required_rejects_unfit_shape():
+    with fhn.Simulator(17, 96, persistent=1) as sim:
+        with pytest.raises(fhn.RdcnnError):
+            sim.advance(3)
 
 
 def test_device_init_matches_host_init(oracle):
