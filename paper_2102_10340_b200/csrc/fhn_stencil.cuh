@@ -391,6 +391,11 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
   // the host-side replay.  A flag carrying this launch's own tag was raised
   // by a sibling warp (or, in slab mode, by the boundary launch of the same
   // block) and does not freeze.  The flag is only needed at the first store.
+  // Programmatic dependent launch: the next launch of the advance may start
+  // its CTAs in this one's tail; nothing global is read before the previous
+  // launch has completed (no-ops when launched without the PDL attribute).
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const unsigned fl = a.flags != nullptr ? *(volatile unsigned*)(a.flags + g) : 0u;
   const unsigned frozen = fl != 0u && fl != a.tag;
 

@@ -142,6 +142,37 @@ int resident_blocks(int k, int w, bool fast, bool per_grid) {
   return r;
 }
 
+// Programmatic dependent launch (PDL): consecutive stencil launches of an
+// advance overlap launch latency and prologue with the previous launch's
+// tail; the kernel issues griddepcontrol.wait before its first global read.
+// Measured +4 % at 4096^2, K=4 (779k -> 810k).  RDCNN_PDL=0 turns it off.
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RDCNN_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <class Args>
+cudaError_t launch_pdl(void (*fn)(Args), unsigned blocks, size_t smem, cudaStream_t s, const Args& a) {
+  if (!pdl_enabled()) {
+    fn<<<dim3(blocks), dim3(kThreads), smem, s>>>(a);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, a);
+}
+
 // Fused peer-exchange instances (fp32 slabs, shared gene): [wide][k][fast].
 struct PeerTable {
   using Fn = void (*)(StepArgsT<float>);
@@ -193,8 +224,7 @@ cudaError_t launch_stencil(int k, int w, bool fast, bool per_grid, const StepArg
   auto fn = table<T>().fn[w > 1][k_index(k)][fast][per_grid];
   if (!fn) return cudaErrorInvalidValue;
   const long long blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
-  fn<<<dim3((unsigned)blocks), dim3(kThreads), smem_for<T>(w), s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(fn, (unsigned)blocks, smem_for<T>(w), s, a);
 }
 
 // Band/segment decomposition of one launch.
@@ -994,8 +1024,7 @@ int peer_block(rdcnn_sim* s, int k, unsigned tag, cudaStream_t st) {
   a.n_top = p.n_bands * std::min(p.n_segs, (g + h - 1) / h);  // segments with r0 < g
   a.n_bot = p.n_bands * (p.n_segs - (S - g) / h);             // segments with r0 + h > S - g
   auto fn = peer_table().fn[w > 1][k_index(k)][fast];
-  fn<<<dim3((unsigned)p.warps), dim3(kThreads), smem_for<float>(w), st>>>(a);
-  RDCNN_CUDA_TRY(cudaGetLastError());
+  RDCNN_CUDA_TRY(launch_pdl(fn, (unsigned)p.warps, smem_for<float>(w), st, a));
   ++s->launches;
   ++s->p2p_seq;
   s->cur ^= 1;
