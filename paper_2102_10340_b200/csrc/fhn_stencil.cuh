@@ -216,15 +216,27 @@ __device__ __forceinline__ void store_row(T* __restrict__ u, T* __restrict__ v, 
 }
 
 // One level of one row: out = step(center) given the rows above/below.
-template <int W, class T, bool kFast>
+// kWrap: the band is the whole row (no halo lanes), so lane 0's left
+// neighbour is lane 31 (indexed shuffles with wrap).  Otherwise lanes 0 and
+// 31 are halo lanes whose outer values are stale anyway, and shfl.up/down
+// with an immediate delta need no lane-index registers.
+template <int W, class T, bool kFast, bool kWrap>
 __device__ __forceinline__ void level_row(const Row<W, T>& up, const Row<W, T>& c,
                                           const Row<W, T>& dn, Row<W, T>& out,
                                           const ParamsT<T>& p, T neg_eps, int lane_l,
                                           int lane_r) {
-  const T ul = __shfl_sync(kFull, c.u[W - 1], lane_l);
-  const T ur = __shfl_sync(kFull, c.u[0], lane_r);
-  const T vl = __shfl_sync(kFull, c.v[W - 1], lane_l);
-  const T vr = __shfl_sync(kFull, c.v[0], lane_r);
+  T ul, ur, vl, vr;
+  if constexpr (kWrap) {
+    ul = __shfl_sync(kFull, c.u[W - 1], lane_l);
+    ur = __shfl_sync(kFull, c.u[0], lane_r);
+    vl = __shfl_sync(kFull, c.v[W - 1], lane_l);
+    vr = __shfl_sync(kFull, c.v[0], lane_r);
+  } else {
+    ul = __shfl_up_sync(kFull, c.u[W - 1], 1);
+    ur = __shfl_down_sync(kFull, c.u[0], 1);
+    vl = __shfl_up_sync(kFull, c.v[W - 1], 1);
+    vr = __shfl_down_sync(kFull, c.v[0], 1);
+  }
 #pragma unroll
   for (int k = 0; k < W; ++k) {
     const T u_l = k > 0 ? c.u[k - 1] : ul;
@@ -368,11 +380,13 @@ struct MinBlocks {
 // slot j % 3); the tick loop is unrolled by 3 so every slot index is a
 // compile-time constant and no register is copied to advance a window.
 //
+// kWrap: full-width bands (halo_groups == 0, cols == 32*W), see level_row.
+//
 // kPeer (slab mode): the launch covers every owned row of the slab; warps
 // whose segment reads ghost rows first wait for the neighbour's "delivered"
 // word, store their edge rows into the neighbour's ghosts as well as locally,
 // and publish completion -- the halo exchange is fused into the step.
-template <int K, int W, class T, bool kFast, bool kPerGrid, bool kPeer = false>
+template <int K, int W, class T, bool kFast, bool kPerGrid, bool kPeer = false, bool kWrap = false>
 __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
     fhn_wavefront_kernel(const StepArgsT<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -499,10 +513,10 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
         const Row<W, T>& ce = win[t - 2][(ph + 1) % 3];
         const Row<W, T>& dn = win[t - 2][(ph + 2) % 3];
         if (t < K) {
-          level_row<W, T, kFast>(up, ce, dn, win[t - 1][ph], p, neg_eps, lane_l, lane_r);
+          level_row<W, T, kFast, kWrap>(up, ce, dn, win[t - 1][ph], p, neg_eps, lane_l, lane_r);
         } else {
           Row<W, T> o;
-          level_row<W, T, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
+          level_row<W, T, kFast, kWrap>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
           if (store) {
             store_row<W, T>(du, du + vout_delta, 0, o);
             fold_finite<W, T>(fin, o);
@@ -534,7 +548,7 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
       read_staged<W, T>(half_now + ph * kSlot, dn);
       if constexpr (K == 1) {
         Row<W, T> o;
-        level_row<W, T, kFast>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
+        level_row<W, T, kFast, kWrap>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
         if (store) {
           store_row<W, T>(du, du + vout_delta, 0, o);
           fold_finite<W, T>(fin, o);
@@ -548,7 +562,7 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
         du += pitch;
         if constexpr (kPeer) ++orow;
       } else {
-        level_row<W, T, kFast>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
+        level_row<W, T, kFast, kWrap>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
       }
     }
   };

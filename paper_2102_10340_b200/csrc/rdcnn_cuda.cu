@@ -81,15 +81,18 @@ int k_index(int k) { return k == 1 ? 0 : k == 2 ? 1 : k == 4 ? 2 : 3; }
 template <class T>
 struct KernelTable {
   using Fn = void (*)(StepArgsT<T>);
-  Fn fn[2][4][2][2] = {};        // [wide][k][fast][per_grid]
-  int resident[2][4][2][2] = {};
+  Fn fn[2][4][2][2][2] = {};        // [wide][k][fast][per_grid][wrap]
+  int resident[2][4][2][2][2] = {};
 };
 
 template <class T, int W, int KI, int FI, int PI>
 void fill_one(KernelTable<T>& t) {
   constexpr int K = 1 << KI;
   if constexpr (K <= Traits<T>::kMaxLevels && (FI == 0 || sizeof(T) == 4))
-    t.fn[W > 1][KI][FI][PI] = &rdcnn_dev::fhn_wavefront_kernel<K, W, T, FI == 1, PI == 1>;
+  {
+    t.fn[W > 1][KI][FI][PI][0] = &rdcnn_dev::fhn_wavefront_kernel<K, W, T, FI == 1, PI == 1, false, false>;
+    t.fn[W > 1][KI][FI][PI][1] = &rdcnn_dev::fhn_wavefront_kernel<K, W, T, FI == 1, PI == 1, false, true>;
+  }
 }
 
 template <class T, int W, int KI>
@@ -128,12 +131,12 @@ size_t smem_for(int w) {
 
 // Resident CTAs per SM of one instance (cached; occupancy is immutable).
 template <class T>
-int resident_blocks(int k, int w, bool fast, bool per_grid) {
+int resident_blocks(int k, int w, bool fast, bool per_grid, bool wrap) {
   KernelTable<T>& t = table<T>();
-  int& r = t.resident[w > 1][k_index(k)][fast][per_grid];
+  int& r = t.resident[w > 1][k_index(k)][fast][per_grid][wrap];
   if (r == 0) {
     int n = 0;
-    auto fn = t.fn[w > 1][k_index(k)][fast][per_grid];
+    auto fn = t.fn[w > 1][k_index(k)][fast][per_grid][wrap];
     if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kThreads, smem_for<T>(w)) !=
                    cudaSuccess || n < 1)
       n = 1;
@@ -176,13 +179,14 @@ cudaError_t launch_pdl(void (*fn)(Args), unsigned blocks, size_t smem, cudaStrea
 // Fused peer-exchange instances (fp32 slabs, shared gene): [wide][k][fast].
 struct PeerTable {
   using Fn = void (*)(StepArgsT<float>);
-  Fn fn[2][4][2] = {};
-  int resident[2][4][2] = {};
+  Fn fn[2][4][2][2] = {};  // [wide][k][fast][wrap]
+  int resident[2][4][2][2] = {};
 };
 
 template <int W, int KI, int FI>
 void fill_peer_one(PeerTable& t) {
-  t.fn[W > 1][KI][FI] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI == 1, false, true>;
+  t.fn[W > 1][KI][FI][0] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI == 1, false, true, false>;
+  t.fn[W > 1][KI][FI][1] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI == 1, false, true, true>;
 }
 
 template <int W>
@@ -203,12 +207,12 @@ PeerTable& peer_table() {
   return t;
 }
 
-int peer_resident_blocks(int k, int w, bool fast) {
+int peer_resident_blocks(int k, int w, bool fast, bool wrap) {
   PeerTable& t = peer_table();
-  int& r = t.resident[w > 1][k_index(k)][fast];
+  int& r = t.resident[w > 1][k_index(k)][fast][wrap];
   if (r == 0) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, t.fn[w > 1][k_index(k)][fast], kThreads,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, t.fn[w > 1][k_index(k)][fast][wrap], kThreads,
                                                       smem_for<float>(w)) != cudaSuccess || n < 1)
       n = 1;
     r = n;
@@ -217,11 +221,11 @@ int peer_resident_blocks(int k, int w, bool fast) {
 }
 
 template <class T>
-cudaError_t launch_stencil(int k, int w, bool fast, bool per_grid, const StepArgsT<T>& a,
+cudaError_t launch_stencil(int k, int w, bool fast, bool per_grid, bool wrap, const StepArgsT<T>& a,
                            long long warps, cudaStream_t s) {
   if (warps <= 0) return cudaSuccess;
   if (k != 1 && k != 2 && k != 4 && k != 8) return cudaErrorInvalidValue;
-  auto fn = table<T>().fn[w > 1][k_index(k)][fast][per_grid];
+  auto fn = table<T>().fn[w > 1][k_index(k)][fast][per_grid][wrap];
   if (!fn) return cudaErrorInvalidValue;
   const long long blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
   return launch_pdl(fn, (unsigned)blocks, smem_for<T>(w), s, a);
@@ -556,7 +560,8 @@ cudaError_t launch_range(rdcnn_sim* s, int k, StepArgsT<T> a, int row_begin, int
   const int w = width_for<T>(s);
   const bool fast = s->mode == RDCNN_FAST;
   const bool per_grid = a.params_stride != 0;
-  const int rw = resident_blocks<T>(k, w, fast, per_grid) * (kThreads / 32);
+  const bool wrap = s->cols / w == 32;  // full-width bands (make_plan: halo 0)
+  const int rw = resident_blocks<T>(k, w, fast, per_grid, wrap) * (kThreads / 32);
   Plan p = make_plan(s->cols, w, k, a.batch, row_begin, row_end, s->seg_rows, s->sm_count, rw);
   if (p.warps == 0) return cudaSuccess;
   a.row_begin = row_begin;
@@ -567,7 +572,7 @@ cudaError_t launch_range(rdcnn_sim* s, int k, StepArgsT<T> a, int row_begin, int
   a.band_groups = p.band_groups;
   a.halo_groups = p.halo;
   ++s->launches;
-  return launch_stencil<T>(k, w, fast, per_grid, a, p.warps, st);
+  return launch_stencil<T>(k, w, fast, per_grid, wrap, a, p.warps, st);
 }
 
 int alloc_common(rdcnn_sim* s) {
@@ -1011,7 +1016,8 @@ int peer_block(rdcnn_sim* s, int k, unsigned tag, cudaStream_t st) {
   a.seq = s->p2p_seq;
   const int w = width_for<float>(s);
   const bool fast = s->mode == RDCNN_FAST;
-  const int rw = peer_resident_blocks(k, w, fast) * (kThreads / 32);
+  const bool wrap = s->cols / w == 32;
+  const int rw = peer_resident_blocks(k, w, fast, wrap) * (kThreads / 32);
   const Plan p = make_plan(s->cols, w, k, 1, 0, s->rows, s->seg_rows, s->sm_count, rw);
   a.row_begin = 0;
   a.row_end = s->rows;
@@ -1023,7 +1029,7 @@ int peer_block(rdcnn_sim* s, int k, unsigned tag, cudaStream_t st) {
   const int h = p.seg_rows, S = s->rows, g = s->ghost;
   a.n_top = p.n_bands * std::min(p.n_segs, (g + h - 1) / h);  // segments with r0 < g
   a.n_bot = p.n_bands * (p.n_segs - (S - g) / h);             // segments with r0 + h > S - g
-  auto fn = peer_table().fn[w > 1][k_index(k)][fast];
+  auto fn = peer_table().fn[w > 1][k_index(k)][fast][wrap];
   RDCNN_CUDA_TRY(launch_pdl(fn, (unsigned)p.warps, smem_for<float>(w), st, a));
   ++s->launches;
   ++s->p2p_seq;
