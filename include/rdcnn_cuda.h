@@ -125,6 +125,12 @@ int rdcnn_sim_set_tuning(rdcnn_sim_t sim, int max_levels, int seg_rows);
  * exact per-step blow-up stop.  mode 0: automatic (default), 1: required
  * (advance fails with RDCNN_EINVAL when the shape does not fit), -1: off. */
 int rdcnn_sim_set_persistent(rdcnn_sim_t sim, int mode);
+/* Profiling: one K-level launch over the whole state with per-warp tracing;
+ * host_trace receives {start ns, end ns, smid} per warp (globaltimer), cap
+ * entries at most; *n_warps = warps launched.  Advances the state by
+ * `levels` iterations. */
+int rdcnn_sim_trace_launch(rdcnn_sim_t sim, int levels, unsigned long long* host_trace,
+                           long long cap, long long* n_warps);
 /* The handle's CUDA stream (cudaStream_t) for interop with other libraries. */
 int rdcnn_sim_stream(rdcnn_sim_t sim, void** stream);
 /* Device pointers of the current front planes (plane u, plane v; float or

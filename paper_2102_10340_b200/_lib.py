@@ -13,7 +13,8 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_long, c_size_t, c_uint, c_uint8, c_uint32, c_uint64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librdcnn_cuda.so")
+# RDCNN_LIB: load another build of the extension (A/B measurements only).
+LIB_PATH = os.environ.get("RDCNN_LIB") or os.path.join(HERE, "librdcnn_cuda.so")
 
 RDCNN_OK, RDCNN_EINVAL, RDCNN_EBLOWUP, RDCNN_ECUDA = 0, 1, 2, 3
 RDCNN_STRICT, RDCNN_FAST = 0, 1
@@ -71,6 +72,8 @@ SIGNATURES = {
     "rdcnn_sim_launch_count": (c_int, [c_void_p, POINTER(c_long)]),
     "rdcnn_sim_set_tuning": (c_int, [c_void_p, c_int, c_int]),
     "rdcnn_sim_set_persistent": (c_int, [c_void_p, c_int]),
+    "rdcnn_sim_trace_launch": (c_int, [c_void_p, c_int, c_void_p, ctypes.c_longlong,
+                                       POINTER(ctypes.c_longlong)]),
     "rdcnn_sim_stream": (c_int, [c_void_p, POINTER(c_void_p)]),
     "rdcnn_sim_device_state": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p)]),
     "rdcnn_slab_create": (c_int, [c_int, c_int, c_int, c_int, c_int, POINTER(c_void_p)]),

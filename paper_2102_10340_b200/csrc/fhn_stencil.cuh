@@ -81,6 +81,8 @@ struct StepArgsT {
   const unsigned* ready;  // [2] this rank's "top / bottom ghosts delivered" words
   unsigned seq;           // block number: this block's ghosts are in when ready[] >= seq
   int n_top, n_bot;       // warps whose segment touches the top / bottom `ghost` rows
+  // Profiling only (rdcnn_sim_trace_launch): per warp {start ns, end ns, smid}.
+  unsigned long long* trace;
 };
 using StepArgs = StepArgsT<float>;
 
@@ -395,6 +397,8 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
   const long long warp_id = (long long)blockIdx.x * kWarpsPerCta + wib;
   const long long per_grid = (long long)a.n_segs * a.n_bands;
   if (warp_id >= per_grid * a.batch) return;
+  unsigned long long t_start = 0;
+  if (a.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const int g = int(warp_id / per_grid);
   const int rem = int(warp_id - (long long)g * per_grid);
   const int band = rem % a.n_bands;
@@ -590,6 +594,15 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
   stage_wait<0>();
 
   if (fin.bad_in_warp() && lane == 0 && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);
+  if (a.trace != nullptr && lane == 0) {
+    unsigned long long t_end;
+    unsigned smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    a.trace[3 * warp_id] = t_start;
+    a.trace[3 * warp_id + 1] = t_end;
+    a.trace[3 * warp_id + 2] = smid;
+  }
 
   if constexpr (kPeer) {
     if (top_edge || bot_edge) {

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -275,6 +276,27 @@ Plan make_plan(int cols, int w, int k, int batch, int row_begin, int row_end,
   p.seg_rows = h;
   p.n_segs = (nrows + h - 1) / h;
   p.warps = (long long)p.n_segs * p.n_bands * batch;
+  // Never spill long segments into a second wave: warps beyond the resident
+  // slots start only when a slot frees.  A short last segment (the runt
+  // row range, at most a third of h) may overflow -- its warps finish early
+  // and the overflow fills their slots (4096^2: 68 x 35 warps, runt 9 rows,
+  // measured faster than 67 segments).  Otherwise use floor(slots/per_seg)
+  // segments (8192^2: 2415 -> 2346 warps, 763k -> 825k Mcell-updates/s).
+  if (seg_override <= 0) {
+    const long long slots = (long long)std::max(sm_count, 1) * std::max(resident_warps_per_sm, 4);
+    const long long per_seg = (long long)batch * p.n_bands;
+    const long long over = p.warps - slots;
+    const int h_last = nrows - (p.n_segs - 1) * p.seg_rows;
+    if (over > 0 && p.warps < 2 * slots && !(h_last * 3 <= p.seg_rows && over <= per_seg)) {
+      const long long segs = slots / per_seg;
+      if (segs >= 1) {
+        const int h2 = (int)((nrows + segs - 1) / segs);
+        p.seg_rows = h2;
+        p.n_segs = (nrows + h2 - 1) / h2;
+        p.warps = (long long)p.n_segs * per_seg;
+      }
+    }
+  }
   return p;
 }
 
@@ -1258,6 +1280,45 @@ int rdcnn_sim_set_tuning(rdcnn_sim_t s, int max_levels, int seg_rows) {
   if (seg_rows < 0) return fail(RDCNN_EINVAL, "seg_rows must be >= 0");
   s->max_levels = max_levels;
   s->seg_rows = seg_rows;
+  return RDCNN_OK;
+}
+
+int rdcnn_sim_trace_launch(rdcnn_sim_t s, int levels, unsigned long long* host_trace, long long cap,
+                           long long* n_warps) {
+  if (!s || !host_trace || !n_warps || s->slab) return fail(RDCNN_EINVAL, "bad argument");
+  if (levels != 1 && levels != 2 && levels != 4 && levels != 8) return fail(RDCNN_EINVAL, "bad levels");
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  const int w = s->elem == 4 ? width_for<float>(s) : width_for<double>(s);
+  const bool fast = s->mode == RDCNN_FAST;
+  const bool per_grid = s->params_stride != 0;
+  const bool wrap = s->cols / w == 32;
+  const int rw = (s->elem == 4 ? resident_blocks<float>(levels, w, fast, per_grid, wrap)
+                               : resident_blocks<double>(levels, w, fast, per_grid, wrap)) * (kThreads / 32);
+  const Plan p = make_plan(s->cols, w, levels, s->batch, 0, s->rows, s->seg_rows, s->sm_count, rw);
+  *n_warps = p.warps;
+  if (p.warps > cap) return fail(RDCNN_EINVAL, "trace needs %lld entries", (long long)p.warps);
+  unsigned long long* d = nullptr;
+  RDCNN_CUDA_TRY(cudaMalloc(&d, sizeof(unsigned long long) * 3 * (size_t)p.warps));
+  int rc = RDCNN_OK;
+  if (s->elem == 4) {
+    StepArgsT<float> a = base_args<float>(s, s->cur, s->cur ^ 1);
+    a.trace = d;
+    a.tag = 1;
+    rc = launch_range<float>(s, levels, a, 0, s->rows, s->stream) == cudaSuccess ? RDCNN_OK : RDCNN_ECUDA;
+  } else {
+    StepArgsT<double> a = base_args<double>(s, s->cur, s->cur ^ 1);
+    a.trace = d;
+    a.tag = 1;
+    rc = launch_range<double>(s, levels, a, 0, s->rows, s->stream) == cudaSuccess ? RDCNN_OK : RDCNN_ECUDA;
+  }
+  if (rc == RDCNN_OK) {
+    s->cur ^= 1;
+    RDCNN_CUDA_TRY(cudaMemcpyAsync(host_trace, d, sizeof(unsigned long long) * 3 * (size_t)p.warps,
+                                   cudaMemcpyDeviceToHost, s->stream));
+    RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  }
+  cudaFree(d);
+  if (rc != RDCNN_OK) return fail(rc, "trace launch failed");
   return RDCNN_OK;
 }
 

@@ -13,7 +13,10 @@ ap.add_argument("--iters", type=int, default=2000)
 ap.add_argument("--levels", default="1,2,4,8")
 ap.add_argument("--segs", default="0")
 ap.add_argument("--mode", default="strict")
+ap.add_argument("--lib", default=None, help="load this build of the extension instead (A/B runs)")
 a = ap.parse_args()
+if a.lib:
+    fhn._lib.load(a.lib)
 for lv in [int(x) for x in a.levels.split(",")]:
     for sg in [int(x) for x in a.segs.split(",")]:
         with fhn.Simulator(a.rows, a.cols, a.batch, levels=lv, seg_rows=sg, mode=a.mode) as sim:
