@@ -83,10 +83,36 @@ __device__ __forceinline__ void lds_v4(uint32_t addr, float& a, float& b, float&
                : "memory");
 }
 
-// Bytes of dynamic shared memory for R rows per CTA.
+// Asynchronous DSMEM store that counts its bytes on the RECEIVER's mbarrier
+// (complete_tx): the receiver learns the halo row has landed by waiting on
+// its own barrier, with no memory fence on either side.
+__device__ __forceinline__ void stas_v4(uint32_t addr, float a, float b, float c, float d, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];\n"
+               ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t mbar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t mbar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t mbar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(mbar), "r"(parity)
+      : "memory");
+}
+
+// Bytes of dynamic shared memory for R rows per CTA: 32-byte header (two
+// flag words, two mbarriers) + the exchange rows.
 template <int W>
 constexpr int cluster_smem_bytes(int R) {
-  return 16 + 2 * (R + 2) * 2 * W * 32 * 4;
+  return 32 + 2 * (R + 2) * 2 * W * 32 * 4;
 }
 
 template <int W>
@@ -99,12 +125,13 @@ __device__ __forceinline__ void publish_row(uint32_t addr, const float (&u)[W], 
   }
 }
 template <int W>
-__device__ __forceinline__ void publish_row_remote(uint32_t addr, const float (&u)[W], const float (&v)[W]) {
+__device__ __forceinline__ void publish_row_remote(uint32_t addr, const float (&u)[W], const float (&v)[W],
+                                                   uint32_t mbar) {
   constexpr uint32_t kPlane = W / 4 * 32 * 16;
 #pragma unroll
   for (int c = 0; c < W / 4; ++c) {
-    st_cluster_v4(addr + c * 512, u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
-    st_cluster_v4(addr + c * 512 + kPlane, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    stas_v4(addr + c * 512, u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3], mbar);
+    stas_v4(addr + c * 512 + kPlane, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3], mbar);
   }
 }
 template <int W>
@@ -163,7 +190,8 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
 
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem_raw);
   const uint32_t flags = base;        // two u32 flags (step parity)
-  const uint32_t X = base + 16;       // exchange rows, local row i at X + i*kRow
+  const uint32_t mbar = base + 16;    // two mbarriers (step parity): this CTA's halo rows landed
+  const uint32_t X = base + 32;       // exchange rows, local row i at X + i*kRow
   const uint32_t par_bytes = (uint32_t)(R + 2) * kRow;
   const uint32_t lane_off = (uint32_t)lane * 16;
   const uint32_t my_first = X + (uint32_t)(1 + warp * RW) * kRow + lane_off;
@@ -171,10 +199,11 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
   const uint32_t above = my_first - kRow;  // the previous warp's last row (or the top halo)
   const uint32_t below = my_last + kRow;   // the next warp's first row (or the bottom halo)
   // Ring: the CTA's first row -> prev CTA's bottom halo (row R+1); its last
-  // row -> next CTA's top halo (row 0).
+  // row -> next CTA's top halo (row 0); each counted on the receiver's mbarrier.
   const unsigned prev = (crank + C - 1) % C, next = (crank + 1) % C;
   const uint32_t to_prev = mapa_shared(X + (uint32_t)(R + 1) * kRow + lane_off, prev);
   const uint32_t to_next = mapa_shared(X + lane_off, next);
+  const uint32_t mbar_prev = mapa_shared(mbar, prev), mbar_next = mapa_shared(mbar, next);
   const bool cta_first = warp == 0, cta_last = warp == nw - 1;
 
   float u[RW][W], v[RW][W];
@@ -191,29 +220,44 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
   }
   if (threadIdx.x == 0) {
     asm volatile("st.shared.v2.u32 [%0], {%1, %1};\n" ::"r"(flags), "r"(0u) : "memory");
+    mbar_init(mbar, 1);
+    mbar_init(mbar + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  cluster_barrier();  // flags zeroed and every CTA of the cluster running before any DSMEM store
+  cluster_barrier();  // flags and mbarriers ready in every CTA before any DSMEM store
 
   Finite<float> fin;
   long long done = 0;
   for (; done < a.steps; ++done) {
     const uint32_t par = (uint32_t)(done & 1) * par_bytes;
-    // 1. publish the warp's edge rows (the CTA's edge rows also to the ring neighbours)
+    const uint32_t mb = (uint32_t)(done & 1) * 8u;  // this step's mbarrier
+    // Arm this step's phase: the two halo rows (prev's last, next's first).
+    // Their bytes may land before or after this arrive; the phase completes
+    // on both.
+    if (threadIdx.x == 0) mbar_arrive_expect_tx(mbar + mb, 2u * kRow);
+    // 1. publish the warp's edge rows (the CTA's edge rows to the ring neighbours)
     publish_row<W>(my_first + par, u[0], v[0]);
     if (RW > 1) publish_row<W>(my_last + par, u[RW - 1], v[RW - 1]);
-    if (cta_first) publish_row_remote<W>(to_prev + par, u[0], v[0]);
-    if (cta_last) publish_row_remote<W>(to_next + par, u[RW - 1], v[RW - 1]);
-    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    if (cta_first) publish_row_remote<W>(to_prev + par, u[0], v[0], mbar_prev + mb);
+    if (cta_last) publish_row_remote<W>(to_next + par, u[RW - 1], v[RW - 1], mbar_next + mb);
+    // Sibling warps read the local rows: CTA-scope ordering.  The cluster
+    // barrier only orders EXECUTION (a neighbour overwrites this parity's
+    // halo rows two steps later, after everyone has read them).
+    asm volatile("fence.acq_rel.cta;\n" ::: "memory");
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     // 2. interior rows need only this warp's registers: overlap the barrier
     float un[RW][W], vn[RW][W];
 #pragma unroll
     for (int r = 1; r < RW - 1; ++r)
       cluster_row<W, kFast>(u[r - 1], v[r - 1], u[r], v[r], u[r + 1], v[r + 1], un[r], vn[r], p, neg_eps, lane_l,
                             lane_r);
-    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+    // The CTA's edge warps read the halo rows: wait until both have landed
+    // (also before a blow-up stop, so no async store is in flight at exit).
+    if (cta_first || cta_last) mbar_wait_parity(mbar + mb, (unsigned)((done >> 1) & 1));
     // The previous step's blow-up flag: every CTA sees the same value here
-    // (written before this barrier's arrive; the next write to this parity
-    // comes after the next barrier).
+    // (written and fenced before this barrier's arrive; the next write to
+    // this parity comes after the next barrier).
     if (done > 0) {
       unsigned f;
       asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(f) : "r"(flags + 4u * (uint32_t)((done - 1) & 1)) : "memory");
@@ -240,9 +284,12 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
         v[r][k] = vn[r][k];
         fin.add(un[r][k], vn[r][k]);
       }
-    if (fin.bad_in_warp() && lane == 0) {
-      const uint32_t fl = flags + 4u * (uint32_t)(done & 1);
-      for (unsigned c = 0; c < C; ++c) st_cluster_u32(mapa_shared(fl, c), 1u);
+    if (fin.bad_in_warp()) {  // rare: publish the stop to every CTA at cluster scope
+      if (lane == 0) {
+        const uint32_t fl = flags + 4u * (uint32_t)(done & 1);
+        for (unsigned c = 0; c < C; ++c) st_cluster_u32(mapa_shared(fl, c), 1u);
+      }
+      asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
     }
   }
   // The last computed step's flag (or the one that stopped the loop).
