@@ -7,20 +7,23 @@
 // the state lives in registers for all `steps` iterations.  Per step:
 //   1. each warp publishes its first and last row (u, v) into the CTA's
 //      shared exchange rows of this step's parity; the CTA's first/last row
-//      also goes into the previous/next CTA's halo row (DSMEM: mapa +
-//      st.shared::cluster), closing the torus ring across the cluster;
-//   2. cluster barrier ARRIVE (release); the warp's interior rows (1..RW-2)
-//      need only its own registers and are computed while the barrier
-//      completes; then WAIT (acquire);
+//      also goes into the previous/next CTA's halo row by st.async, whose
+//      bytes are counted on the RECEIVER's mbarrier (complete_tx) -- the
+//      torus ring across the cluster;
+//   2. each warp arrives (release) on this parity's mbarrier, computes its
+//      interior rows (1..RW-2, registers only) and then waits on it: the
+//      barrier completes when all warps of the CTA have published and both
+//      halo rows have landed.  There is no per-step cluster barrier and no
+//      GPU-scope fence: a CTA synchronises only with its ring neighbours;
 //   3. the edge rows: up/down rows from shared memory, left/right columns
 //      from warp shuffles (the row wraps around the warp: the torus column
 //      wrap), the reference cell update (fhn_cell, strict or fast).
-// Non-finite results set a per-parity flag word in EVERY CTA (remote stores,
-// only on blow-up); all CTAs read their local copy after the next barrier and
-// stop together, holding the post-blow-up state, so the exact iteration is
-// known without a replay (engine.hpp:79, BlowUpError(iter+1)).
+// Blow-up: each warp records the first step whose output it saw non-finite
+// (atomicMin); the host re-runs exactly that many steps from the call's
+// input (kept: output goes to the other buffer), leaving the post-blow-up
+// state and the exact iteration (engine.hpp:79, BlowUpError(iter+1)).
 //
-// Shared memory layout per CTA: [flag0, flag1, pad, pad] then
+// Shared memory layout per CTA: two local mbarriers, two halo mbarriers, then
 // X[2 parities][R + 2 rows][2 planes][W/4 chunks][32 lanes] float4 -- chunk-
 // major so each STS.128/LDS.128 of a warp is 512 contiguous bytes (no bank
 // conflicts).  Row 0 is the top halo, rows 1..R the CTA's own (only each
@@ -40,7 +43,7 @@ struct ClusterArgs {
   int R;                 // rows per CTA (= warps per CTA x rows per warp)
   long long steps;
   ParamsT<float> p;
-  long long* first_bad;  // 0, or the 1-based iteration whose output went non-finite
+  long long* first_bad;  // preset to all-ones; atomicMin of the 1-based first non-finite step
 };
 
 constexpr int kClusterMax = 16;
@@ -97,6 +100,16 @@ __device__ __forceinline__ void mbar_init(uint32_t mbar, unsigned count) {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t mbar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_wait_parity_cta(uint32_t mbar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAITC_%=;\n"
+      "}\n" ::"r"(mbar), "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait_parity(uint32_t mbar, unsigned parity) {
   asm volatile(
       "{\n"
@@ -108,8 +121,8 @@ __device__ __forceinline__ void mbar_wait_parity(uint32_t mbar, unsigned parity)
       : "memory");
 }
 
-// Bytes of dynamic shared memory for R rows per CTA: 32-byte header (two
-// flag words, two mbarriers) + the exchange rows.
+// Bytes of dynamic shared memory for R rows per CTA: 32-byte header (four
+// mbarriers) + the exchange rows.
 template <int W>
 constexpr int cluster_smem_bytes(int R) {
   return 32 + 2 * (R + 2) * 2 * W * 32 * 4;
@@ -189,8 +202,8 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
   const int lane_l = (lane + 31) & 31, lane_r = (lane + 1) & 31;
 
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem_raw);
-  const uint32_t flags = base;        // two u32 flags (step parity)
-  const uint32_t mbar = base + 16;    // two mbarriers (step parity): this CTA's halo rows landed
+  const uint32_t lbar = base;         // two mbarriers (step parity): the CTA's own rows are in
+  const uint32_t mbar = base + 16;    // two mbarriers (step parity): both halo rows landed
   const uint32_t X = base + 32;       // exchange rows, local row i at X + i*kRow
   const uint32_t par_bytes = (uint32_t)(R + 2) * kRow;
   const uint32_t lane_off = (uint32_t)lane * 16;
@@ -218,51 +231,49 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
       v[r][k] = y.x; v[r][k + 1] = y.y; v[r][k + 2] = y.z; v[r][k + 3] = y.w;
     }
   }
+  // Per parity: lbar completes when all nw warps of this CTA have published
+  // (arrive, release); mbar when both halo rows' bytes have landed
+  // (complete_tx from the ring neighbours' st.async; armed by thread 0).
   if (threadIdx.x == 0) {
-    asm volatile("st.shared.v2.u32 [%0], {%1, %1};\n" ::"r"(flags), "r"(0u) : "memory");
+    mbar_init(lbar, (unsigned)nw);
+    mbar_init(lbar + 8, (unsigned)nw);
     mbar_init(mbar, 1);
     mbar_init(mbar + 8, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  cluster_barrier();  // flags and mbarriers ready in every CTA before any DSMEM store
+  cluster_barrier();  // mbarriers ready in every CTA before any DSMEM store
 
+  // Dataflow, no per-step cluster barrier: a CTA waits only for its own warps
+  // and its two ring neighbours.  Write-after-read safety with one step of
+  // slack: the rows of parity p are rewritten at step n+2 only by a writer
+  // that has waited at step n+1 for data its readers publish after finishing
+  // step n (siblings: all nw arrivals; a neighbour: this CTA's edge row,
+  // published by the very warp that read the halo).
   Finite<float> fin;
-  long long done = 0;
-  for (; done < a.steps; ++done) {
+  bool flagged = false;
+  for (long long done = 0; done < a.steps; ++done) {
     const uint32_t par = (uint32_t)(done & 1) * par_bytes;
-    const uint32_t mb = (uint32_t)(done & 1) * 8u;  // this step's mbarrier
-    // Arm this step's phase: the two halo rows (prev's last, next's first).
-    // Their bytes may land before or after this arrive; the phase completes
-    // on both.
-    if (threadIdx.x == 0) mbar_arrive_expect_tx(mbar + mb, 2u * kRow);
+    const uint32_t pb = (uint32_t)(done & 1) * 8u;
+    const uint32_t lb = lbar + pb, mb = mbar + pb;  // this step's barriers
     // 1. publish the warp's edge rows (the CTA's edge rows to the ring neighbours)
     publish_row<W>(my_first + par, u[0], v[0]);
     if (RW > 1) publish_row<W>(my_last + par, u[RW - 1], v[RW - 1]);
-    if (cta_first) publish_row_remote<W>(to_prev + par, u[0], v[0], mbar_prev + mb);
-    if (cta_last) publish_row_remote<W>(to_next + par, u[RW - 1], v[RW - 1], mbar_next + mb);
-    // Sibling warps read the local rows: CTA-scope ordering.  The cluster
-    // barrier only orders EXECUTION (a neighbour overwrites this parity's
-    // halo rows two steps later, after everyone has read them).
-    asm volatile("fence.acq_rel.cta;\n" ::: "memory");
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
-    // 2. interior rows need only this warp's registers: overlap the barrier
+    if (cta_first) publish_row_remote<W>(to_prev + par, u[0], v[0], mbar_prev + (mb - mbar));
+    if (cta_last) publish_row_remote<W>(to_next + par, u[RW - 1], v[RW - 1], mbar_next + (mb - mbar));
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(lb) : "memory");
+      if (warp == 0) mbar_arrive_expect_tx(mb, 2u * kRow);  // arms the two halo rows' bytes
+    }
+    // 2. interior rows need only this warp's registers: overlap the wait
     float un[RW][W], vn[RW][W];
 #pragma unroll
     for (int r = 1; r < RW - 1; ++r)
       cluster_row<W, kFast>(u[r - 1], v[r - 1], u[r], v[r], u[r + 1], v[r + 1], un[r], vn[r], p, neg_eps, lane_l,
                             lane_r);
-    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
-    // The CTA's edge warps read the halo rows: wait until both have landed
-    // (also before a blow-up stop, so no async store is in flight at exit).
-    if (cta_first || cta_last) mbar_wait_parity(mbar + mb, (unsigned)((done >> 1) & 1));
-    // The previous step's blow-up flag: every CTA sees the same value here
-    // (written and fenced before this barrier's arrive; the next write to
-    // this parity comes after the next barrier).
-    if (done > 0) {
-      unsigned f;
-      asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(f) : "r"(flags + 4u * (uint32_t)((done - 1) & 1)) : "memory");
-      if (f) break;
-    }
+    const unsigned phase = (unsigned)((done >> 1) & 1);
+    mbar_wait_parity_cta(lb, phase);
+    if (cta_first || cta_last) mbar_wait_parity(mb, phase);
     // 3. edge rows with the neighbours' rows from shared memory
     {
       float ua[W], va[W], ub[W], vb[W];
@@ -284,21 +295,16 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
         v[r][k] = vn[r][k];
         fin.add(un[r][k], vn[r][k]);
       }
-    if (fin.bad_in_warp()) {  // rare: publish the stop to every CTA at cluster scope
-      if (lane == 0) {
-        const uint32_t fl = flags + 4u * (uint32_t)(done & 1);
-        for (unsigned c = 0; c < C; ++c) st_cluster_u32(mapa_shared(fl, c), 1u);
-      }
-      asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
+    // Blow-up: record the first step whose output went non-finite (exact per
+    // warp; the minimum over warps is the lattice's).  The run continues --
+    // stopping would need every CTA to agree on the step -- and the host
+    // re-runs exactly that many steps from the untouched input.
+    if (!flagged && fin.bad_in_warp()) {
+      flagged = true;
+      if (lane == 0) atomicMin(reinterpret_cast<unsigned long long*>(a.first_bad), (unsigned long long)(done + 1));
     }
   }
-  // The last computed step's flag (or the one that stopped the loop).
   cluster_barrier();
-  if (done > 0 && threadIdx.x == 0 && crank == 0) {
-    unsigned f;
-    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(f) : "r"(flags + 4u * (uint32_t)((done - 1) & 1)) : "memory");
-    *a.first_bad = f ? done : 0;
-  }
 #pragma unroll
   for (int r = 0; r < RW; ++r) {
     const size_t off = (size_t)(grow0 + r) * a.cols + (size_t)lane * W;

@@ -837,8 +837,10 @@ int cluster_advance(rdcnn_sim* s, const ClusterPlan& pl, long steps, long* first
   cfg.stream = s->stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ClusterFn fn = cluster_fn(pl.W, pl.RW, s->mode == RDCNN_FAST);
+  RDCNN_CUDA_TRY(cudaMemsetAsync(s->d_first_bad, 0xFF, sizeof(long long), s->stream));
   RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
-  RDCNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, cluster_fn(pl.W, pl.RW, s->mode == RDCNN_FAST), a));
+  RDCNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, a));
   RDCNN_CUDA_TRY(cudaEventRecord(s->ev1, s->stream));
   long long fb = 0;
   RDCNN_CUDA_TRY(cudaMemcpyAsync(&fb, s->d_first_bad, sizeof fb, cudaMemcpyDeviceToHost, s->stream));
@@ -847,6 +849,16 @@ int cluster_advance(rdcnn_sim* s, const ClusterPlan& pl, long steps, long* first
   RDCNN_CUDA_TRY(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
   s->last_ms = ms;
   s->launches = 1;
+  if (fb > 0 && fb <= steps) {
+    // Re-run exactly fb steps from the untouched input (cur): the output is
+    // the state right after the first non-finite step.
+    a.steps = fb;
+    RDCNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, a));
+    RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+    s->launches = 2;
+  } else {
+    fb = 0;
+  }
   s->cur ^= 1;
   if (first_bad) first_bad[0] = (long)fb;
   if (fb) return fail(RDCNN_EBLOWUP, "blow-up: non-finite state");
