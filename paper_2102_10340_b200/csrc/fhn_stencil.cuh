@@ -312,6 +312,64 @@ __device__ __forceinline__ void read_staged(uint32_t src, Row<W, T>& r) {
   }
 }
 
+// ---- TMA bulk staging (fp32, W = 4) ------------------------------------------
+// A warp's band row is 32 lanes x 16 bytes = 512 contiguous bytes per plane
+// (two pieces where the band wraps around the torus edge), so lane 0 stages
+// it with cp.async.bulk (the TMA engine) and the completion is counted on a
+// per-slot mbarrier; every lane waits on the barrier instead of its own
+// cp.async group.  Built with -DRDCNN_BULK=1 only: measured 6 % SLOWER than
+// per-lane cp.async (4096^2: 785k vs 833k; batched 128^2: 876k vs 932k) --
+// the elected copy, expect_tx and per-slot waits cost more issue slots than
+// two LDGSTS per lane in an issue-bound kernel (profiles/README.md).
+#ifndef RDCNN_BULK
+#define RDCNN_BULK 0
+#endif
+template <int W, class T>
+struct BulkStage {
+  static constexpr bool value = RDCNN_BULK && W == 4 && sizeof(T) == 4;
+};
+
+// One elected lane: arm the slot's barrier with the row's 1024 bytes and
+// issue the bulk copies of both planes.  All operands are warp-uniform
+// (derived from blockIdx and kernel parameters), so they live in uniform
+// registers and each copy is one UBLKCP.  The slot being recycled was last
+// read (LDS) one tick earlier by this same warp and those values have been
+// consumed, so no proxy fence is needed for the write-after-read.
+__device__ __forceinline__ bool elect_one() {
+  unsigned p;
+  asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(p));
+  return p != 0;
+}
+__device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+template <class T>
+__device__ __forceinline__ void bulk_stage_row(uint32_t dst, const T* su, ptrdiff_t vdelta, uint32_t bytes_a,
+                                               ptrdiff_t d_b, uint32_t bytes_b, uint32_t mbar) {
+  if (elect_one()) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 1024;\n" ::"r"(mbar) : "memory");
+    bulk_copy(dst, su, bytes_a, mbar);
+    bulk_copy(dst + 512u, su + vdelta, bytes_a, mbar);
+    if (bytes_b != 0) {
+      bulk_copy(dst + bytes_a, su + d_b, bytes_b, mbar);
+      bulk_copy(dst + 512u + bytes_a, su + vdelta + d_b, bytes_b, mbar);
+    }
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void bulk_wait(uint32_t mbar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "BW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra BW_%=;\n"
+      "}\n" ::"r"(mbar), "r"(parity)
+      : "memory");
+}
+
 // ---- peer ring synchronisation (kPeer) --------------------------------------
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   unsigned v;
@@ -336,10 +394,10 @@ __device__ __forceinline__ void edge_done(unsigned* count, int n, unsigned* sig,
   }
 }
 
-// Shared memory per CTA of the wavefront kernel.
+// Shared memory per CTA of the wavefront kernel (+ the bulk-staging barriers).
 template <int W, class T>
 constexpr int wavefront_smem_bytes(int warps) {
-  return warps * kStage * 2 * 32 * int(sizeof(T)) * W;
+  return warps * (kStage * 2 * 32 * int(sizeof(T)) * W + (BulkStage<W, T>::value ? 64 : 0));
 }
 
 template <int V>
@@ -480,17 +538,54 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
 
   constexpr uint32_t kLaneBytes = uint32_t(sizeof(T)) * W;
   constexpr uint32_t kSlot = 2 * 32 * kLaneBytes;  // bytes of one staged row (u,v)
-  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem_raw) +
-                        (uint32_t)wib * (kStage * kSlot) + lane * kLaneBytes;
+  constexpr bool kBulk = BulkStage<W, T>::value;
+  constexpr uint32_t kWarpSmem = kStage * kSlot + (kBulk ? 64u : 0u);
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)wib * kWarpSmem +
+                        lane * kLaneBytes;
+  // Bulk staging works on warp-uniform quantities only: the band row starts
+  // at lane 0's column group; a band that wraps the torus edge has a second
+  // piece starting at group 0.  Slot s's barrier is at mbar0 + 8*s.
+  const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)wib * kWarpSmem;
+  const uint32_t mbar0 = ring0 + kStage * kSlot;
+  uint32_t bytes_a = 32u * kLaneBytes, bytes_b = 0;
+  ptrdiff_t d_b = 0;
+  const T* ub = nullptr;  // uniform running source row (lane 0's group)
+  if constexpr (kBulk) {
+    const int gl0 = band * a.band_groups - a.halo_groups;  // lane 0's column group
+    const int grp0 = wrap_index(gl0, G);
+    int na = 32;
+    if (gl0 < 0) na = -gl0;
+    else if (gl0 + 32 > G) na = G - gl0;
+    bytes_a = (uint32_t)na * kLaneBytes;
+    bytes_b = 32u * kLaneBytes - bytes_a;
+    d_b = -(ptrdiff_t)grp0 * W;  // group 0 relative to lane 0's group
+    ub = a.u_in + (size_t)g * (size_t)a.grid_stride + (size_t)grp0 * W + (size_t)r_first * pitch;
+    if (elect_one()) {
+#pragma unroll
+      for (int q = 0; q < kStage; ++q)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mbar0 + 8u * q) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+  }
+  auto stage = [&](uint32_t slot, uint32_t mb) {  // slot: the lane-0 (base) address
+    if constexpr (kBulk) {
+      bulk_stage_row<T>(slot, ub, vdelta, bytes_a, d_b, bytes_b, mb);
+      ub += pitch;
+      if (rows_left == 1) ub -= span;  // same wrap point as su (src_next)
+    } else {
+      stage_row<W, T>(slot + lane * kLaneBytes, su, su + vdelta, 0);
+    }
+  };
 
   // Prime the staging ring with the rows of ticks 0 .. kPrefetch-1.
 #pragma unroll
   for (int d = 0; d < kPrefetch; ++d) {
     if (d < n_load) {
-      stage_row<W, T>(ring + d * kSlot, su, su + vdelta, 0);
+      stage(ring0 + d * kSlot, mbar0 + 8u * d);
       src_next();
     }
-    stage_commit();
+    if constexpr (!kBulk) stage_commit();
   }
 
   Row<W, T> win[K > 1 ? K - 1 : 1][3];
@@ -500,7 +595,11 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
   // slot ph of the half the current 3-tick group uses; the prefetch of tick
   // j+3 goes to slot ph of the other half.  Both half bases swap once per
   // group, so every slot address is a base plus a compile-time offset.
-  uint32_t half_now = ring, half_other = ring + 3 * kSlot;
+  // Half bases are warp-uniform; a lane reads its own chunk at + lane_off.
+  const uint32_t lane_off = lane * kLaneBytes;
+  uint32_t half_now = ring0, half_other = ring0 + 3 * kSlot;
+  uint32_t mb_now = mbar0, mb_other = mbar0 + 24u;  // their slots' barriers (bulk)
+  uint32_t phase_now = 0, phase_other = 0;           // barrier phase of each half's next use
 
   // One tick.  PH = j % 3 (compile-time ring slot); kSteady = every level is
   // active in this tick, so the validity tests disappear.
@@ -539,17 +638,24 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
     // Stage the row of tick j + kPrefetch into the slot of tick j - 3 (an
     // empty group past the end keeps the wait_group accounting uniform).
     if (j + kPrefetch < n_load) {
-      stage_row<W, T>(half_other + ph * kSlot, su, su + vdelta, 0);
+      stage(half_other + ph * kSlot, mb_other + 8u * ph);
       src_next();
     }
-    stage_commit();
+    if constexpr (!kBulk) stage_commit();
     // Level 1 from the level-0 rows of ticks j-2, j-1, j.
+    // The row of tick j has landed.  Bulk: every filled slot is waited on
+    // its own barrier, ticks 0 and 1 included (per-slot barriers complete in
+    // any order, unlike cp.async groups; and no copy may still be in flight
+    // when the CTA exits).
+    if constexpr (kBulk) {
+      if (kSteady || j < n_load) bulk_wait(mb_now + 8u * ph, phase_now);
+    }
     if (kSteady || (j >= 2 && j < n_load)) {
-      stage_wait<kPrefetch>();  // the row of tick j has landed
+      if constexpr (!kBulk) stage_wait<kPrefetch>();
       Row<W, T> up, ce, dn;
-      read_staged<W, T>(ph >= 2 ? half_now + (ph - 2) * kSlot : half_other + (ph + 1) * kSlot, up);
-      read_staged<W, T>(ph >= 1 ? half_now + (ph - 1) * kSlot : half_other + 2 * kSlot, ce);
-      read_staged<W, T>(half_now + ph * kSlot, dn);
+      read_staged<W, T>(lane_off + (ph >= 2 ? half_now + (ph - 2) * kSlot : half_other + (ph + 1) * kSlot), up);
+      read_staged<W, T>(lane_off + (ph >= 1 ? half_now + (ph - 1) * kSlot : half_other + 2 * kSlot), ce);
+      read_staged<W, T>(lane_off + half_now + ph * kSlot, dn);
       if constexpr (K == 1) {
         Row<W, T> o;
         level_row<W, T, kFast, kWrap>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
@@ -590,8 +696,14 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
     const uint32_t t_half = half_now;
     half_now = half_other;
     half_other = t_half;
+    const uint32_t t_mb = mb_now;
+    mb_now = mb_other;
+    mb_other = t_mb;
+    const uint32_t t_ph = phase_now ^ 1u;  // the half just consumed is next used one phase on
+    phase_now = phase_other;
+    phase_other = t_ph;
   }
-  stage_wait<0>();
+  if constexpr (!kBulk) stage_wait<0>();
 
   if (fin.bad_in_warp() && lane == 0 && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);
   if (a.trace != nullptr && lane == 0) {

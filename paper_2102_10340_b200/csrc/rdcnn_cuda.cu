@@ -552,7 +552,10 @@ namespace {
 
 template <class T>
 int width_for(const rdcnn_sim* s) {
-  return (s->cols % Traits<T>::kWide == 0) ? Traits<T>::kWide : 1;
+  // The fp32 wide instances stage rows with cp.async.bulk, which needs every
+  // band to wrap the torus edge at most once: at least 32 column groups.
+  const bool bulk = rdcnn_dev::BulkStage<Traits<T>::kWide, T>::value;
+  return (s->cols % Traits<T>::kWide == 0 && (!bulk || s->cols / Traits<T>::kWide >= 32)) ? Traits<T>::kWide : 1;
 }
 
 template <class T>
