@@ -588,3 +588,43 @@ def test_peer_ring_two_processes_ipc(oracle, blowup):
     fin = np.isfinite(ou) & np.isfinite(ov)
     assert np.array_equal(np.isfinite(got_u), np.isfinite(ou))
     assert np.array_equal(bits(got_u)[fin], bits(ou)[fin]) and np.array_equal(bits(got_v)[fin], bits(ov)[fin])
+
+
+@pytest.mark.parametrize("rows,cols", [(256, 256), (128, 128)])
+def test_persistent_cluster_fast_mode_matches_wavefront(rows, cols):
+    """Fast mode (FMA-contracted) evaluates the same fhn_cell sequence in both
+    kernels, so the one-launch cluster path and the wavefront path agree bit
+    for bit."""
+    rng = np.random.default_rng(rows)
+    u0 = rng.random(rows * cols, dtype=np.float32)
+    v0 = rng.random(rows * cols, dtype=np.float32) * 0.3
+    out = []
+    for pers in (1, -1):
+        with fhn.Simulator(rows, cols, mode="fast", persistent=pers) as sim:
+            sim.upload(u0, v0)
+            assert int(sim.advance(333)[0]) == 0
+            out.append(sim.download())
+    assert np.array_equal(bits(out[0][0]), bits(out[1][0])) and np.array_equal(bits(out[0][1]), bits(out[1][1]))
+
+
+def test_trace_launch_reports_every_warp():
+    """rdcnn_sim_trace_launch (profiling entry point): one record per warp,
+    end >= start, SM ids in range; the traced launch still advances the state
+    exactly (== one K-level step of the regular path)."""
+    import ctypes
+
+    lib = fhn.load()
+    rows = cols = 512
+    with fhn.Simulator(rows, cols, levels=4, persistent=-1) as a, fhn.Simulator(rows, cols, levels=4, persistent=-1) as b:
+        a.init(2, 3)
+        b.init(2, 3)
+        cap = 1 << 16
+        buf = (ctypes.c_ulonglong * (3 * cap))()
+        n = ctypes.c_longlong()
+        assert lib.rdcnn_sim_trace_launch(a._h, 4, buf, cap, ctypes.byref(n)) == 0
+        t = np.frombuffer(buf, dtype=np.uint64, count=3 * n.value).reshape(-1, 3)
+        assert n.value > 0 and (t[:, 1] >= t[:, 0]).all() and (t[:, 2] < 1024).all()
+        assert int(b.advance(4)[0]) == 0
+        ua, va = a.download()
+        ub, vb = b.download()
+    assert np.array_equal(bits(ua), bits(ub)) and np.array_equal(bits(va), bits(vb))
