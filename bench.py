@@ -12,10 +12,13 @@ larger than the 126 MB L2, so no explicit L2 flush is needed.
 
   python bench.py                         # N=1, our sm_100a path
   python bench.py --impl reference        # the reference CPU path (oracle/_ref)
-  torchrun --nproc-per-node N bench.py --gpus N   # row slabs, NCCL halo exchange
+  torchrun --nproc-per-node N bench.py --gpus N   # row slabs, fused peer halo exchange
+  torchrun --nproc-per-node N bench.py --gpus N --workload cfg5   # one 32768^2 torus over N GPUs
 
 For N > 1 each rank owns a 4096-row slab of a (4096*N) x 4096 torus (weak
-scaling) and exchanges `levels` halo rows with its ring neighbours per block.
+scaling, cfg2) or 32768/N rows of one 32768^2 torus (strong scaling, cfg5,
+BASELINE configs[4]) and exchanges `levels` halo rows with its ring
+neighbours per block.
 """
 from __future__ import annotations
 
@@ -34,6 +37,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 GENE7 = [0.1, -0.05, 1.3, -0.1, 1.0, 0.06, 1.0]  # dt,a,b,eps,c,Du,Dv: slow growth
+DEFAULT_GENE7 = [0.1, -0.3, 1.3, -0.1, 1.0, 0.06, 1.0]  # gene.hpp:13-24
 BYTES_PER_CELL_UPDATE = 16  # read u,v + write u,v, fp32
 FLOPS_PER_CELL_UPDATE = 27  # 26 add/sub/mul + 1 divide
 
@@ -44,8 +48,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--size", type=int, default=4096)
-    ap.add_argument("--iters-per-step", type=int, default=10000)
+    ap.add_argument("--workload", default="cfg2", choices=("cfg2", "cfg5"),
+                    help="cfg2 (default): a size x size torus per GPU, weak scaling; cfg5: ONE "
+                         "size x size torus (default 32768) split over the N GPUs, strong scaling")
+    ap.add_argument("--size", type=int, default=None,
+                    help="cfg2: rows = cols per GPU (default 4096); cfg5: the lattice edge (32768)")
+    ap.add_argument("--iters-per-step", type=int, default=None,
+                    help="default 10000 (cfg2), 100 (cfg5)")
     ap.add_argument("--levels", type=int, default=4, choices=(1, 2, 4, 8))
     ap.add_argument("--seg-rows", type=int, default=0)
     ap.add_argument("--mode", default="strict", choices=("strict", "fast"))
@@ -63,6 +72,43 @@ def parse():
 # ---------------------------------------------------------------------------
 # helpers
 # ---------------------------------------------------------------------------
+
+class Workload:
+    """BASELINE.json configs the bench runs.
+
+    cfg2: init_center_square(size, size, 42), slow-growth gene a=-0.05; at N>1
+          each GPU owns a size-row slab of a (size*N) x size torus (weak scaling).
+    cfg5: init_full_random(size, size, 42) with the reference default gene, ONE
+          size x size torus (default 32768^2) row-slabbed over the N GPUs (strong
+          scaling)."""
+
+    def __init__(self, args, world: int):
+        self.name = args.workload
+        if self.name == "cfg5":
+            self.cols = args.size or 32768
+            self.rows_global = self.cols
+            if self.rows_global % world:
+                raise SystemExit(f"cfg5: {self.rows_global} rows do not split over {world} GPUs")
+            self.rows_rank = self.rows_global // world
+            self.typ, self.gene7 = 2, DEFAULT_GENE7
+            self.iters = args.iters_per_step or 100
+            self.scaling = "strong"
+            self.desc = (f"cfg5: FHN RD-CNN {self.rows_global}x{self.cols} fp32 torus, typ=2 (full "
+                         f"random) seed 42, reference default gene, {self.iters} iterations per step")
+        else:
+            n = args.size or 4096
+            self.cols = n
+            self.rows_rank = n
+            self.rows_global = n * world
+            self.typ, self.gene7 = 1, GENE7
+            self.iters = args.iters_per_step or 10000
+            self.scaling = "weak"
+            self.desc = (f"cfg2: FHN RD-CNN {n}x{n} fp32 torus per GPU, typ=1 seed 42, "
+                         f"slow-growth gene a=-0.05, {self.iters} iterations per step")
+
+    def gene(self, fhn):
+        g = self.gene7
+        return fhn.Gene(dt=g[0], a=g[1], b=g[2], eps=g[3], c=g[4], Du=g[5], Dv=g[6])
 
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -136,26 +182,27 @@ def ncu_traffic():
         return None, None
     with open(path) as f:
         d = json.load(f)
-    return d.get("dram_bytes_per_launch"), d.get("launch_cells_times_levels")
+    return d.get("dram_bytes_per_launch"), d.get("cell_updates_per_launch")
 
 
-def cpu_baseline_sample(size: int, budget_s: float):
+def cpu_baseline_sample(wl: "Workload", budget_s: float):
     """The reference's own parallel backend (oracle/_ref, reference headers
     compiled read-only) on a bounded prefix of the same workload."""
     from oracle.oracle import Reference
     ref = Reference()
     threads = ref.max_threads()
-    u, v = ref.init(1, size, size, 42)
+    R, C = wl.rows_global, wl.cols
+    u, v = ref.init(wl.typ, R, C, 42)
     # calibrate with 2 iterations, then size the sample to the budget
-    u, v, _, sec = ref.run_timed(size, size, u, v, 2, GENE7, backend="parallel")
+    u, v, _, sec = ref.run_timed(R, C, u, v, 2, wl.gene7, backend="parallel")
     per_iter = max(sec / 2, 1e-6)
     iters = int(max(2, min(2000, budget_s / per_iter)))
-    u, v, bad, sec = ref.run_timed(size, size, u, v, iters, GENE7, backend="parallel")
-    value = size * size * iters / sec / 1e6
+    u, v, bad, sec = ref.run_timed(R, C, u, v, iters, wl.gene7, backend="parallel")
+    value = R * C * iters / sec / 1e6
     return {"value": round(value, 2), "unit": "Mcell-updates/s", "cores": threads,
             "kind": "reference",
             "sample": f"reference parallel backend (oracle/_ref, {threads} OpenMP threads), "
-                      f"{size}x{size} typ=1 seed 42 a=-0.05, iterations 3..{iters + 2} "
+                      f"{R}x{C} typ={wl.typ} seed 42 ({wl.name} gene), iterations 3..{iters + 2} "
                       f"({sec:.2f} s) of the same run"}
 
 
@@ -178,29 +225,30 @@ def bench_reference(args, rank, world):
     if rank != 0:
         return
     from oracle.oracle import Reference
+    wl = Workload(args, world)
     ref = Reference()
-    n = args.size
+    R, C = wl.rows_global, wl.cols  # the same global lattice our arm advances
     threads = ref.max_threads()
-    u, v = ref.init(1, n, n, 42)
+    u, v = ref.init(wl.typ, R, C, 42)
     # size each step to ~2 s of CPU work so the whole run stays within minutes
-    u, v, _, sec = ref.run_timed(n, n, u, v, 2, GENE7, backend="parallel")
-    iters = int(max(1, min(args.iters_per_step, 2.0 / max(sec / 2, 1e-6))))
+    u, v, _, sec = ref.run_timed(R, C, u, v, 2, wl.gene7, backend="parallel")
+    iters = int(max(1, min(wl.iters, 2.0 / max(sec / 2, 1e-6))))
     for _ in range(args.warmup):
-        u, v, _, _ = ref.run_timed(n, n, u, v, iters, GENE7, backend="parallel")
+        u, v, _, _ = ref.run_timed(R, C, u, v, iters, wl.gene7, backend="parallel")
     total = 0.0
     for _ in range(args.steps):
-        u, v, bad, sec = ref.run_timed(n, n, u, v, iters, GENE7, backend="parallel")
+        u, v, bad, sec = ref.run_timed(R, C, u, v, iters, wl.gene7, backend="parallel")
         total += sec
-    value = n * n * iters * args.steps / total / 1e6
+    value = R * C * iters * args.steps / total / 1e6
     sample = (f"reference parallel backend via run_timed (oracle/_ref = reference headers), "
-              f"{threads} threads on {cpu_model()}; each step = {iters} iterations of {n}x{n}")
+              f"{threads} threads on {cpu_model()}; each step = {iters} iterations of {R}x{C}")
     line = {
         "impl": "reference", "metric": "Mcell-updates/s", "value": round(value, 2),
         "unit": "Mcell-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"cfg2: FHN RD-CNN {n}x{n} fp32 typ=1 seed 42, slow-growth gene "
-                               f"a=-0.05, iterations per step {iters}", "rows": n, "cols": n},
+        "scaling": wl.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl.desc.replace(f"{wl.iters} iterations", f"{iters} iterations")
+                   + (f"; global {R}x{C}" if world > 1 else ""), "rows": R, "cols": C},
         "cpu_baseline": {"value": round(value, 2), "unit": "Mcell-updates/s", "cores": threads,
                          "kind": "reference", "sample": sample},
         "e2e": {"value": round(value, 2), "unit": "Mcell-updates/s", "h2d_bytes_per_step": 0,
@@ -227,10 +275,10 @@ def bench_ours(args, rank, world, local_rank):
         local_rank = 0
     torch.cuda.set_device(local_rank)
     red_dev = "cpu" if one_dev else "cuda"
-    n = args.size
-    S = args.iters_per_step
-    gene = fhn.Gene(dt=GENE7[0], a=GENE7[1], b=GENE7[2], eps=GENE7[3], c=GENE7[4], Du=GENE7[5],
-                    Dv=GENE7[6])
+    wl = Workload(args, world)
+    n = wl.cols
+    S = wl.iters
+    gene = wl.gene(fhn)
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -241,10 +289,10 @@ def bench_ours(args, rank, world, local_rank):
 
     launches = 0
     if world == 1 and not args.slab:
-        sim = fhn.Simulator(n, n, device=local_rank, mode=args.mode, levels=args.levels,
+        sim = fhn.Simulator(wl.rows_global, n, device=local_rank, mode=args.mode, levels=args.levels,
                             seg_rows=args.seg_rows)
         sim.set_params(gene)
-        sim.init(1, 42)
+        sim.init(wl.typ, 42)
         stream = torch.cuda.ExternalStream(sim.stream(), device=local_rank)
         for _ in range(args.warmup):
             sim.advance(S)
@@ -261,14 +309,14 @@ def bench_ours(args, rank, world, local_rank):
             ev1.record(stream)
             torch.cuda.synchronize()
         t_ms = ev0.elapsed_time(ev1)
-        cells_global = n * n
+        cells_global = wl.rows_global * n
     else:
         from paper_2102_10340_b200.slab import SlabStepper
-        rows_global = n * world
+        rows_global = wl.rows_global
         slab = SlabStepper(rows_global, n, rank, world, ghost=args.levels, device=local_rank,
                            mode=args.mode, seg_rows=args.seg_rows, transport=args.transport)
         slab.set_params(gene)
-        slab.init(1, 42)
+        slab.init(wl.typ, 42)
         slab.fill_ghosts()
         hs = ctypes.c_void_p()
         fhn.load().rdcnn_sim_stream(slab._h, ctypes.byref(hs))
@@ -304,7 +352,7 @@ def bench_ours(args, rank, world, local_rank):
 
     # ---- roofline of the dominant kernel (the K-level wavefront stencil) ----
     peaks, peak_kind = measured_peaks()
-    per_rank_cells = n * n
+    per_rank_cells = wl.rows_rank * n
     launches_per_rank = max(launches, 1)
     if (world > 1 or args.slab) and args.transport == "nccl":
         # 3 launches per block (two boundary strips + interior); the interior
@@ -314,7 +362,9 @@ def bench_ours(args, rank, world, local_rank):
     levels = args.levels
     alg_bytes_per_launch = BYTES_PER_CELL_UPDATE * per_rank_cells * levels
     achieved_gbs = alg_bytes_per_launch / avg_launch_s / 1e9
-    traffic, _ = ncu_traffic()
+    traffic, traffic_units = ncu_traffic()
+    if traffic_units != per_rank_cells * levels:
+        traffic = None  # the committed capture is of another launch size
     sm_mhz = clock_info.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
     fp32_peak_tops = 148 * 128 * sm_mhz * 1e6 / 1e12  # FP32 lanes x clock (non-FMA ops)
     fp32_achieved = value * 1e6 * FLOPS_PER_CELL_UPDATE / world / 1e12
@@ -334,8 +384,9 @@ def bench_ours(args, rank, world, local_rank):
     # ---- end to end through the public API with host buffers (N=1 only) ----
     e2e = None
     if world == 1 and not args.slab:
-        u_h = torch.empty(n * n, dtype=torch.float32).pin_memory()
-        v_h = torch.empty(n * n, dtype=torch.float32).pin_memory()
+        cells = wl.rows_global * n
+        u_h = torch.empty(cells, dtype=torch.float32).pin_memory()
+        v_h = torch.empty(cells, dtype=torch.float32).pin_memory()
         sim.download_ptr(u_h.data_ptr(), v_h.data_ptr())
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -346,9 +397,9 @@ def bench_ours(args, rank, world, local_rank):
             sim.download_ptr(u_h.data_ptr(), v_h.data_ptr())
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
-        e2e = {"value": round(n * n * S * args.e2e_steps / e2e_s / 1e6, 2),
-               "unit": "Mcell-updates/s", "h2d_bytes_per_step": 2 * 4 * n * n,
-               "d2h_bytes_per_step": 2 * 4 * n * n,
+        e2e = {"value": round(cells * S * args.e2e_steps / e2e_s / 1e6, 2),
+               "unit": "Mcell-updates/s", "h2d_bytes_per_step": 2 * 4 * cells,
+               "d2h_bytes_per_step": 2 * 4 * cells,
                "path": "rdcnn_sim_upload (pinned host) -> rdcnn_sim_advance -> rdcnn_sim_download",
                "steps": args.e2e_steps}
         # sanity: state stays finite
@@ -388,7 +439,7 @@ def bench_ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline_sample(n, args.cpu_seconds)
+            cpu = cpu_baseline_sample(wl, args.cpu_seconds)
         except Exception as e:  # noqa: BLE001 - report, never hide
             cpu = {"value": None, "unit": "Mcell-updates/s", "cores": None, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -398,17 +449,18 @@ def bench_ours(args, rank, world, local_rank):
             "metric": "Mcell-updates/s", "value": round(value, 2), "unit": "Mcell-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t_ms / args.steps, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": wl.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {
-                "workload": (f"cfg2: FHN RD-CNN {n}x{n} fp32 torus per GPU, typ=1 seed 42, "
-                             f"slow-growth gene a=-0.05, {S} iterations per step"
-                             + (f"; global {n * world}x{n} row-slabbed, halo exchange: "
+                "workload": (wl.desc
+                             + (f"; global {wl.rows_global}x{n} row-slabbed ({wl.rows_rank} rows per "
+                                f"GPU), halo exchange: "
                                 + ("fused peer stores in the step kernel" if args.transport == "p2p"
                                    else "NCCL send/recv overlapped with the interior kernel")
                                 if world > 1 or args.slab else "")),
-                "rows": n * world, "cols": n, "iterations_per_step": S, "levels_per_launch": levels,
-                "mode": args.mode, "l2": (f"double-buffered state {2 * 8 * n * n / 2**20:.0f} MiB/GPU "
-                       + ("> 126 MB L2 (no flush needed)" if 2 * 8 * n * n > 126e6
+                "rows": wl.rows_global, "cols": n, "iterations_per_step": S, "levels_per_launch": levels,
+                "mode": args.mode,
+                "l2": (f"double-buffered state {2 * 8 * per_rank_cells / 2**20:.0f} MiB/GPU "
+                       + ("> 126 MB L2 (no flush needed)" if 2 * 8 * per_rank_cells > 126e6
                           else "fits in L2: small-size run, not a reported number")),
                 "parallelism": f"slab{world}" if world > 1 or args.slab else "single",
                 **({"transport": args.transport} if world > 1 or args.slab else {}),
