@@ -247,6 +247,11 @@ int rdcnn_sim_frame_active(rdcnn_sim_t sim, int slot, const double* medians,
 int rdcnn_sim_frame_normalize(rdcnn_sim_t sim, int slot, int grid, double lo,
                               double hi, uint8_t* out);
 
+/* checksum (grid.hpp:100-126) of every grid of the current state, computed
+ * on the device (one thread per grid: FNV-1a 64 over u's bytes then v's);
+ * out[batch].  Equal to rdcnn_checksum_f32/_f64 of the downloaded planes. */
+int rdcnn_sim_checksums(rdcnn_sim_t sim, uint64_t* out);
+
 /* ---- host helpers (reference-identical, no device needed) --------------- */
 int rdcnn_init_center_square_host(int rows, int cols, uint64_t seed, float* u,
                                   float* v);

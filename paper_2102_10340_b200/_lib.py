@@ -92,6 +92,7 @@ SIGNATURES = {
     "rdcnn_slab_step_fused": (c_int, [c_void_p, c_int, c_void_p]),
     "rdcnn_slab_checkpoint_enable": (c_int, [c_void_p, c_int]),
     "rdcnn_slab_restore": (c_int, [c_void_p]),
+    "rdcnn_sim_checksums": (c_int, [c_void_p, c_void_p]),
     "rdcnn_sim_frames_reserve": (c_int, [c_void_p, c_int]),
     "rdcnn_sim_frame_capture": (c_int, [c_void_p, c_int]),
     "rdcnn_sim_frame_download": (c_int, [c_void_p, c_int, c_void_p]),

@@ -1180,6 +1180,29 @@ int normalize_impl(rdcnn_sim* s, const void* src_dev, double lo, double hi, uint
   return RDCNN_OK;
 }
 
+// checksum / fnv1a (grid.hpp:100-126) of every grid of a batch on the device:
+// one thread per grid, FNV-1a 64 over the raw bytes of its u plane then its v
+// plane -- sequential within a grid, independent across grids.
+__global__ void fnv_batch_kernel(const unsigned char* __restrict__ u, const unsigned char* __restrict__ v,
+                                 size_t plane_bytes, size_t grid_stride_bytes, int batch,
+                                 unsigned long long* __restrict__ out) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= batch) return;
+  unsigned long long h = 0xcbf29ce484222325ull;
+  for (const unsigned char* plane : {u, v}) {
+    const unsigned char* p = plane + (size_t)g * grid_stride_bytes;
+    size_t i = 0;
+    for (; i + 16 <= plane_bytes; i += 16) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(p + i));
+      for (unsigned word : {w.x, w.y, w.z, w.w})
+#pragma unroll
+        for (int k = 0; k < 4; ++k) h = (h ^ ((word >> (8 * k)) & 0xFFu)) * 0x100000001b3ull;
+    }
+    for (; i < plane_bytes; ++i) h = (h ^ p[i]) * 0x100000001b3ull;
+  }
+  out[g] = h;
+}
+
 uint64_t fnv_planes(const void* u, const void* v, size_t bytes) {
   uint64_t h = 0xcbf29ce484222325ull;
   for (const void* plane : {u, v}) {
@@ -1720,6 +1743,32 @@ int rdcnn_slab_restore(rdcnn_sim_t s) {
 }
 
 // ---- snapshot store and analysis (sweep.hpp:48-112, frame.hpp:28-66) ------
+
+int rdcnn_sim_checksums(rdcnn_sim_t s, uint64_t* out) {
+  if (!s || !out) return fail(RDCNN_EINVAL, "null argument");
+  if (s->slab) return fail(RDCNN_EINVAL, "not a periodic handle");
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  const size_t plane = (size_t)s->rows * s->cols * s->elem;
+  if (plane % 16 != 0 || (size_t)s->grid_stride * s->elem % 16 != 0) {
+    // Unaligned shapes: hash on the host after a download.
+    std::vector<unsigned char> hu(plane * s->batch), hv(plane * s->batch);
+    RDCNN_TRY(copy_state(s, hu.data(), hv.data(), false));
+    for (int g = 0; g < s->batch; ++g) out[g] = fnv_planes(hu.data() + g * plane, hv.data() + g * plane, plane);
+    return RDCNN_OK;
+  }
+  unsigned long long* d = nullptr;
+  RDCNN_CUDA_TRY(cudaMallocAsync(&d, sizeof(unsigned long long) * (size_t)s->batch, s->stream));
+  const unsigned char* u = static_cast<const unsigned char*>(s->buf[s->cur]);
+  const unsigned char* v = u + plane * s->batch;
+  fnv_batch_kernel<<<(s->batch + 31) / 32, 32, 0, s->stream>>>(u, v, plane, (size_t)s->grid_stride * s->elem,
+                                                                  s->batch, d);
+  RDCNN_CUDA_TRY(cudaGetLastError());
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(out, d, sizeof(unsigned long long) * (size_t)s->batch, cudaMemcpyDeviceToHost,
+                                 s->stream));
+  RDCNN_CUDA_TRY(cudaFreeAsync(d, s->stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RDCNN_OK;
+}
 
 int rdcnn_sim_frames_reserve(rdcnn_sim_t s, int nframes) {
   if (!s || s->slab) return fail(RDCNN_EINVAL, "not a periodic handle");

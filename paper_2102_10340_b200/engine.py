@@ -286,6 +286,12 @@ class Simulator:
         check(self._lib.rdcnn_sim_advance(self._h, int(steps), bad))
         return np.array(bad[:], dtype=np.int64)
 
+    def checksums(self) -> np.ndarray:
+        """checksum (grid.hpp:100-126) of every grid, computed on the device."""
+        out = np.empty(self.batch, np.uint64)
+        check(self._lib.rdcnn_sim_checksums(self._h, out.ctypes.data))
+        return out
+
     def elapsed_ms(self) -> float:
         ms = ctypes.c_double()
         check(self._lib.rdcnn_sim_elapsed_ms(self._h, ctypes.byref(ms)))

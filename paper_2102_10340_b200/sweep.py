@@ -251,6 +251,7 @@ def sweep_grid(spec: SweepSpec, image: Optional[np.ndarray] = None, device: int 
     final_range = maxs[-1] - mins[-1]
     thr = spec.classifier.activity_rel * final_range
     counts = np.stack([sim.frame_active(f, meds[f], thr) for f in range(F)])  # [F, B]
+    digests = sim.checksums()  # per grid, on the device
     fu, fv = sim.download()
     fu = fu.reshape(B, -1)
     fv = fv.reshape(B, -1)
@@ -260,7 +261,7 @@ def sweep_grid(spec: SweepSpec, image: Optional[np.ndarray] = None, device: int 
             continue
         c.outcome = classify(mins[:, idx], maxs[:, idx], counts[:, idx], rows * cols, spec.classifier,
                              float(final_range[idx]))
-        c.digest = checksum(GridState(rows, cols, fu[idx], fv[idx]))
+        c.digest = int(digests[idx])
         c.final_u = fu[idx].copy()
         if frames_u is not None:
             c.buffer = [fr[idx].copy() for fr in frames_u]

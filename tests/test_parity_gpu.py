@@ -628,3 +628,19 @@ def test_trace_launch_reports_every_warp():
         ua, va = a.download()
         ub, vb = b.download()
     assert np.array_equal(bits(ua), bits(ub)) and np.array_equal(bits(va), bits(vb))
+
+
+@pytest.mark.parametrize("rows,cols,batch,precision", [
+    (128, 128, 37, "single"), (17, 23, 5, "single"), (24, 40, 3, "double"), (64, 64, 1, "single")])
+def test_device_checksums_equal_host(rows, cols, batch, precision):
+    """rdcnn_sim_checksums (FNV-1a of u then v per grid, on the device) equals
+    the reference checksum of the downloaded planes, grid by grid."""
+    with fhn.Simulator(rows, cols, batch=batch, precision=precision) as sim:
+        sim.init(2, 11)
+        sim.advance(7)
+        got = sim.checksums()
+        u, v = sim.download()
+    u = u.reshape(batch, -1)
+    v = v.reshape(batch, -1)
+    want = [fhn.checksum(fhn.GridState(rows, cols, u[g], v[g])) for g in range(batch)]
+    assert [int(x) for x in got] == want

@@ -1,0 +1,47 @@
+"""Wall-time breakdown of the cfg4 parameter sweep (4096 x 128^2 x 5000
+iterations, nssp 5) through sweep_grid, phase by phase (monkey-patched
+timers around the Simulator calls)."""
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+import paper_2102_10340_b200 as fhn  # noqa: E402
+from paper_2102_10340_b200 import sweep as sw  # noqa: E402
+from paper_2102_10340_b200.engine import RunConfig, Simulator  # noqa: E402
+
+T = {}
+
+
+def timed(name, fn):
+    def w(*a, **k):
+        t0 = time.perf_counter()
+        r = fn(*a, **k)
+        T[name] = T.get(name, 0.0) + time.perf_counter() - t0
+        return r
+    return w
+
+
+for name in ("advance", "frame_capture", "frame_stats", "frame_active", "download", "init", "set_params",
+             "frames_reserve", "frame_download"):
+    setattr(Simulator, name, timed(name, getattr(Simulator, name)))
+sw.classify = timed("classify", sw.classify)
+sw.checksum = timed("checksum", sw.checksum)
+
+side = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+cfg = RunConfig()
+cfg.nn = cfg.nm = 128
+cfg.iter_max = 5000
+cfg.nssp = 5
+spec = sw.SweepSpec("du", list(np.linspace(0.02, 0.70, side)), "dv", list(np.linspace(0.50, 1.20, side)),
+                    base_config=cfg)
+t0 = time.perf_counter()
+res = sw.sweep_grid(spec)
+wall = time.perf_counter() - t0
+labels = {}
+for c in res.cells:
+    labels[c.outcome.label] = labels.get(c.outcome.label, 0) + 1
+print(f"sweep {side}x{side} cells of 128^2 x 5000: wall {wall:.3f} s; labels {labels}")
+for k, v in sorted(T.items(), key=lambda x: -x[1]):
+    print(f"  {k:15s} {v:.3f} s")
