@@ -64,8 +64,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slab", action="store_true",
                     help="run the multi-GPU slab path even at N=1 (a world-1 ring)")
-    ap.add_argument("--transport", default="p2p", choices=("p2p", "nccl"),
-                    help="slab halo exchange: fused peer stores in the step kernel, or NCCL")
+    ap.add_argument("--transport", default="auto", choices=("auto", "p2p", "nccl"),
+                    help="slab halo exchange: fused peer stores in the step kernel (p2p), NCCL, "
+                         "or auto (p2p unless a rank cannot map its neighbours' memory)")
     return ap.parse_args()
 
 
@@ -354,7 +355,8 @@ def bench_ours(args, rank, world, local_rank):
     peaks, peak_kind = measured_peaks()
     per_rank_cells = wl.rows_rank * n
     launches_per_rank = max(launches, 1)
-    if (world > 1 or args.slab) and args.transport == "nccl":
+    transport = slab.transport if (world > 1 or args.slab) else None
+    if transport == "nccl":
         # 3 launches per block (two boundary strips + interior); the interior
         # carries ~all the work, so the per-block time is the launch figure
         launches_per_rank = max(launches // 3, 1)
@@ -454,7 +456,7 @@ def bench_ours(args, rank, world, local_rank):
                 "workload": (wl.desc
                              + (f"; global {wl.rows_global}x{n} row-slabbed ({wl.rows_rank} rows per "
                                 f"GPU), halo exchange: "
-                                + ("fused peer stores in the step kernel" if args.transport == "p2p"
+                                + ("fused peer stores in the step kernel" if transport == "p2p"
                                    else "NCCL send/recv overlapped with the interior kernel")
                                 if world > 1 or args.slab else "")),
                 "rows": wl.rows_global, "cols": n, "iterations_per_step": S, "levels_per_launch": levels,
@@ -463,7 +465,7 @@ def bench_ours(args, rank, world, local_rank):
                        + ("> 126 MB L2 (no flush needed)" if 2 * 8 * per_rank_cells > 126e6
                           else "fits in L2: small-size run, not a reported number")),
                 "parallelism": f"slab{world}" if world > 1 or args.slab else "single",
-                **({"transport": args.transport} if world > 1 or args.slab else {}),
+                **({"transport": transport} if world > 1 or args.slab else {}),
             },
             "roofline": roofline,
             "cpu_baseline": cpu,

@@ -80,7 +80,7 @@ class SlabStepper:
     def __init__(self, global_rows: int, cols: int, rank: int, world: int, ghost: int = 4,
                  device: int = 0, mode: str = "strict",
                  exchange: Optional[Callable] = None, seg_rows: int = 0, native: Optional[bool] = None,
-                 transport: str = "p2p", attach: bool = True, exact_blowup: bool = True):
+                 transport: str = "auto", attach: bool = True, exact_blowup: bool = True):
         """``native`` (default: True unless a Python ``exchange`` is given)
         runs the whole block loop in the C-ABI (rdcnn_slab_advance, no host
         work per block); otherwise each block is driven from Python with
@@ -90,7 +90,9 @@ class SlabStepper:
         the step kernel -- edge rows are stored straight into the neighbours'
         ghost rows over peer memory (CUDA IPC) and signalled with release
         stores, one launch per block; ``"nccl"`` runs boundary kernel ->
-        NCCL send/recv on a comm stream || interior kernel.  ``attach=False``
+        NCCL send/recv on a comm stream || interior kernel; ``"auto"``
+        (default) is p2p unless some rank cannot map its neighbours' memory,
+        then NCCL on every rank (``self.transport`` says which).  ``attach=False``
         leaves the ring to the caller (in-process rings, see ``attach_peers``).
         ``exact_blowup`` keeps a device copy of each advance's input so a
         blow-up is reported at its exact iteration (see ``advance``)."""
@@ -103,24 +105,50 @@ class SlabStepper:
         self.device = device
         self.native = (exchange is None) if native is None else native
         self.exchange = exchange or exchange_halos
-        h = ctypes.c_void_p()
-        m = RDCNN_FAST if mode == "fast" else RDCNN_STRICT
-        check(self._lib.rdcnn_slab_create(self.rows, cols, ghost, device, m, ctypes.byref(h)))
-        self._h = h
-        check(self._lib.rdcnn_sim_set_tuning(self._h, ghost, seg_rows))
+        self._mode, self._seg_rows = (RDCNN_FAST if mode == "fast" else RDCNN_STRICT), seg_rows
         self.launches = 0
         self._dist_ring = False
         self.exact_blowup = bool(exact_blowup) and self.native
-        if self.exact_blowup:
-            check(self._lib.rdcnn_slab_checkpoint_enable(self._h, 1))
-        if transport not in ("p2p", "nccl"):
+        self._create()
+        if transport not in ("p2p", "nccl", "auto"):
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport if self.native else "python"
         if self.native and attach:
-            if transport == "p2p":
+            if transport == "nccl":
+                self._attach_ring()
+            elif transport == "p2p":
                 self._attach_peers()
             else:
-                self._attach_ring()
+                # auto: the fused peer ring when every rank can map its
+                # neighbours' memory, else (on every rank) the NCCL ring.
+                if not self._all_ranks(self._try_attach_peers()):
+                    self.close()
+                    self._create()
+                    self._dist_ring = False
+                    self._attach_ring()
+                    self.transport = "nccl"
+                else:
+                    self.transport = "p2p"
+
+    def _create(self):
+        h = ctypes.c_void_p()
+        check(self._lib.rdcnn_slab_create(self.rows, self.cols, self.ghost, self.device, self._mode,
+                                          ctypes.byref(h)))
+        self._h = h
+        check(self._lib.rdcnn_sim_set_tuning(self._h, self.ghost, self._seg_rows))
+        if self.exact_blowup:
+            check(self._lib.rdcnn_slab_checkpoint_enable(self._h, 1))
+
+    def _all_ranks(self, ok: bool) -> bool:
+        if self.world == 1:
+            return ok
+        import torch
+        import torch.distributed as dist
+
+        dev = f"cuda:{self.device}" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item())
 
     # -- fused peer ring -------------------------------------------------------
     def export_peer(self) -> "_lib.PeerDesc":
@@ -147,6 +175,31 @@ class SlabStepper:
         prev, nxt = ring_neighbours(self.rank, self.world)
         self.attach_peers(_lib.PeerDesc.from_buffer_copy(blobs[prev]),
                           _lib.PeerDesc.from_buffer_copy(blobs[nxt]))
+
+    def _try_attach_peers(self) -> bool:
+        """_attach_peers that never skips a collective: a rank that cannot
+        export or map still joins the descriptor exchange, and reports."""
+        try:
+            mine = bytes(self.export_peer())
+        except Exception:  # noqa: BLE001 - reported through the return value
+            mine = None
+        if self.world == 1:
+            blobs = [mine]
+        else:
+            import torch.distributed as dist
+
+            blobs = [None] * self.world
+            dist.all_gather_object(blobs, mine)
+            self._dist_ring = True
+        if any(b is None for b in blobs):
+            return False
+        prev, nxt = ring_neighbours(self.rank, self.world)
+        try:
+            self.attach_peers(_lib.PeerDesc.from_buffer_copy(blobs[prev]),
+                              _lib.PeerDesc.from_buffer_copy(blobs[nxt]))
+        except Exception:  # noqa: BLE001 - reported through the return value
+            return False
+        return True
 
     def _attach_ring(self):
         """NCCL communicator for the ring (id from rank 0, shared through

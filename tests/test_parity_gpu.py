@@ -532,7 +532,8 @@ def _ipc_rank(rank, world, port, rows, cols, iters, q, gene7=None):
         orc = Oracle()
         u0, v0 = orc.init(2, rows, cols, 9)
         S = rows // world
-        s = SlabStepper(rows, cols, rank=rank, world=world, ghost=4, device=0, transport="p2p")
+        s = SlabStepper(rows, cols, rank=rank, world=world, ghost=4, device=0, transport="auto")
+        assert s.transport == "p2p"  # auto picks the fused peer ring when IPC mapping works
         if gene7 is not None:
             import paper_2102_10340_b200 as fhn_
             s.set_params(fhn_.Gene(**gene7))
