@@ -176,8 +176,9 @@ int rdcnn_slab_poll_blowup(rdcnn_sim_t sim, int* bad, unsigned* tag);
 int rdcnn_nccl_unique_id(uint8_t id[128]);
 int rdcnn_slab_attach_ring(rdcnn_sim_t sim, const uint8_t id[128], int rank,
                            int world);
-/* Exchange the front buffer's edge rows into the ring's ghosts (once, after
- * initialising the slabs; NCCL ring or peer ring). */
+/* NCCL ring: exchange the front buffer's edge rows into the ring's ghosts
+ * (once, after initialising the slabs).  Peer ring: only completes the
+ * state (the neighbours read it in place); barrier the ranks afterwards. */
 int rdcnn_slab_fill_ghosts(rdcnn_sim_t sim);
 /* Advance by `steps`.  Peer ring: one fused launch per block of k <= ghost
  * levels.  NCCL ring: per block, boundary kernel -> NCCL ring exchange on a
@@ -188,12 +189,13 @@ int rdcnn_slab_advance(rdcnn_sim_t sim, long steps, long* first_bad);
 
 /* Fused peer ring (the default multi-GPU transport): the halo exchange runs
  * INSIDE the step kernel.  Per block, one launch computes every owned row;
- * the warps producing the first/last `ghost` rows also store them straight
- * into the ring neighbours' ghost rows (peer memory: CUDA IPC mappings over
- * NVLink, or plain pointers when the neighbour lives in the same process),
- * then publish a per-direction "delivered" word with a release store; the
- * neighbours' edge warps acquire it before reading their ghosts.  No NCCL,
- * no exchange copies, no host work per block.
+ * the warps producing the first/last `ghost` rows stage the level-0 rows
+ * beyond the slab straight from the ring neighbours' input buffers (peer
+ * memory: CUDA IPC mappings over NVLink, or plain pointers when the
+ * neighbour lives in the same process) and, when done, publish a
+ * per-direction word with a release store ("my edge rows are written, and I
+ * have finished reading yours"); the neighbours' edge warps acquire it.  No
+ * NCCL, no exchange copies, no host work per block.
  *
  * Protocol: every rank exports its descriptor, the descriptors are shared
  * (e.g. torch.distributed all_gather_object), every rank attaches with its

@@ -69,12 +69,12 @@ struct StepArgsT {
   unsigned* flags;        // per grid: 0 clean, else tag of the first bad launch
   unsigned tag;           // this launch's tag (launch index + 1)
   // Fused peer halo exchange (kPeer instances, slab mode only).
-  // Level-K edge rows are also stored straight into the ring neighbours'
-  // ghost rows of THEIR output buffer (peer memory: CUDA IPC over NVLink, or
-  // the same device), and the edge warps signal completion with one release
-  // store per block and direction.
-  T* peer_top;            // prev rank's bottom ghost row 0 (receives owned row 0)
-  T* peer_bot;            // next rank's top ghost row 0 (receives owned row rows-ghost)
+  // The level-0 rows beyond the slab are read straight from the ring
+  // neighbours' INPUT buffers (peer memory: CUDA IPC over NVLink, or the same
+  // device); the edge warps signal completion with one release store per
+  // block and direction.
+  const T* peer_top;      // prev rank's owned row rows_prev (one past its last) in its input buffer
+  const T* peer_bot;      // next rank's owned row 0 in its input buffer
   unsigned* edge_count;   // [2] this rank's completion counters: top / bottom edge warps
   unsigned* sig_prev;     // prev rank's "bottom ghosts delivered" word
   unsigned* sig_next;     // next rank's "top ghosts delivered" word
@@ -443,8 +443,8 @@ struct MinBlocks {
 // kWrap: full-width bands (halo_groups == 0, cols == 32*W), see level_row.
 //
 // kPeer (slab mode): the launch covers every owned row of the slab; warps
-// whose segment reads ghost rows first wait for the neighbour's "delivered"
-// word, store their edge rows into the neighbour's ghosts as well as locally,
+// whose segment reaches beyond it first wait for the neighbour's word, then
+// stage those rows straight from the neighbour's input buffer (peer memory)
 // and publish completion -- the halo exchange is fused into the step.
 template <int K, int W, class T, bool kFast, bool kPerGrid, bool kPeer = false, bool kWrap = false>
 __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
@@ -502,21 +502,18 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
   const int n_load = h + 2 * K;       // level-0 rows x_0 .. x_{n_load-1}
   const int nt = h + 3 * K - 1;       // ticks until level K has produced h rows
 
-  // Fused exchange: a warp reads top (bottom) ghosts iff it produces one of
-  // the first (last) `ghost` rows.  Wait until the neighbour has delivered
-  // this block's ghosts -- the same signal says it has finished reading the
-  // ghost rows of ours that this block's edge stores overwrite.
+  // Fused exchange: a warp reads the previous (next) rank's last (first)
+  // rows iff it produces one of the first (last) `ghost` rows.  Wait until
+  // that neighbour's edge warps of the previous block are done -- they wrote
+  // those rows.  Our own signal at the end tells the neighbour we are done
+  // reading them, so its next write of that buffer (two blocks on) cannot
+  // race our reads.
   bool top_edge = false, bot_edge = false;
-  int orow = r0;
-  T* ptop = nullptr;
-  T* pbot = nullptr;
   if constexpr (kPeer) {
     top_edge = r0 < a.ghost;
     bot_edge = r0 + h > a.rows - a.ghost;
     if (top_edge) wait_ready(a.ready + 0, a.seq);
     if (bot_edge) wait_ready(a.ready + 1, a.seq);
-    ptop = a.peer_top + (size_t)grp * W;
-    pbot = a.peer_bot + (size_t)grp * W - (size_t)(a.rows - a.ghost) * pitch;
   }
 
   // Running source row (wraps on the torus; never in ghosted slabs) and
@@ -526,11 +523,47 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
   const ptrdiff_t vdelta = vin - uin;
   int rows_left = a.periodic ? a.rows - r_first : 0x7FFFFFFF;
   const size_t span = (size_t)a.rows * pitch;
+  // kPeer pulls the rows beyond its slab straight from the ring neighbours'
+  // input buffers (peer memory): the running source pointer starts in the
+  // previous rank's last rows and jumps into this slab -- and from this
+  // slab's end into the next rank's first rows -- exactly like the torus
+  // wrap jumps, so the tick loop is unchanged.
+  ptrdiff_t jump = -(ptrdiff_t)span, jump2 = 0;
+  int rows_left2 = a.rows;
+  if constexpr (kPeer) {
+    auto delta = [](const T* to, const T* from) {
+      return (ptrdiff_t)(((intptr_t)to - (intptr_t)from) / (intptr_t)sizeof(T));
+    };
+    const T* local0 = uin + (size_t)a.ghost * pitch;       // owned row 0 (this lane's columns)
+    const T* local_end = local0 + (size_t)a.rows * pitch;  // owned row `rows`
+    const T* prev_end = a.peer_top + (size_t)grp * W;      // prev's owned row rows_prev
+    const T* next0 = a.peer_bot + (size_t)grp * W;         // next's owned row 0
+    const int rf = r0 - K;
+    rows_left2 = 0x7FFFFFFF;
+    if (rf < 0) {
+      su = prev_end + (ptrdiff_t)rf * (ptrdiff_t)pitch;
+      rows_left = -rf;
+      jump = delta(local0, prev_end);
+      rows_left2 = a.rows;
+      jump2 = delta(next0, local_end);
+    } else {
+      su = local0 + (size_t)rf * pitch;
+      rows_left = a.rows - rf;
+      jump = delta(next0, local_end);
+    }
+  }
   auto src_next = [&]() {
     su += pitch;
     if (--rows_left == 0) {
-      su -= span;
-      rows_left = a.rows;
+      if constexpr (kPeer) {
+        su += jump;
+        rows_left = rows_left2;
+        jump = jump2;
+        rows_left2 = 0x7FFFFFFF;
+      } else {
+        su -= span;
+        rows_left = a.rows;
+      }
     }
   };
   T* du = uout + (size_t)(a.periodic ? r0 : r0 + a.ghost) * pitch;
@@ -623,15 +656,8 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
           if (store) {
             store_row<W, T>(du, du + vout_delta, 0, o);
             fold_finite<W, T>(fin, o);
-            if constexpr (kPeer) {
-              if (orow < a.ghost)
-                store_row<W, T>(ptop, ptop + vout_delta, (size_t)orow * pitch, o);
-              else if (orow >= a.rows - a.ghost)
-                store_row<W, T>(pbot, pbot + vout_delta, (size_t)orow * pitch, o);
-            }
           }
           du += pitch;
-          if constexpr (kPeer) ++orow;
         }
       }
     }
@@ -662,15 +688,8 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
         if (store) {
           store_row<W, T>(du, du + vout_delta, 0, o);
           fold_finite<W, T>(fin, o);
-          if constexpr (kPeer) {
-            if (orow < a.ghost)
-              store_row<W, T>(ptop, ptop + vout_delta, (size_t)orow * pitch, o);
-            else if (orow >= a.rows - a.ghost)
-              store_row<W, T>(pbot, pbot + vout_delta, (size_t)orow * pitch, o);
-          }
         }
         du += pitch;
-        if constexpr (kPeer) ++orow;
       } else {
         level_row<W, T, kFast, kWrap>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
       }
@@ -718,7 +737,7 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
 
   if constexpr (kPeer) {
     if (top_edge || bot_edge) {
-      __threadfence_system();  // this lane's peer stores before the count
+      __threadfence_system();  // this lane's reads of the neighbours' rows are done
       __syncwarp();
       if (lane == 0) {
         if (top_edge) edge_done(a.edge_count + 0, a.n_top, a.sig_prev, a.seq + 1u);

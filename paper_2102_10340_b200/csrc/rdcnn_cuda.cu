@@ -1042,10 +1042,10 @@ int slab_step_impl(rdcnn_sim* s, int k, cudaStream_t st, bool boundary) {
 int peer_block(rdcnn_sim* s, int k, unsigned tag, cudaStream_t st) {
   StepArgsT<float> a = base_args<float>(s, s->cur, s->cur ^ 1);
   a.tag = tag;
-  const int ob = s->cur ^ 1;
+  const int ib = s->cur;  // the neighbours' INPUT buffers (all ranks run the same blocks)
   const size_t pitch = (size_t)s->pitch;
-  a.peer_top = static_cast<float*>(s->peer_buf[0][ob]) + (size_t)(s->ghost + s->peer_rows[0]) * pitch;
-  a.peer_bot = static_cast<float*>(s->peer_buf[1][ob]);
+  a.peer_top = static_cast<const float*>(s->peer_buf[0][ib]) + (size_t)(s->ghost + s->peer_rows[0]) * pitch;
+  a.peer_bot = static_cast<const float*>(s->peer_buf[1][ib]) + (size_t)s->ghost * pitch;
   a.edge_count = s->p2p_words + 2;
   a.sig_prev = s->peer_words[0] + 1;
   a.sig_next = s->peer_words[1] + 0;
@@ -1652,17 +1652,10 @@ int rdcnn_slab_fill_ghosts(rdcnn_sim_t s) {
   if (!s || !s->slab || (!s->comm_stream && !s->p2p)) return fail(RDCNN_EINVAL, "slab ring not attached");
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   if (s->p2p) {
-    // Own edge rows of the front buffer into the neighbours' front ghosts
-    // (peer copies); the caller barriers the ranks before the first block.
-    const size_t pitch = (size_t)s->pitch, g = (size_t)s->ghost, S = (size_t)s->rows;
-    float* mine = s->u_ptr<float>(s->cur);
-    float* prev_bottom = static_cast<float*>(s->peer_buf[0][s->cur]) + (g + (size_t)s->peer_rows[0]) * pitch;
-    float* next_top = static_cast<float*>(s->peer_buf[1][s->cur]);
-    const size_t bytes = g * pitch * sizeof(float);
-    RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
-    RDCNN_CUDA_TRY(cudaMemcpyAsync(prev_bottom, mine + g * pitch, bytes, cudaMemcpyDefault, s->stream));
-    RDCNN_CUDA_TRY(cudaMemcpyAsync(next_top, mine + S * pitch, bytes, cudaMemcpyDefault, s->stream));
-    RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+    // The peer ring reads the neighbours' rows in place: nothing to copy.
+    // The state must be complete before any neighbour's first block reads
+    // it; the caller barriers the ranks after this returns.
+    RDCNN_CUDA_TRY(cudaDeviceSynchronize());
     return RDCNN_OK;
   }
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
