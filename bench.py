@@ -354,14 +354,13 @@ def bench_ours(args, rank, world, local_rank):
     # ---- roofline of the dominant kernel (the K-level wavefront stencil) ----
     peaks, peak_kind = measured_peaks()
     per_rank_cells = wl.rows_rank * n
-    launches_per_rank = max(launches, 1)
     transport = slab.transport if (world > 1 or args.slab) else None
-    if transport == "nccl":
-        # 3 launches per block (two boundary strips + interior); the interior
-        # carries ~all the work, so the per-block time is the launch figure
-        launches_per_rank = max(launches // 3, 1)
-    avg_launch_s = (t_ms / 1e3) / launches_per_rank
     levels = args.levels
+    # One K-level block = one launch on the per-launch path; the persistent
+    # wavefront kernel runs every block of an advance in one launch, so the
+    # unit is the block (iterations / K), measured live by the CUDA events.
+    blocks_per_rank = max(S * args.steps // levels, 1)
+    avg_launch_s = (t_ms / 1e3) / blocks_per_rank
     alg_bytes_per_launch = BYTES_PER_CELL_UPDATE * per_rank_cells * levels
     achieved_gbs = alg_bytes_per_launch / avg_launch_s / 1e9
     traffic, traffic_units = ncu_traffic()
@@ -374,10 +373,10 @@ def bench_ours(args, rank, world, local_rank):
         "bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": peaks["hbm_gbs"],
         "unit": "GB/s", "frac": round(achieved_gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback",
-        "note": (f"achieved = 16 B x cells x {levels} levels per launch / avg launch time "
-                 f"({avg_launch_s * 1e6:.1f} us over {launches_per_rank} launches); with {levels}-level "
-                 "temporal blocking the kernel reads/writes HBM once per launch, so frac > 1 "
-                 "is expected and the FP32 pipe is the binding roof (see fp32)"),
+        "note": (f"achieved = 16 B x cells x {levels} levels per K-level block / avg block time "
+                 f"({avg_launch_s * 1e6:.1f} us over {blocks_per_rank} blocks, {launches} launches); "
+                 f"with {levels}-level temporal blocking the kernel reads/writes HBM once per block, "
+                 "so frac > 1 is expected and the FP32 pipe is the binding roof (see fp32)"),
         "fp32": {"achieved_tops": round(fp32_achieved, 2), "peak_tops": round(fp32_peak_tops, 2),
                  "frac": round(fp32_achieved / fp32_peak_tops, 4),
                  "basis": "27 FP32 ops per cell-update; peak = 148 SM x 128 lanes x median SM clock"},

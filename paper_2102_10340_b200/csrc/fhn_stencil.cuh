@@ -424,57 +424,15 @@ struct MinBlocks {
   static constexpr int value = kWarps / kWarpsPerCta;
 };
 
-// K levels per launch, W columns per lane, element type T.
-//
-// Schedule (a skewed wavefront, levels visited top-down within a tick): at
-// tick j the warp has level-0 rows x_0..x_j (x_j = r0 - K + j) and
-//   level t computes row x_j - (2t - 1) from the three level-(t-1) rows
-//   produced at ticks j-3, j-2, j-1 (level 1: the level-0 rows of ticks
-//   j-2, j-1, j, read back from the staging ring).
-// Visiting t = K..1 means no level consumes a row produced in the same tick,
-// so the K level updates of one tick are independent instruction streams the
-// scheduler can interleave, and each level's oldest row slot can be
-// overwritten in place once the level above has read it.
-//
-// Register rotation: level-t rows (t = 1..K-1) live in rings of 3 (tick j ->
-// slot j % 3); the tick loop is unrolled by 3 so every slot index is a
-// compile-time constant and no register is copied to advance a window.
-//
-// kWrap: full-width bands (halo_groups == 0, cols == 32*W), see level_row.
-//
-// kPeer (slab mode): the launch covers every owned row of the slab; warps
-// whose segment reaches beyond it first wait for the neighbour's word, then
-// stage those rows straight from the neighbour's input buffer (peer memory)
-// and publish completion -- the halo exchange is fused into the step.
-template <int K, int W, class T, bool kFast, bool kPerGrid, bool kPeer = false, bool kWrap = false>
-__global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
-    fhn_wavefront_kernel(const StepArgsT<T> a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31;
-  const int wib = kWarpsPerCta == 1 ? 0 : int(threadIdx.x >> 5);
-  const long long warp_id = (long long)blockIdx.x * kWarpsPerCta + wib;
-  const long long per_grid = (long long)a.n_segs * a.n_bands;
-  if (warp_id >= per_grid * a.batch) return;
-  unsigned long long t_start = 0;
-  if (a.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-  const int g = int(warp_id / per_grid);
-  const int rem = int(warp_id - (long long)g * per_grid);
-  const int band = rem % a.n_bands;
-  const int seg = rem / a.n_bands;
-
-  // A grid that already blew up in an earlier launch of this advance stays
-  // frozen (no stores), so the input of its first bad launch survives for
-  // the host-side replay.  A flag carrying this launch's own tag was raised
-  // by a sibling warp (or, in slab mode, by the boundary launch of the same
-  // block) and does not freeze.  The flag is only needed at the first store.
-  // Programmatic dependent launch: the next launch of the advance may start
-  // its CTAs in this one's tail; nothing global is read before the previous
-  // launch has completed (no-ops when launched without the PDL attribute).
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  const unsigned fl = a.flags != nullptr ? *(volatile unsigned*)(a.flags + g) : 0u;
-  const unsigned frozen = fl != 0u && fl != a.tag;
-
+// One K-level block of one warp's band x segment: stage, step, store;
+// returns whether a stored value was non-finite (folded over the warp).
+// (A persistent variant that looped over blocks, each warp waiting only for
+// its 8 neighbours, measured 2.5 % slower than launches + PDL: profiles/.)
+template <int K, int W, class T, bool kFast, bool kPerGrid, bool kPeer, bool kWrap>
+__device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned char* smem_raw, int lane, int wib,
+                                                int g, int band, int seg, unsigned frozen,
+                                                const T* __restrict__ u_in_b, const T* __restrict__ v_in_b,
+                                                T* __restrict__ u_out_b, T* __restrict__ v_out_b) {
   // Shared gene: read straight from the kernel-parameter bank.  Per-grid
   // genes (sweeps) come from global memory once per warp.
   const ParamsT<T> p = kPerGrid ? a.params[g] : a.shared;
@@ -491,10 +449,10 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
   const int lane_r = (lane + 1) & 31;
 
   const size_t goff = (size_t)g * (size_t)a.grid_stride + (size_t)grp * W;
-  const T* __restrict__ uin = a.u_in + goff;
-  const T* __restrict__ vin = a.v_in + goff;
-  T* __restrict__ uout = a.u_out + goff;
-  T* __restrict__ vout = a.v_out + goff;
+  const T* __restrict__ uin = u_in_b + goff;
+  const T* __restrict__ vin = v_in_b + goff;
+  T* __restrict__ uout = u_out_b + goff;
+  T* __restrict__ vout = v_out_b + goff;
   const size_t pitch = (size_t)a.pitch;
 
   const int r0 = a.row_begin + seg * a.seg_rows;
@@ -592,7 +550,7 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
     bytes_a = (uint32_t)na * kLaneBytes;
     bytes_b = 32u * kLaneBytes - bytes_a;
     d_b = -(ptrdiff_t)grp0 * W;  // group 0 relative to lane 0's group
-    ub = a.u_in + (size_t)g * (size_t)a.grid_stride + (size_t)grp0 * W + (size_t)r_first * pitch;
+    ub = u_in_b + (size_t)g * (size_t)a.grid_stride + (size_t)grp0 * W + (size_t)r_first * pitch;
     if (elect_one()) {
 #pragma unroll
       for (int q = 0; q < kStage; ++q)
@@ -724,17 +682,6 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
   }
   if constexpr (!kBulk) stage_wait<0>();
 
-  if (fin.bad_in_warp() && lane == 0 && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);
-  if (a.trace != nullptr && lane == 0) {
-    unsigned long long t_end;
-    unsigned smid;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    a.trace[3 * warp_id] = t_start;
-    a.trace[3 * warp_id + 1] = t_end;
-    a.trace[3 * warp_id + 2] = smid;
-  }
-
   if constexpr (kPeer) {
     if (top_edge || bot_edge) {
       __threadfence_system();  // this lane's reads of the neighbours' rows are done
@@ -745,6 +692,75 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
       }
     }
   }
+
+  return fin.bad_in_warp();
+}
+
+// K levels per launch, W columns per lane, element type T.
+//
+// Schedule (a skewed wavefront, levels visited top-down within a tick): at
+// tick j the warp has level-0 rows x_0..x_j (x_j = r0 - K + j) and
+//   level t computes row x_j - (2t - 1) from the three level-(t-1) rows
+//   produced at ticks j-3, j-2, j-1 (level 1: the level-0 rows of ticks
+//   j-2, j-1, j, read back from the staging ring).
+// Visiting t = K..1 means no level consumes a row produced in the same tick,
+// so the K level updates of one tick are independent instruction streams the
+// scheduler can interleave, and each level's oldest row slot can be
+// overwritten in place once the level above has read it.
+//
+// Register rotation: level-t rows (t = 1..K-1) live in rings of 3 (tick j ->
+// slot j % 3); the tick loop is unrolled by 3 so every slot index is a
+// compile-time constant and no register is copied to advance a window.
+//
+// kWrap: full-width bands (halo_groups == 0, cols == 32*W), see level_row.
+//
+// kPeer (slab mode): the launch covers every owned row of the slab; warps
+// whose segment reaches beyond it first wait for the neighbour's word, then
+// stage those rows straight from the neighbour's input buffer (peer memory)
+// and publish completion -- the halo exchange is fused into the step.
+template <int K, int W, class T, bool kFast, bool kPerGrid, bool kPeer = false, bool kWrap = false>
+__global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
+    fhn_wavefront_kernel(const StepArgsT<T> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = kWarpsPerCta == 1 ? 0 : int(threadIdx.x >> 5);
+  const long long warp_id = (long long)blockIdx.x * kWarpsPerCta + wib;
+  const long long per_grid = (long long)a.n_segs * a.n_bands;
+  if (warp_id >= per_grid * a.batch) return;
+  unsigned long long t_start = 0;
+  if (a.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  const int g = int(warp_id / per_grid);
+  const int rem = int(warp_id - (long long)g * per_grid);
+  const int band = rem % a.n_bands;
+  const int seg = rem / a.n_bands;
+
+  // A grid that already blew up in an earlier launch of this advance stays
+  // frozen (no stores), so the input of its first bad launch survives for
+  // the host-side replay.  A flag carrying this launch's own tag was raised
+  // by a sibling warp (or, in slab mode, by the boundary launch of the same
+  // block) and does not freeze.  The flag is only needed at the first store.
+  // Programmatic dependent launch: the next launch of the advance may start
+  // its CTAs in this one's tail; nothing global is read before the previous
+  // launch has completed (no-ops when launched without the PDL attribute).
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  const unsigned fl = a.flags != nullptr ? *(volatile unsigned*)(a.flags + g) : 0u;
+  const unsigned frozen = fl != 0u && fl != a.tag;
+
+  const bool bad = wavefront_block<K, W, T, kFast, kPerGrid, kPeer, kWrap>(
+      a, smem_raw, lane, wib, g, band, seg, frozen, a.u_in, a.v_in, a.u_out, a.v_out);
+
+  if (bad && lane == 0 && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);
+  if (a.trace != nullptr && lane == 0) {
+    unsigned long long t_end;
+    unsigned smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    a.trace[3 * warp_id] = t_start;
+    a.trace[3 * warp_id + 1] = t_end;
+    a.trace[3 * warp_id + 2] = smid;
+  }
+
 }
 
 }  // namespace rdcnn_dev

@@ -869,14 +869,7 @@ int cluster_advance(rdcnn_sim* s, const ClusterPlan& pl, long steps, long* first
 }
 
 template <class T>
-int advance_impl(rdcnn_sim* s, long steps, long* first_bad) {
-  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
-  if constexpr (sizeof(T) == 4) {
-    ClusterPlan pl;
-    if (steps > 0 && cluster_plan_for(s, &pl)) return cluster_advance(s, pl, steps, first_bad);
-    if (s->cluster_mode > 0) return fail(RDCNN_EINVAL, "persistent cluster path required but %dx%d (batch %d) does not fit it",
-                                         s->rows, s->cols, s->batch);
-  }
+int advance_launches(rdcnn_sim* s, long steps, long* first_bad) {
   s->launches = 0;
   if (first_bad)
     for (int g = 0; g < s->batch; ++g) first_bad[g] = 0;
@@ -911,6 +904,18 @@ int advance_impl(rdcnn_sim* s, long steps, long* first_bad) {
   }
   if (any) return fail(RDCNN_EBLOWUP, "blow-up: non-finite state");
   return RDCNN_OK;
+}
+
+template <class T>
+int advance_impl(rdcnn_sim* s, long steps, long* first_bad) {
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  if constexpr (sizeof(T) == 4) {
+    ClusterPlan pl;
+    if (steps > 0 && cluster_plan_for(s, &pl)) return cluster_advance(s, pl, steps, first_bad);
+    if (s->cluster_mode > 0) return fail(RDCNN_EINVAL, "persistent cluster path required but %dx%d (batch %d) does not fit it",
+                                         s->rows, s->cols, s->batch);
+  }
+  return advance_launches<T>(s, steps, first_bad);
 }
 
 int copy_state(rdcnn_sim* s, void* u, void* v, bool upload) {
