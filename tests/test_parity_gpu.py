@@ -548,17 +548,17 @@ def _ipc_rank(rank, world, port, rows, cols, iters, q, gene7=None):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("blowup", (False, True))
-def test_peer_ring_two_processes_ipc(oracle, blowup):
-    """Two processes (one slab each) on one GPU: the peer memory is opened
+@pytest.mark.parametrize("world,blowup", [(2, False), (2, True), (3, False), (3, True)])
+def test_peer_ring_processes_ipc(oracle, world, blowup):
+    """2 or 3 processes (one slab each) on one GPU: the peer memory is opened
     from CUDA IPC handles shared over torch.distributed, as on a multi-GPU
-    box; the result equals the unsplit oracle run.  With an unstable gene
-    both ranks agree on the exact blow-up iteration and hold the oracle's
-    post-blow-up state."""
+    box (world 3: distinct previous and next neighbours); the result equals
+    the unsplit oracle run.  With an unstable gene every rank agrees on the
+    exact blow-up iteration and holds the oracle's post-blow-up state."""
     import multiprocessing as mp
     import socket
 
-    rows, cols, world = 48, 64, 2
+    rows, cols = 48, 64
     gene = fhn.Gene(Du=2.6) if blowup else fhn.Gene()
     iters = 400 if blowup else 21
     u0, v0 = oracle.init(2, rows, cols, 9)
@@ -585,7 +585,7 @@ def test_peer_ring_two_processes_ipc(oracle, blowup):
     assert all(p.exitcode == 0 for p in procs)
     got_u = np.concatenate([np.frombuffer(r[2], np.float32) for r in res])
     got_v = np.concatenate([np.frombuffer(r[3], np.float32) for r in res])
-    assert [r[1] for r in res] == [want, want]
+    assert [r[1] for r in res] == [want] * world
     fin = np.isfinite(ou) & np.isfinite(ov)
     assert np.array_equal(np.isfinite(got_u), np.isfinite(ou))
     assert np.array_equal(bits(got_u)[fin], bits(ou)[fin]) and np.array_equal(bits(got_v)[fin], bits(ov)[fin])
