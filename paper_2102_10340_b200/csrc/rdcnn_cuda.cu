@@ -150,6 +150,7 @@ int resident_blocks(int k, int w, bool fast, bool per_grid, bool wrap) {
 // advance overlap launch latency and prologue with the previous launch's
 // tail; the kernel issues griddepcontrol.wait before its first global read.
 // Measured +4 % at 4096^2, K=4 (779k -> 810k).  RDCNN_PDL=0 turns it off.
+// Used only for launches that fill the chip (see launch_pdl).
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("RDCNN_PDL");
@@ -158,9 +159,15 @@ bool pdl_enabled() {
   return on;
 }
 
+// `full`: the launch fills at least 3/4 of the resident warp slots.  A
+// smaller launch must not use PDL: the next launch's CTAs would be
+// dispatched at once into the many free slots and wait in
+// griddepcontrol.wait beside the running warps, slowing them (1024^2, 49 %
+// of the slots: 252k with PDL vs 341k without; 1536^2, 94 %: 519k vs 461k).
 template <class Args>
-cudaError_t launch_pdl(void (*fn)(Args), unsigned blocks, size_t smem, cudaStream_t s, const Args& a) {
-  if (!pdl_enabled()) {
+cudaError_t launch_pdl(void (*fn)(Args), unsigned blocks, size_t smem, cudaStream_t s, const Args& a,
+                       bool full = true) {
+  if (!pdl_enabled() || !full) {
     fn<<<dim3(blocks), dim3(kThreads), smem, s>>>(a);
     return cudaGetLastError();
   }
@@ -223,13 +230,13 @@ int peer_resident_blocks(int k, int w, bool fast, bool wrap) {
 
 template <class T>
 cudaError_t launch_stencil(int k, int w, bool fast, bool per_grid, bool wrap, const StepArgsT<T>& a,
-                           long long warps, cudaStream_t s) {
+                           long long warps, cudaStream_t s, bool full) {
   if (warps <= 0) return cudaSuccess;
   if (k != 1 && k != 2 && k != 4 && k != 8) return cudaErrorInvalidValue;
   auto fn = table<T>().fn[w > 1][k_index(k)][fast][per_grid][wrap];
   if (!fn) return cudaErrorInvalidValue;
   const long long blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
-  return launch_pdl(fn, (unsigned)blocks, smem_for<T>(w), s, a);
+  return launch_pdl(fn, (unsigned)blocks, smem_for<T>(w), s, a, full);
 }
 
 // Band/segment decomposition of one launch.
@@ -597,7 +604,8 @@ cudaError_t launch_range(rdcnn_sim* s, int k, StepArgsT<T> a, int row_begin, int
   a.band_groups = p.band_groups;
   a.halo_groups = p.halo;
   ++s->launches;
-  return launch_stencil<T>(k, w, fast, per_grid, wrap, a, p.warps, st);
+  return launch_stencil<T>(k, w, fast, per_grid, wrap, a, p.warps, st,
+                           4 * p.warps >= 3LL * rw * s->sm_count);
 }
 
 int alloc_common(rdcnn_sim* s) {
@@ -1072,7 +1080,7 @@ int peer_block(rdcnn_sim* s, int k, unsigned tag, cudaStream_t st) {
   a.n_top = p.n_bands * std::min(p.n_segs, (g + h - 1) / h);  // segments with r0 < g
   a.n_bot = p.n_bands * (p.n_segs - (S - g) / h);             // segments with r0 + h > S - g
   auto fn = peer_table().fn[w > 1][k_index(k)][fast][wrap];
-  RDCNN_CUDA_TRY(launch_pdl(fn, (unsigned)p.warps, smem_for<float>(w), st, a));
+  RDCNN_CUDA_TRY(launch_pdl(fn, (unsigned)p.warps, smem_for<float>(w), st, a, 4 * p.warps >= 3LL * rw * s->sm_count));
   ++s->launches;
   ++s->p2p_seq;
   s->cur ^= 1;
