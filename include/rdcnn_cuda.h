@@ -202,7 +202,7 @@ int rdcnn_slab_advance(rdcnn_sim_t sim, long steps, long* first_bad);
  * ring neighbours' descriptors (prev = rank-1, next = rank+1 mod world; world
  * 1 passes its own), calls rdcnn_slab_fill_ghosts, and the ranks barrier once
  * before the first block.  All ranks must then run the same blocks.  Destroy
- * only after a barrier (neighbours write into this slab's ghost rows). */
+ * only after a barrier (neighbours read this slab's rows in place). */
 typedef struct {
   uint8_t ipc[3][64];   /* cudaIpcMemHandle_t: buffer 0, buffer 1, sync words */
   uint64_t ptr[3];      /* the same allocations as device pointers (exporter's process) */
@@ -216,7 +216,7 @@ int rdcnn_slab_attach_peers(rdcnn_sim_t sim, int rank, int world,
                             const rdcnn_slab_peer_desc* next);
 /* One fused block of k levels on `stream` (NULL: the handle's stream); for
  * drivers that interleave several in-process ranks on one stream.  The ring
- * must have been filled (rdcnn_slab_fill_ghosts). */
+ * must have been made ready (rdcnn_slab_fill_ghosts + a barrier). */
 int rdcnn_slab_step_fused(rdcnn_sim_t sim, int k, void* stream);
 
 /* Exact blow-up iteration for slab runs (engine.hpp:79 BlowUpError(iter+1)).

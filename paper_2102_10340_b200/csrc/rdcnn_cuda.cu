@@ -1506,7 +1506,8 @@ int rdcnn_slab_poll_blowup(rdcnn_sim_t s, int* bad, unsigned* tag) {
   return RDCNN_OK;
 }
 
-// ---- native slab ring: NCCL halo exchange overlapped with the interior -------
+// ---- native slab ring: NCCL transport (boundary launch, NCCL send/recv of the
+// ghost rows on a comm stream overlapped with the interior launch) ----------
 
 int rdcnn_nccl_unique_id(uint8_t id[128]) {
   if (!id) return fail(RDCNN_EINVAL, "null argument");
