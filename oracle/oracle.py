@@ -197,21 +197,37 @@ class Reference:
         return int(self.L.ref_checksum_f32(rows, cols, _p(np.ascontiguousarray(u)), _p(np.ascontiguousarray(v))))
 
     def sweep_labels(self, x_param, xs, y_param, ys, gene7=DEFAULT_GENE7, ka=1.0, typ=1, nn=32, nm=32,
-                     iter_max=100, nssp=5, seed=42, per_cell_seed=False) -> str:
+                     iter_max=100, nssp=5, seed=42, per_cell_seed=False, parallel_cells=False) -> str:
         """The reference's sweep_grid labels CSV (sweep.hpp:227-247)."""
-        f = self.L.ref_sweep_labels_f32
+        f = self.L.ref_sweep_labels_par_f32 if parallel_cells else self.L.ref_sweep_labels_f32
         f.restype = c_int
         f.argtypes = [ctypes.c_char_p, c_void_p, c_int, ctypes.c_char_p, c_void_p, c_int, c_void_p, c_int,
                       c_int, c_int, c_long, c_int, c_uint64, c_int, ctypes.c_char_p, c_size_t]
         xa = np.asarray(xs, np.float64)
         ya = np.asarray(ys, np.float64)
         g8 = np.asarray(list(gene7) + [ka], np.float64)
-        buf = ctypes.create_string_buffer(1 << 20)
+        buf = ctypes.create_string_buffer(1 << 22)
         rc = f(x_param.encode(), _p(xa), len(xa), y_param.encode(), _p(ya), len(ya), _p(g8), typ, nn, nm,
                iter_max, nssp, seed, int(per_cell_seed), buf, len(buf))
         if rc != 0:
             raise ValueError("reference sweep_grid rejected the spec")
         return buf.value.decode()
+
+    def init_image(self, path: str, ka: float = 1.0):
+        """The reference's typ=3 state from an image file (load_grayscale +
+        init_from_image); returns (rows, cols, u, v)."""
+        f = self.L.ref_init_image_f32
+        f.restype = c_int
+        f.argtypes = [ctypes.c_char_p, c_double, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t]
+        r, c = ctypes.c_int(), ctypes.c_int()
+        cap = 1 << 27
+        u = np.empty(cap, np.float32)
+        v = np.empty(cap, np.float32)
+        rc = f(path.encode(), ka, ctypes.byref(r), ctypes.byref(c), _p(u), _p(v), cap)
+        if rc != 0:
+            raise ValueError(f"reference could not load {path} (rc {rc})")
+        n = r.value * c.value
+        return r.value, c.value, u[:n].copy(), v[:n].copy()
 
     def format_double(self, x: float) -> str:
         f = self.L.ref_format_double

