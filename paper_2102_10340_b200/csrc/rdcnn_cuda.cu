@@ -513,6 +513,9 @@ struct rdcnn_sim {
   long launches = 0;
   int max_levels = 4;
   int seg_rows = 0;
+  int tuned_seg[4] = {0, 0, 0, 0};  // autotuned segment height per K (0: not tuned)
+  bool tuned[4] = {false, false, false, false};
+  int seg_force = 0;                // set while an autotune candidate runs
   int cluster_mode = 0;       // persistent cluster path: 0 auto, 1 required, -1 off
   long long* d_first_bad = nullptr;  // cluster path result word
   int sm_count = 148;
@@ -586,6 +589,15 @@ StepArgsT<T> base_args(rdcnn_sim* s, int in_buf, int out_buf) {
   return a;
 }
 
+// Segment height override for a launch: an autotune candidate, the user's
+// seg_rows, or the autotuned height (full periodic launches only).
+int seg_for(const rdcnn_sim* s, int k, int row_begin, int row_end) {
+  if (s->seg_force > 0) return s->seg_force;
+  if (s->seg_rows > 0) return s->seg_rows;
+  if (s->slab || row_begin != 0 || row_end != s->rows) return 0;
+  return s->tuned_seg[k_index(k)];
+}
+
 template <class T>
 cudaError_t launch_range(rdcnn_sim* s, int k, StepArgsT<T> a, int row_begin, int row_end,
                          cudaStream_t st) {
@@ -594,7 +606,7 @@ cudaError_t launch_range(rdcnn_sim* s, int k, StepArgsT<T> a, int row_begin, int
   const bool per_grid = a.params_stride != 0;
   const bool wrap = s->cols / w == 32;  // full-width bands (make_plan: halo 0)
   const int rw = resident_blocks<T>(k, w, fast, per_grid, wrap) * (kThreads / 32);
-  Plan p = make_plan(s->cols, w, k, a.batch, row_begin, row_end, s->seg_rows, s->sm_count, rw);
+  Plan p = make_plan(s->cols, w, k, a.batch, row_begin, row_end, seg_for(s, k, row_begin, row_end), s->sm_count, rw);
   if (p.warps == 0) return cudaSuccess;
   a.row_begin = row_begin;
   a.row_end = row_end;
@@ -876,6 +888,76 @@ int cluster_advance(rdcnn_sim* s, const ClusterPlan& pl, long steps, long* first
   return RDCNN_OK;
 }
 
+// Autotuned segment height for lattices that cannot fill the chip.  Their
+// launches are latency-bound and the best height depends on how the warps
+// spread over the SMs' schedulers (512^2: 6 rows run 25 % faster than the
+// plan's 8), which no simple model captures.  Segmentation never changes
+// the arithmetic, so the first long advance times a few candidate heights on
+// its OWN first blocks (3 blocks each, CUDA events) and keeps the fastest
+// per level count; no extra work is done.  An explicit seg_rows disables it.
+template <class T>
+int autotune_segments(rdcnn_sim* s, const Schedule& sched, long* n_io) {
+  const int k = sched.kmax;
+  const int ki = k_index(k);
+  static const bool off = [] {
+    const char* e = std::getenv("RDCNN_AUTOTUNE");
+    return e && e[0] == '0';
+  }();
+  if (off || s->slab || s->seg_rows > 0 || s->tuned[ki]) return RDCNN_OK;
+  const int w = width_for<T>(s);
+  const bool fast = s->mode == RDCNN_FAST, per_grid = s->params_stride != 0, wrap = s->cols / w == 32;
+  const int rw = resident_blocks<T>(k, w, fast, per_grid, wrap) * (kThreads / 32);
+  const Plan p0 = make_plan(s->cols, w, k, s->batch, 0, s->rows, 0, s->sm_count, rw);
+  if (4 * p0.warps >= 3LL * rw * s->sm_count) {  // fills the chip: the plan is right
+    s->tuned[ki] = true;
+    return RDCNN_OK;
+  }
+  static const int kCand[] = {0, 3, 4, 5, 6, 8, 10, 12, 16, 24};
+  constexpr int kReps = 3;
+  std::vector<int> cand;
+  for (int h : kCand)
+    if (h <= s->rows) cand.push_back(h);
+  if (sched.full < (long)(cand.size() * kReps) + 8) return RDCNN_OK;  // too short to tune on
+  std::vector<cudaEvent_t> ev(cand.size() + 1);
+  for (auto& e : ev) RDCNN_CUDA_TRY(cudaEventCreate(&e));
+  long n = *n_io;
+  for (size_t c = 0; c < cand.size(); ++c) {
+    s->seg_force = cand[c];  // 0: the default plan
+    RDCNN_CUDA_TRY(cudaEventRecord(ev[c], s->stream));
+    for (int r = 0; r < kReps; ++r, ++n) {
+      StepArgsT<T> a = base_args<T>(s, s->cur, s->cur ^ 1);
+      a.tag = (unsigned)(n + 1);
+      const int saved = s->tuned_seg[ki];
+      s->tuned_seg[ki] = 0;
+      const cudaError_t e = launch_range<T>(s, k, a, 0, s->rows, s->stream);
+      s->tuned_seg[ki] = saved;
+      if (e != cudaSuccess) {
+        s->seg_force = 0;
+        return fail(RDCNN_ECUDA, "autotune launch failed: %s", cudaGetErrorString(e));
+      }
+      s->cur ^= 1;
+    }
+  }
+  s->seg_force = 0;
+  RDCNN_CUDA_TRY(cudaEventRecord(ev.back(), s->stream));
+  RDCNN_CUDA_TRY(cudaEventSynchronize(ev.back()));
+  float best = 1e30f;
+  int best_h = 0;
+  for (size_t c = 0; c < cand.size(); ++c) {
+    float ms = 0;
+    RDCNN_CUDA_TRY(cudaEventElapsedTime(&ms, ev[c], ev[c + 1]));
+    if (ms < best * 0.98f) {  // prefer the default plan unless clearly faster
+      best = ms;
+      best_h = cand[c];
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  s->tuned_seg[ki] = best_h;
+  s->tuned[ki] = true;
+  *n_io = n;
+  return RDCNN_OK;
+}
+
 template <class T>
 int advance_launches(rdcnn_sim* s, long steps, long* first_bad) {
   s->launches = 0;
@@ -886,7 +968,9 @@ int advance_launches(rdcnn_sim* s, long steps, long* first_bad) {
   const int cur0 = s->cur;
   RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
   const long nl = sched.count();
-  for (long n = 0; n < nl; ++n) {
+  long n = 0;
+  RDCNN_TRY(autotune_segments<T>(s, sched, &n));
+  for (; n < nl; ++n) {
     StepArgsT<T> a = base_args<T>(s, s->cur, s->cur ^ 1);
     a.tag = (unsigned)(n + 1);
     RDCNN_CUDA_TRY(launch_range<T>(s, sched.depth(n), a, 0, s->rows, s->stream));
@@ -1331,6 +1415,10 @@ int rdcnn_sim_set_tuning(rdcnn_sim_t s, int max_levels, int seg_rows) {
   if (seg_rows < 0) return fail(RDCNN_EINVAL, "seg_rows must be >= 0");
   s->max_levels = max_levels;
   s->seg_rows = seg_rows;
+  for (int i = 0; i < 4; ++i) {
+    s->tuned[i] = false;
+    s->tuned_seg[i] = 0;
+  }
   return RDCNN_OK;
 }
 
@@ -1345,7 +1433,7 @@ int rdcnn_sim_trace_launch(rdcnn_sim_t s, int levels, unsigned long long* host_t
   const bool wrap = s->cols / w == 32;
   const int rw = (s->elem == 4 ? resident_blocks<float>(levels, w, fast, per_grid, wrap)
                                : resident_blocks<double>(levels, w, fast, per_grid, wrap)) * (kThreads / 32);
-  const Plan p = make_plan(s->cols, w, levels, s->batch, 0, s->rows, s->seg_rows, s->sm_count, rw);
+  const Plan p = make_plan(s->cols, w, levels, s->batch, 0, s->rows, seg_for(s, levels, 0, s->rows), s->sm_count, rw);
   *n_warps = p.warps;
   if (p.warps > cap) return fail(RDCNN_EINVAL, "trace needs %lld entries", (long long)p.warps);
   unsigned long long* d = nullptr;
