@@ -668,3 +668,21 @@ def test_slab_fast_mode_matches_periodic(ghost):
         assert int(sim.advance(iters)[0]) == 0
         pu, pv = sim.download()
     assert np.array_equal(bits(su), bits(pu)) and np.array_equal(bits(sv), bits(pv))
+
+
+@pytest.mark.parametrize("rows,cols", [(512, 512), (384, 640)])
+def test_autotuned_segments_bit_identical(rows, cols):
+    """A long advance of an under-filled lattice autotunes its segment height
+    on its own first blocks; the result equals a fixed-segment run bit for
+    bit, and a second advance (tuned plan) continues identically."""
+    rng = np.random.default_rng(rows + cols)
+    u0 = rng.random(rows * cols, dtype=np.float32)
+    v0 = rng.random(rows * cols, dtype=np.float32) * 0.3
+    out = []
+    for seg in (0, 7):  # 0: autotune; 7: explicit height (autotune off)
+        with fhn.Simulator(rows, cols, seg_rows=seg, persistent=-1) as sim:
+            sim.upload(u0, v0)
+            assert int(sim.advance(400)[0]) == 0
+            assert int(sim.advance(123)[0]) == 0
+            out.append(sim.download())
+    assert np.array_equal(bits(out[0][0]), bits(out[1][0])) and np.array_equal(bits(out[0][1]), bits(out[1][1]))
