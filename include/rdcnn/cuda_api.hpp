@@ -28,8 +28,13 @@
 // CPU backends are not re-implemented: selecting one throws
 // std::invalid_argument (there is no silent fallback).  The CUDA kernels are
 // FitzHugh-Nagumo in fp32 (strict or fast) and fp64 (strict); other
-// CellModels throw.
+// CellModels run on a generic device stencil from nvcc-compiled callers
+// (rdcnn/cuda_model.cuh) and throw from host-compiled ones.
 #pragma once
+
+#if defined(__CUDACC__)
+#include "rdcnn/cuda_model.cuh"
+#endif
 
 #include <algorithm>
 #include <array>
@@ -528,8 +533,12 @@ bool step(StepBuffers<T>& bufs, const Gene& gene, const Backend& backend) {
   return detail::advance_host(bufs, gene, backend, 1) == 0;
 }
 
-/// The CellModel overload: the FHN model runs on the device; any other model
-/// is rejected (the sm_100a kernel is specialised to FHN).
+/// The CellModel overload (kernels.hpp:233-259, generic over CellModel,
+/// model.hpp:13-21).  The FHN model runs on the sm_100a wavefront kernels.
+/// Any other model runs on the generic device stencil of
+/// rdcnn/cuda_model.cuh when the caller is compiled with nvcc (model methods
+/// marked __host__ __device__); a host-compiled caller cannot ship its model
+/// to the GPU and gets std::invalid_argument.
 template <class M, class T = typename M::value_type>
   requires CellModel<M>
 bool step(StepBuffers<T>& bufs, const M& model, const Backend& backend) {
@@ -539,7 +548,19 @@ bool step(StepBuffers<T>& bufs, const M& model, const Backend& backend) {
     g.dt = p.dt; g.a = p.a; g.b = p.b; g.eps = p.eps; g.c = p.c; g.Du = p.du; g.Dv = p.dv;
     return step(bufs, g, backend);  // float -> double -> float is exact
   } else {
-    throw std::invalid_argument("the cuda backend implements the FitzHugh-Nagumo model only");
+#if defined(__CUDACC__)
+    detail::require_cuda(backend);
+    const bool ok = cuda_model::step_device<M, T>(bufs.front.u.data(), bufs.front.v.data(), bufs.back.u.data(),
+                                                  bufs.back.v.data(), bufs.rows(), bufs.cols(), model);
+    bufs.swap();
+    return ok;
+#else
+    (void)bufs;
+    (void)model;
+    (void)backend;
+    throw std::invalid_argument(
+        "the cuda backend runs non-FHN CellModels only from nvcc-compiled code (rdcnn/cuda_model.cuh)");
+#endif
   }
 }
 
