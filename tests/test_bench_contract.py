@@ -1,0 +1,49 @@
+"""bench.py keeps the driver's JSON contract (one line; metric/value/unit/
+n_gpus/steps/warmup/ms_per_step/higher_is_better/scaling/vs_baseline/dtype/
+data/config, plus roofline, cpu_baseline, e2e, gpu_launches, clocks)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+             "scaling", "vs_baseline", "dtype", "data", "config"}
+
+
+def run_bench(*args, timeout=600):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                       timeout=timeout, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_contract():
+    """The reference arm (the reference's own parallel backend on the host)."""
+    d = run_bench("--impl", "reference", "--size", "64", "--steps", "2", "--warmup", "1")
+    assert BASE_KEYS <= set(d)
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "Mcell-updates/s"
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+@pytest.mark.gpu
+def test_our_arm_contract():
+    d = run_bench("--size", "512", "--steps", "3", "--warmup", "3", "--iters-per-step", "40",
+                  "--no-cpu-baseline", "--e2e-steps", "1")
+    assert BASE_KEYS <= set(d) and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["roofline"]["bound"] in ("hbm", "tensor") and d["roofline"]["peak"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 2 * 4 * 512 * 512 and d["e2e"]["value"] > 0
+    assert d["gpu_launches"] > 0 and "sm_mhz" in d["clocks"]
+    assert d["config"]["workload"].startswith("cfg2")
+
+
+@pytest.mark.gpu
+def test_our_arm_slab_contract():
+    d = run_bench("--slab", "--size", "512", "--steps", "2", "--warmup", "3", "--iters-per-step", "40",
+                  "--no-cpu-baseline", "--e2e-steps", "1")
+    assert d["config"]["transport"] == "p2p" and d["value"] > 0
