@@ -16,12 +16,10 @@ import argparse
 import datetime
 import json
 import os
-import statistics
 import sys
 import time
 from typing import List, Optional, Tuple
 
-import numpy as np
 
 from . import engine
 from .engine import BlowUpError, Gene, GridState, RunConfig, Simulator, checksum, checksum_hex, validate_config

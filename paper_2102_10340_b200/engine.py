@@ -29,12 +29,12 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 import time
-from typing import Callable, List, Optional, Sequence
+from typing import Callable, List, Optional
 
 import numpy as np
 
 from . import _lib
-from ._lib import RDCNN_EBLOWUP, RDCNN_FAST, RDCNN_STRICT, ParamsF32, ParamsF64, check, load
+from ._lib import RDCNN_FAST, RDCNN_STRICT, ParamsF32, ParamsF64, check, load
 
 DTYPES = {"single": np.float32, "double": np.float64}
 

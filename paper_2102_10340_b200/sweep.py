@@ -19,8 +19,8 @@ from typing import List, Optional, Tuple
 
 import numpy as np
 
-from .engine import (DTYPES, BlowUpError, Gene, GridState, RunConfig, ScheduleError, Simulator, checksum,
-                     gene_valid, init_center_square, init_from_image, init_full_random, validate_config)
+from .engine import (DTYPES, Gene, RunConfig, ScheduleError, Simulator, gene_valid, init_center_square,
+                     init_from_image, init_full_random, validate_config)
 
 REGIMES = ("Homogeneous", "Patterned", "Growing", "BlowUp")
 GENE_FIELDS = {"a": "a", "b": "b", "eps": "eps", "c": "c", "du": "Du", "dv": "Dv", "dt": "dt", "ka": "ka"}

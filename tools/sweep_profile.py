@@ -7,7 +7,6 @@ import time
 import numpy as np
 
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
-import paper_2102_10340_b200 as fhn  # noqa: E402
 from paper_2102_10340_b200 import sweep as sw  # noqa: E402
 from paper_2102_10340_b200.engine import RunConfig, Simulator  # noqa: E402
 
@@ -27,7 +26,8 @@ for name in ("advance", "frame_capture", "frame_stats", "frame_active", "downloa
              "frames_reserve", "frame_download"):
     setattr(Simulator, name, timed(name, getattr(Simulator, name)))
 sw.classify = timed("classify", sw.classify)
-sw.checksum = timed("checksum", sw.checksum)
+for name in ("checksums",):
+    setattr(Simulator, name, timed(name, getattr(Simulator, name)))
 
 side = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 cfg = RunConfig()
