@@ -835,7 +835,8 @@ bool cluster_plan_for(rdcnn_sim* s, ClusterPlan* out) {
   return false;
 }
 
-int cluster_advance(rdcnn_sim* s, const ClusterPlan& pl, long steps, long* first_bad) {
+int cluster_advance(rdcnn_sim* s, const ClusterPlan& pl, long steps, long* first_bad, bool* fell_back) {
+  *fell_back = false;
   if (!s->d_first_bad) RDCNN_CUDA_TRY(cudaMalloc(&s->d_first_bad, sizeof(long long)));
   rdcnn_dev::ClusterArgs a{};
   a.u_in = s->u_ptr<float>(s->cur);
@@ -863,7 +864,20 @@ int cluster_advance(rdcnn_sim* s, const ClusterPlan& pl, long steps, long* first
   ClusterFn fn = cluster_fn(pl.W, pl.RW, s->mode == RDCNN_FAST);
   RDCNN_CUDA_TRY(cudaMemsetAsync(s->d_first_bad, 0xFF, sizeof(long long), s->stream));
   RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
-  RDCNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, a));
+  {
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
+    if (e != cudaSuccess) {
+      // The 16-CTA cluster could not be placed right now (e.g. SMs held by
+      // another context).  In automatic mode the wavefront path takes over;
+      // the state is untouched (the launch did not happen).
+      cudaGetLastError();
+      if (s->cluster_mode == 0) {
+        *fell_back = true;
+        return RDCNN_OK;
+      }
+      return fail(RDCNN_ECUDA, "cluster launch failed: %s", cudaGetErrorString(e));
+    }
+  }
   RDCNN_CUDA_TRY(cudaEventRecord(s->ev1, s->stream));
   long long fb = 0;
   RDCNN_CUDA_TRY(cudaMemcpyAsync(&fb, s->d_first_bad, sizeof fb, cudaMemcpyDeviceToHost, s->stream));
@@ -1003,7 +1017,11 @@ int advance_impl(rdcnn_sim* s, long steps, long* first_bad) {
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   if constexpr (sizeof(T) == 4) {
     ClusterPlan pl;
-    if (steps > 0 && cluster_plan_for(s, &pl)) return cluster_advance(s, pl, steps, first_bad);
+    if (steps > 0 && cluster_plan_for(s, &pl)) {
+      bool fell_back = false;
+      const int rc = cluster_advance(s, pl, steps, first_bad, &fell_back);
+      if (!fell_back) return rc;
+    }
     if (s->cluster_mode > 0) return fail(RDCNN_EINVAL, "persistent cluster path required but %dx%d (batch %d) does not fit it",
                                          s->rows, s->cols, s->batch);
   }
