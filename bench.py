@@ -124,7 +124,8 @@ class ClockSampler:
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+              "enforced.power.limit")
 
     def __init__(self, device: int):
         self.device = device
@@ -154,7 +155,7 @@ class ClockSampler:
     def summary(self):
         if not self.path or not os.path.exists(self.path):
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, lim, reasons = [], [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         with open(self.path) as f:
             for line in f:
@@ -166,13 +167,20 @@ class ClockSampler:
                     mx.append(float(p[2]))
                 except ValueError:
                     continue
+                try:
+                    pw.append(float(p[3]))
+                    lim.append(float(p[9]))
+                except (ValueError, IndexError):
+                    pass
                 for name, val in zip(names, p[5:9]):
                     if val.lower() == "active":
                         reasons.add(name)
         os.unlink(self.path)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm),
+                "power_w": round(statistics.median(pw), 1) if pw else None,
+                "power_limit_w": max(lim) if lim else None}
 
 
 def ncu_traffic():
