@@ -323,7 +323,8 @@ def cmd_sweep(a) -> int:
         os.makedirs(out_dir, exist_ok=True)
         with open(os.path.join(out_dir, "manifest.txt"), "w") as f:
             f.write(manifest_text(g, cfg))
-        res = sweep_grid(spec, image=image, device=a.device, levels=a.levels)
+        devices = [int(d) for d in a.devices.split(",")] if a.devices else None
+        res = sweep_grid(spec, image=image, device=a.device, levels=a.levels, devices=devices)
         with open(os.path.join(out_dir, "labels.csv"), "w") as f:
             f.write(res.labels_csv)
         from .imageio import normalize_frame
@@ -372,6 +373,7 @@ def main(argv: Optional[List[str]] = None) -> int:
     add_sim_flags(w)
     w.add_argument("--range", default="")
     w.add_argument("--per-cell-seed", action="store_true")
+    w.add_argument("--devices", default="", help="comma-separated GPUs to split the cells over")
     w.add_argument("--parallel-cells", action="store_true")
     cc = ClassifierConfig()
     w.add_argument("--homogeneity-rel", type=float, default=cc.homogeneity_rel)

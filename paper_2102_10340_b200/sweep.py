@@ -180,32 +180,13 @@ def labels_csv(res: SweepResult) -> str:
     return "".join(out)
 
 
-def sweep_grid(spec: SweepSpec, image: Optional[np.ndarray] = None, device: int = 0,
-               levels: int = 4) -> SweepResult:
-    """sweep_grid (sweep.hpp:255-326) as one batched device run."""
-    validate_sweep_spec(spec)
-    base = dataclasses.replace(spec.base_config)
-    issues = validate_config(base, spec.base_gene)
-    if base.init_mode == 3 and image is not None:
-        issues = [i for i in issues if not i.startswith("MissingImage")]
-    if issues:
-        raise ValueError(issues[0].split(": ", 1)[-1])
-    if base.iter_max % base.nssp != 0:
-        raise ScheduleError("nssp must divide iter_max for sweep cells")
-    if base.init_mode == 3:
-        if image is None:
-            raise ValueError("typ=3 requires an image")
-        base.nn, base.nm = int(image.shape[0]), int(image.shape[1])
-    cells: List[SweepCell] = []
-    for y in spec.y_values:
-        for x in spec.x_values:
-            g = _set(_set(spec.base_gene, spec.x_param, x), spec.y_param, y)
-            if not gene_valid(g):
-                raise ValueError(f"sweep cell gene invalid at {spec.x_param}={format_double(x)} "
-                                 f"{spec.y_param}={format_double(y)}")
-            cells.append(SweepCell(x_value=float(x), y_value=float(y), gene=g))
-
+def _run_cells(cells: List[SweepCell], idx0: int, spec: SweepSpec, base: RunConfig,
+               image: Optional[np.ndarray], device: int, levels: int) -> None:
+    """Runs `cells` (global indices idx0..) as one batched handle on `device`
+    and fills in their outcomes (sweep.hpp:296-326)."""
     B, rows, cols = len(cells), base.nn, base.nm
+    if B == 0:
+        return
     prec = base.precision
     sim = Simulator(rows, cols, batch=B, device=device, levels=levels, precision=prec)
     sim.set_params([c.gene for c in cells])
@@ -219,7 +200,7 @@ def sweep_grid(spec: SweepSpec, image: Optional[np.ndarray] = None, device: int 
         U = np.empty((B, rows * cols), DTYPES[prec])
         V = np.empty_like(U)
         for idx, c in enumerate(cells):
-            seed = base.seed + idx if spec.per_cell_seed else base.seed
+            seed = base.seed + idx0 + idx if spec.per_cell_seed else base.seed
             if base.init_mode == 1:
                 s = init_center_square(rows, cols, seed, prec)
             elif base.init_mode == 2:
@@ -266,6 +247,47 @@ def sweep_grid(spec: SweepSpec, image: Optional[np.ndarray] = None, device: int 
         if frames_u is not None:
             c.buffer = [fr[idx].copy() for fr in frames_u]
     sim.close()
+
+
+def sweep_grid(spec: SweepSpec, image: Optional[np.ndarray] = None, device: int = 0,
+               levels: int = 4, devices: Optional[List[int]] = None) -> SweepResult:
+    """sweep_grid (sweep.hpp:255-326) as one batched device run, or with
+    `devices`, the cells split in contiguous chunks over several GPUs."""
+    validate_sweep_spec(spec)
+    base = dataclasses.replace(spec.base_config)
+    issues = validate_config(base, spec.base_gene)
+    if base.init_mode == 3 and image is not None:
+        issues = [i for i in issues if not i.startswith("MissingImage")]
+    if issues:
+        raise ValueError(issues[0].split(": ", 1)[-1])
+    if base.iter_max % base.nssp != 0:
+        raise ScheduleError("nssp must divide iter_max for sweep cells")
+    if base.init_mode == 3:
+        if image is None:
+            raise ValueError("typ=3 requires an image")
+        base.nn, base.nm = int(image.shape[0]), int(image.shape[1])
+    cells: List[SweepCell] = []
+    for y in spec.y_values:
+        for x in spec.x_values:
+            g = _set(_set(spec.base_gene, spec.x_param, x), spec.y_param, y)
+            if not gene_valid(g):
+                raise ValueError(f"sweep cell gene invalid at {spec.x_param}={format_double(x)} "
+                                 f"{spec.y_param}={format_double(y)}")
+            cells.append(SweepCell(x_value=float(x), y_value=float(y), gene=g))
+
+    devs = list(devices) if devices else [device]
+    bounds = np.linspace(0, len(cells), len(devs) + 1).astype(int)
+    jobs = [(cells[lo:hi], int(lo), dev) for lo, hi, dev in zip(bounds[:-1], bounds[1:], devs) if hi > lo]
+    if len(jobs) == 1:
+        _run_cells(jobs[0][0], jobs[0][1], spec, base, image, jobs[0][2], levels)
+    elif jobs:
+        # Replicas only (SURVEY §8e): independent cells, no exchange; the C-ABI
+        # calls release the GIL, so the devices advance concurrently.
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(len(jobs)) as ex:
+            list(ex.map(lambda j: _run_cells(j[0], j[1], spec, base, image, j[2], levels), jobs))
+    rows, cols = base.nn, base.nm
     res = SweepResult(list(spec.x_values), list(spec.y_values), spec.x_param, spec.y_param, rows, cols, cells)
     res.labels_csv = labels_csv(res)
     return res

@@ -107,3 +107,24 @@ def test_frame_stats_and_normalisation(oracle):
         u, _ = sim.download()
         a = sim.frame_normalize(-1, 0, float(u.min()), float(u.max()))
         assert a.shape == (rows, cols)
+
+
+@pytest.mark.parametrize("per_cell_seed", (False, True))
+def test_sweep_split_over_devices_identical(per_cell_seed):
+    """cfg4 as 'replicas only': the cells split over several
+    handles/devices (here three handles on GPU 0, advanced concurrently from
+    threads) give the same labels CSV, digests and blow-ups as one batch."""
+    from paper_2102_10340_b200.engine import RunConfig
+    from paper_2102_10340_b200.sweep import SweepSpec, sweep_grid
+
+    cfg = RunConfig()
+    cfg.nn = cfg.nm = 64
+    cfg.iter_max, cfg.nssp, cfg.init_mode = 400, 4, 2
+    spec = SweepSpec("du", list(np.linspace(0.02, 0.9, 7)), "dt", [0.1, 0.5, 40.0], base_config=cfg,
+                     per_cell_seed=per_cell_seed)
+    one = sweep_grid(spec)
+    split = sweep_grid(spec, devices=[0, 0, 0])
+    assert split.labels_csv == one.labels_csv
+    assert [c.digest for c in split.cells] == [c.digest for c in one.cells]
+    assert [c.blowup_iteration for c in split.cells] == [c.blowup_iteration for c in one.cells]
+    assert any(c.blew_up for c in one.cells)
