@@ -109,6 +109,7 @@ def test_frame_stats_and_normalisation(oracle):
         assert a.shape == (rows, cols)
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("per_cell_seed", (False, True))
 def test_sweep_split_over_devices_identical(per_cell_seed):
     """cfg4 as 'replicas only': the cells split over several
