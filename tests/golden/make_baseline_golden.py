@@ -2,9 +2,10 @@
 ITSELF (oracle/_ref: the reference headers compiled read-only, run through
 their public API on this container's CPU cores).  Writes
 tests/golden/baseline_golden.json; tests/test_baseline_gpu.py reproduces every
-entry on the B200 bit for bit.  Takes ~20 minutes on 8 cores:
+entry on the B200 bit for bit.  On 8 cores:
 
-    python tests/golden/make_baseline_golden.py
+    python tests/golden/make_baseline_golden.py            # everything (~45 min)
+    python tests/golden/make_baseline_golden.py cfg2_f64   # adds the fp64 entry (~1 min)
 
 cfg1  256^2 typ=1 seed 42, default gene, 1000 iterations            (also a KAT)
 cfg2  4096^2 typ=1 seed 42, slow-growth gene a=-0.05, 100 000 iterations,
@@ -111,5 +112,25 @@ def main():
     print("done", out["seconds"], "s")
 
 
+def add_cfg2_f64():
+    """fp64 (the reference's double instantiation) on the cfg2 lattice: the
+    first 1000 iterations, merged into the existing JSON (~1 minute)."""
+    ref = Reference()
+    path = os.path.join(ROOT, "tests", "golden", "baseline_golden.json")
+    with open(path) as f:
+        out = json.load(f)
+    n = 4096
+    u, v = ref.init_f64(1, n, n, 42)
+    u, v, bad, _ = ref.run_timed_f64(n, n, u, v, 1000, SLOW_GROWTH, backend="parallel")
+    out["cfg2_f64"] = {"rows": n, "cols": n, "typ": 1, "seed": 42, "gene7": SLOW_GROWTH, "iters": 1000,
+                       "checksum": f"{ref.checksum(n, n, u, v):016x}", "bad_iter": bad}
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print("cfg2_f64", out["cfg2_f64"]["checksum"])
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["cfg2_f64"]:
+        add_cfg2_f64()
+    else:
+        main()

@@ -135,3 +135,15 @@ def test_cfg5_32768_x100_slab_peer_ring(gold):
     finally:
         s.close()
     _cfg5_check(c, u, v)
+
+
+def test_cfg2_f64_4096_x1000(gold):
+    """The reference's double instantiation on the cfg2 lattice (fp64 strict)."""
+    if "cfg2_f64" not in gold:
+        pytest.skip("fp64 entry not generated")
+    c = gold["cfg2_f64"]
+    with fhn.Simulator(c["rows"], c["cols"], precision="double") as sim:
+        sim.set_params(gene(c["gene7"]))
+        sim.init(1, 42)
+        assert int(sim.advance(c["iters"])[0]) == c["bad_iter"]
+        assert digest(sim, c["rows"], c["cols"]) == c["checksum"]
