@@ -47,9 +47,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", default="cfg2", choices=("cfg2", "cfg5"),
+    ap.add_argument("--workload", default="cfg2", choices=("cfg2", "cfg5", "cfg1", "cfg3"),
                     help="cfg2 (default): a size x size torus per GPU, weak scaling; cfg5: ONE "
-                         "size x size torus (default 32768) split over the N GPUs, strong scaling")
+                         "size x size torus (default 32768) split over the N GPUs, strong scaling; "
+                         "cfg1 (256^2 x 1000) / cfg3 (8192^2 image x 200): one lattice per GPU, "
+                         "independent replicas")
     ap.add_argument("--size", type=int, default=None,
                     help="cfg2: rows = cols per GPU (default 4096); cfg5: the lattice edge (32768)")
     ap.add_argument("--iters-per-step", type=int, default=None,
@@ -84,7 +86,18 @@ class Workload:
 
     def __init__(self, args, world: int):
         self.name = args.workload
-        if self.name == "cfg5":
+        self.replicas = self.name in ("cfg1", "cfg3")
+        if self.replicas:
+            n = args.size or (256 if self.name == "cfg1" else 8192)
+            self.cols = self.rows_rank = self.rows_global = n
+            self.typ, self.gene7 = (1 if self.name == "cfg1" else 3), DEFAULT_GENE7
+            self.iters = args.iters_per_step or (1000 if self.name == "cfg1" else 200)
+            self.scaling = "weak"
+            self.desc = (f"{self.name}: FHN RD-CNN {n}x{n} fp32 torus per GPU, "
+                         + ("typ=1 seed 42" if self.typ == 1 else "typ=3 synthetic 8-bit image (SURVEY §8d)")
+                         + f", reference default gene, {self.iters} iterations per step"
+                         + ("; independent replicas, one per GPU" if world > 1 else ""))
+        elif self.name == "cfg5":
             self.cols = args.size or 32768
             self.rows_global = self.cols
             if self.rows_global % world:
@@ -109,6 +122,29 @@ class Workload:
     def gene(self, fhn):
         g = self.gene7
         return fhn.Gene(dt=g[0], a=g[1], b=g[2], eps=g[3], c=g[4], Du=g[5], Dv=g[6])
+
+    def pixels(self):
+        """cfg3 image: SURVEY §8d pattern (checker blocks 37x53 + a sine ramp), 8-bit."""
+        import numpy as np
+        n = self.cols
+        i = np.arange(n)[:, None]
+        j = np.arange(n)[None, :]
+        x = np.where(((i // 37) + (j // 53)) % 2 == 1, 0.8, 0.2) + 0.1 * np.sin(0.05 * i)
+        return np.clip(np.round(x * 255), 0, 255).astype(np.uint8)
+
+    def ref_state(self, ref):
+        """The initial state through the reference's own initialisers."""
+        if self.typ != 3:
+            return ref.init(self.typ, self.rows_global, self.cols, 42)
+        from paper_2102_10340_b200 import imageio
+        fd, path = tempfile.mkstemp(suffix=".pgm")
+        os.close(fd)
+        try:
+            imageio.write_pgm(path, self.pixels())
+            _, _, u, v = ref.init_image(path, 1.0)
+        finally:
+            os.unlink(path)
+        return u, v
 
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -200,7 +236,7 @@ def cpu_baseline_sample(wl: "Workload", budget_s: float):
     ref = Reference()
     threads = ref.max_threads()
     R, C = wl.rows_global, wl.cols
-    u, v = ref.init(wl.typ, R, C, 42)
+    u, v = wl.ref_state(ref)
     # calibrate with 2 iterations, then size the sample to the budget
     u, v, _, sec = ref.run_timed(R, C, u, v, 2, wl.gene7, backend="parallel")
     per_iter = max(sec / 2, 1e-6)
@@ -237,7 +273,7 @@ def bench_reference(args, rank, world):
     ref = Reference()
     R, C = wl.rows_global, wl.cols  # the same global lattice our arm advances
     threads = ref.max_threads()
-    u, v = ref.init(wl.typ, R, C, 42)
+    u, v = wl.ref_state(ref)
     # size each step to ~2 s of CPU work so the whole run stays within minutes
     u, v, _, sec = ref.run_timed(R, C, u, v, 2, wl.gene7, backend="parallel")
     iters = int(max(1, min(wl.iters, 2.0 / max(sec / 2, 1e-6))))
@@ -296,15 +332,20 @@ def bench_ours(args, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     launches = 0
-    if world == 1 and not args.slab:
+    if (world == 1 and not args.slab) or wl.replicas:
         sim = fhn.Simulator(wl.rows_global, n, device=local_rank, mode=args.mode, levels=args.levels,
                             seg_rows=args.seg_rows)
         sim.set_params(gene)
-        sim.init(wl.typ, 42)
+        if wl.typ == 3:
+            sim.init_image(wl.pixels(), 1.0)
+        else:
+            sim.init(wl.typ, 42)
         stream = torch.cuda.ExternalStream(sim.stream(), device=local_rank)
         for _ in range(args.warmup):
             sim.advance(S)
         torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
         with ClockSampler(local_rank) as clocks:
             ev0 = torch.cuda.Event(enable_timing=True)
             ev1 = torch.cuda.Event(enable_timing=True)
@@ -316,8 +357,12 @@ def bench_ours(args, rank, world, local_rank):
                     raise RuntimeError(f"blow-up at iteration {bad[0]}")
             ev1.record(stream)
             torch.cuda.synchronize()
-        t_ms = ev0.elapsed_time(ev1)
-        cells_global = wl.rows_global * n
+        t = torch.tensor([ev0.elapsed_time(ev1)], device=red_dev)
+        if dist is not None:  # replicas: the job takes as long as its slowest GPU
+            dist.barrier()
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+        cells_global = wl.rows_global * n * (world if wl.replicas else 1)
     else:
         from paper_2102_10340_b200.slab import SlabStepper
         rows_global = wl.rows_global
@@ -361,7 +406,8 @@ def bench_ours(args, rank, world, local_rank):
     # ---- roofline of the dominant kernel (the K-level wavefront stencil) ----
     peaks, peak_kind = measured_peaks()
     per_rank_cells = wl.rows_rank * n
-    transport = slab.transport if (world > 1 or args.slab) else None
+    use_slab = (world > 1 or args.slab) and not wl.replicas
+    transport = slab.transport if use_slab else None
     levels = args.levels
     # One K-level block = one launch on the per-launch path; the persistent
     # wavefront kernel runs every block of an advance in one launch, so the
@@ -391,24 +437,29 @@ def bench_ours(args, rank, world, local_rank):
 
     # ---- end to end through the public API with host buffers (N=1 only) ----
     e2e = None
-    if world == 1 and not args.slab:
+    if not use_slab:
         cells = wl.rows_global * n
         u_h = torch.empty(cells, dtype=torch.float32).pin_memory()
         v_h = torch.empty(cells, dtype=torch.float32).pin_memory()
         sim.download_ptr(u_h.data_ptr(), v_h.data_ptr())
         torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             sim.upload_ptr(u_h.data_ptr(), v_h.data_ptr())
             bad = sim.advance(S)
-            launches_e2e = sim.launch_count()
             sim.download_ptr(u_h.data_ptr(), v_h.data_ptr())
         torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
-        e2e = {"value": round(cells * S * args.e2e_steps / e2e_s / 1e6, 2),
-               "unit": "Mcell-updates/s", "h2d_bytes_per_step": 2 * 4 * cells,
-               "d2h_bytes_per_step": 2 * 4 * cells,
-               "path": "rdcnn_sim_upload (pinned host) -> rdcnn_sim_advance -> rdcnn_sim_download",
+        te = torch.tensor([time.perf_counter() - t0], device=red_dev)
+        if dist is not None:  # replicas: max wall time over ranks
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        e2e = {"value": round(cells * world * S * args.e2e_steps / e2e_s / 1e6, 2),
+               "unit": "Mcell-updates/s", "h2d_bytes_per_step": 2 * 4 * cells * world,
+               "d2h_bytes_per_step": 2 * 4 * cells * world,
+               "path": "rdcnn_sim_upload (pinned host) -> rdcnn_sim_advance -> rdcnn_sim_download"
+                       + ("; per rank, max wall time over ranks" if world > 1 else ""),
                "steps": args.e2e_steps}
         # sanity: state stays finite
         un = u_h.numpy()
@@ -464,14 +515,14 @@ def bench_ours(args, rank, world, local_rank):
                                 f"GPU), halo exchange: "
                                 + ("fused peer stores in the step kernel" if transport == "p2p"
                                    else "NCCL send/recv overlapped with the interior kernel")
-                                if world > 1 or args.slab else "")),
+                                if use_slab else "")),
                 "rows": wl.rows_global, "cols": n, "iterations_per_step": S, "levels_per_launch": levels,
                 "mode": args.mode,
                 "l2": (f"double-buffered state {2 * 8 * per_rank_cells / 2**20:.0f} MiB/GPU "
                        + ("> 126 MB L2 (no flush needed)" if 2 * 8 * per_rank_cells > 126e6
                           else "fits in L2: small-size run, not a reported number")),
-                "parallelism": f"slab{world}" if world > 1 or args.slab else "single",
-                **({"transport": transport} if world > 1 or args.slab else {}),
+                "parallelism": (f"slab{world}" if use_slab else f"replicas{world}" if world > 1 else "single"),
+                **({"transport": transport} if use_slab else {}),
             },
             "roofline": roofline,
             "cpu_baseline": cpu,
