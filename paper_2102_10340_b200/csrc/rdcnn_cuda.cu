@@ -13,7 +13,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -909,6 +912,12 @@ int cluster_advance(rdcnn_sim* s, const ClusterPlan& pl, long steps, long* first
 // the arithmetic, so the first long advance times a few candidate heights on
 // its OWN first blocks (3 blocks each, CUDA events) and keeps the fastest
 // per level count; no extra work is done.  An explicit seg_rows disables it.
+// The result is kept process-wide per launch shape, so later handles of the
+// same shape (bench reps, sweep chunks, per-call step handles) reuse it.
+using TuneKey = std::tuple<int, int, int, int, int, int, int, int>;  // device, rows, cols, batch, elem, mode, per-grid, K
+std::mutex g_tune_mu;
+std::map<TuneKey, int> g_tune_cache;
+
 template <class T>
 int autotune_segments(rdcnn_sim* s, const Schedule& sched, long* n_io) {
   const int k = sched.kmax;
@@ -925,6 +934,16 @@ int autotune_segments(rdcnn_sim* s, const Schedule& sched, long* n_io) {
   if (4 * p0.warps >= 3LL * rw * s->sm_count) {  // fills the chip: the plan is right
     s->tuned[ki] = true;
     return RDCNN_OK;
+  }
+  const TuneKey key{s->device, s->rows, s->cols, s->batch, s->elem, s->mode, int(per_grid), k};
+  {
+    std::lock_guard<std::mutex> lock(g_tune_mu);
+    const auto it = g_tune_cache.find(key);
+    if (it != g_tune_cache.end()) {
+      s->tuned_seg[ki] = it->second;
+      s->tuned[ki] = true;
+      return RDCNN_OK;
+    }
   }
   static const int kCand[] = {0, 3, 4, 5, 6, 8, 10, 12, 16, 24};
   constexpr int kReps = 3;
@@ -968,6 +987,10 @@ int autotune_segments(rdcnn_sim* s, const Schedule& sched, long* n_io) {
   for (auto& e : ev) cudaEventDestroy(e);
   s->tuned_seg[ki] = best_h;
   s->tuned[ki] = true;
+  {
+    std::lock_guard<std::mutex> lock(g_tune_mu);
+    g_tune_cache.emplace(key, best_h);
+  }
   *n_io = n;
   return RDCNN_OK;
 }

@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "rdcnn/bench.hpp"
 #include "rdcnn/engine.hpp"
 #include "rdcnn/init.hpp"
 
@@ -292,9 +293,131 @@ void double_precision() {
   CHECK(it == 6);  // golden f64_blowup_16_dt100
 }
 
+// test_bench.cpp "emit_csv freezes ...", "emit_table shapes ...", "emitters
+// reject empty input", "emit_json mirrors the CSV fields" (host only).
+void bench_emitters() {
+  BenchRecord r;
+  r.backend = "parallel";
+  r.hardware = "cpu";
+  r.n = 512;
+  r.iters = 10000;
+  r.seconds = 8.0;
+  const Throughput tp = throughput(512, 512, 10000, 8.0);
+  r.mcells_per_s = tp.mcells_per_s;
+  r.ns_per_cell_iter = tp.ns_per_cell_iter;
+  r.checksum = 0x0123456789abcdefull;
+  CHECK(emit_csv({r}) ==
+        "backend,hardware,n,iters,seconds,mcells_per_s,ns_per_cell_iter,checksum\n"
+        "parallel,cpu,512,10000,8,327.68,3.0518,0123456789abcdef\n");
+  BenchRecord skipped = r;
+  skipped.skipped = true;
+  CHECK(emit_csv({skipped, r}) == emit_csv({r}));
+
+  BenchRecord a;
+  a.backend = "reference";
+  a.hardware = "cpu";
+  a.n = 128;
+  a.iters = 100;
+  a.seconds = 1.0;
+  a.mcells_per_s = 1.6384;
+  a.ns_per_cell_iter = 610.35;
+  BenchRecord b = a;
+  b.n = 256;
+  b.skipped = true;
+  BenchRecord c = a;
+  c.backend = "cuda";
+  const std::string table = emit_table({a, b, c});
+  CHECK(table ==
+        "backend    N=128       N=256\n"
+        "reference  1.6384 (1)  -\n"
+        "cuda       1.6384 (1)  -\n");
+  BenchRecord d = a;
+  d.hardware = "b200";
+  const std::string t2 = emit_table({a, d});
+  CHECK(t2.find("hardware") != std::string::npos && t2.find("b200") != std::string::npos);
+
+  bool csv_empty = false, table_empty = false, json_empty = false;
+  try { emit_csv({}); } catch (const std::invalid_argument&) { csv_empty = true; }
+  try { emit_table({}); } catch (const std::invalid_argument&) { table_empty = true; }
+  try { emit_json({}); } catch (const std::invalid_argument&) { json_empty = true; }
+  CHECK(csv_empty && table_empty && json_empty);
+
+  BenchRecord j;
+  j.backend = "blocked";
+  j.hardware = "cpu";
+  j.n = 128;
+  j.iters = 1000;
+  j.seconds = 0.5;
+  j.mcells_per_s = 32.768;
+  j.ns_per_cell_iter = 30.518;
+  j.checksum = 0xffull;
+  BenchRecord js = j;
+  js.n = 4096;
+  js.skipped = true;
+  // The reference's JSON library output: sorted keys, two-space indent.
+  CHECK(emit_json({j, js}) ==
+        "[\n  {\n    \"backend\": \"blocked\",\n    \"checksum\": \"00000000000000ff\",\n"
+        "    \"hardware\": \"cpu\",\n    \"iters\": 1000,\n    \"mcells_per_s\": 32.768,\n    \"n\": 128,\n"
+        "    \"ns_per_cell_iter\": 30.518,\n    \"seconds\": 0.5\n  },\n  {\n    \"backend\": \"blocked\",\n"
+        "    \"hardware\": \"cpu\",\n    \"iters\": 1000,\n    \"n\": 4096,\n    \"skipped\": true\n  }\n]\n");
+  using detail_bench::json_number;
+  CHECK(json_number(8.0) == "8.0" && json_number(327.68) == "327.68" && json_number(-0.25) == "-0.25");
+  CHECK(json_number(1e15) == "1e+15" && json_number(123456789012345.0) == "123456789012345.0");
+  CHECK(json_number(1.5e-5) == "1.5e-05" && json_number(0.0001) == "0.0001" && json_number(0.1) == "0.1");
+  CHECK(json_number(0.0) == "0.0" && json_number(1.0 / 3.0) == "0.3333333333333333");
+}
+
+// test_bench.cpp "bench_suite measures every cell ...", "... propagates
+// blow-up with the offending cell named", "... validates its inputs" on the
+// cuda backend; checksums from the reference (oracle/_ref, parallel backend).
+void bench_suite_cuda() {
+  const auto recs = bench_suite({kCuda}, {16, 24}, 50, Gene{}, 42, Precision::Single, 1, "b200");
+  CHECK(recs.size() == 2);
+  for (const BenchRecord& r : recs) {
+    CHECK(!r.skipped && r.seconds > 0 && r.backend == "cuda" && r.hardware == "b200" && r.iters == 50);
+    const double cells = double(r.n) * r.n * double(r.iters);
+    CHECK(std::abs(r.mcells_per_s / (cells / (r.seconds * 1e6)) - 1) < 1e-3);
+    CHECK(std::abs(r.ns_per_cell_iter * r.mcells_per_s / 1000.0 - 1) < 1e-3);
+  }
+  if (recs.size() == 2) {
+    CHECK(checksum_hex(recs[0].checksum) == "e2abf7e7daef46ef");
+    CHECK(checksum_hex(recs[1].checksum) == "913f5a3a6c8bc5b3");
+  }
+  const auto d = bench_suite({kCuda}, {16}, 50, Gene{}, 42, Precision::Double, 3);
+  CHECK(d.size() == 1 && checksum_hex(d[0].checksum) == "38c10a624dba5a04");
+
+  Gene g;
+  g.dt = 100;
+  bool named = false;
+  try {
+    bench_suite({kCuda}, {16}, 100, g, 1, Precision::Single, 1);
+  } catch (const BenchCellError& e) {
+    named = e.backend == "cuda" && e.n == 16 && e.iteration == 4;
+  }
+  CHECK(named);
+
+  int rejected = 0;
+  try { bench_suite({kCuda}, {0}, 10, Gene{}, 1); } catch (const std::invalid_argument&) { ++rejected; }
+  try { bench_suite({kCuda}, {16}, 0, Gene{}, 1); } catch (const std::invalid_argument&) { ++rejected; }
+  try { bench_suite({kCuda}, {16}, 10, Gene{}, 1, Precision::Single, 0); } catch (const std::invalid_argument&) { ++rejected; }
+  CHECK(rejected == 3);
+
+  // "doubling iterations roughly doubles wall time": a lattice that fills
+  // the chip, long enough that launch latency is noise.
+  const auto short_run = bench_suite({kCuda}, {2048}, 2000, Gene{}, 7, Precision::Single, 3);
+  const auto long_run = bench_suite({kCuda}, {2048}, 4000, Gene{}, 7, Precision::Single, 3);
+  const double ratio = long_run[0].seconds / short_run[0].seconds;
+  CHECK(ratio > 1.6 && ratio < 2.4);
+}
+
 }  // namespace
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "--host-only") {
+    bench_emitters();
+    std::printf("cpp api (host only): %d checks passed, %d failed\n", g_pass, g_fail);
+    return g_fail;
+  }
   double_precision();
   gene_and_metric();
   kat_criterion1();
@@ -307,6 +430,8 @@ int main() {
   exact_order_paths_agree();
   shift_equivariance();
   backend_selection();
+  bench_emitters();
+  bench_suite_cuda();
   std::printf("cpp api: %d checks passed, %d failed\n", g_pass, g_fail);
   return g_fail;
 }

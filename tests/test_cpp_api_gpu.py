@@ -37,3 +37,11 @@ def test_model_seam_on_gpu():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+def test_cpp_bench_emitters_host():
+    """CPU: bench.hpp's emit_csv / emit_table / emit_json formats on the drop-in
+    API (test_bench.cpp cases), no device work."""
+    r = subprocess.run([BIN, "--host-only"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 failed" in r.stdout
