@@ -5,12 +5,15 @@
 // Exit code = number of failed checks.
 #include <cmath>
 #include <cstdio>
+#include <fstream>
+#include <sstream>
 #include <string>
 #include <vector>
 
 #include "rdcnn/bench.hpp"
 #include "rdcnn/engine.hpp"
 #include "rdcnn/init.hpp"
+#include "rdcnn/sweep.hpp"
 
 using namespace rdcnn;
 
@@ -410,9 +413,65 @@ void bench_suite_cuda() {
   CHECK(ratio > 1.6 && ratio < 2.4);
 }
 
+// sweep_grid (sweep.hpp:249-326) on a spec file written by
+// tests/test_cpp_api_gpu.py ("key value..." lines); prints labels_csv.  With
+// keep_buffers, every completed cell's device-computed outcome is re-derived
+// on the host by classify_outcome over its snapshot buffer (the reference's
+// own host classifier) and its digest by checksum of the final frame.
+int run_sweep_file(const char* path, bool f64) {
+  std::ifstream in(path);
+  SweepSpec spec;
+  spec.base_config.backend = kCuda;
+  std::string line;
+  while (std::getline(in, line)) {
+    std::istringstream ls(line);
+    std::string key;
+    ls >> key;
+    auto num = [&] { double x; ls >> x; return x; };
+    if (key == "x_param") ls >> spec.x_param;
+    else if (key == "y_param") ls >> spec.y_param;
+    else if (key == "xs") for (double x; ls >> x;) spec.x_values.push_back(x);
+    else if (key == "ys") for (double y; ls >> y;) spec.y_values.push_back(y);
+    else if (key == "typ") spec.base_config.init_mode = parse_init_mode(int(num()));
+    else if (key == "nn") spec.base_config.nn = int(num());
+    else if (key == "nm") spec.base_config.nm = int(num());
+    else if (key == "iter_max") spec.base_config.iter_max = long(num());
+    else if (key == "nssp") spec.base_config.nssp = int(num());
+    else if (key == "seed") spec.base_config.seed = uint64_t(num());
+    else if (key == "per_cell_seed") spec.per_cell_seed = num() != 0;
+    else if (key == "keep_buffers") spec.keep_buffers = num() != 0;
+  }
+  auto check_cells = [&](const auto& res) {
+    int bad = 0, checked = 0;
+    for (const auto& c : res.cells) {
+      if (c.blew_up || !c.buffer) continue;
+      ++checked;
+      const RegimeResult host = classify_outcome(*c.buffer, spec.classifier);
+      GridState<typename std::decay_t<decltype(c.final_u)>::value_type> last(res.rows, res.cols);
+      last.u = c.buffer->frames_u.back();
+      last.v = c.buffer->frames_v.back();
+      if (host.label != c.outcome.label || host.final_range != c.outcome.final_range ||
+          host.activity_counts != c.outcome.activity_counts || checksum(last) != c.digest || last.u != c.final_u)
+        ++bad;
+    }
+    std::fprintf(stderr, "keep_buffers: %d cells re-checked on the host, %d mismatches\n", checked, bad);
+    return bad;
+  };
+  if (f64) {
+    const auto res = sweep_grid<double>(spec);
+    std::fputs(res.labels_csv.c_str(), stdout);
+    return spec.keep_buffers ? check_cells(res) : 0;
+  }
+  const auto res = sweep_grid<float>(spec);
+  std::fputs(res.labels_csv.c_str(), stdout);
+  return spec.keep_buffers ? check_cells(res) : 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
+  if (argc > 2 && (std::string(argv[1]) == "--sweep" || std::string(argv[1]) == "--sweep-f64"))
+    return run_sweep_file(argv[2], std::string(argv[1]) == "--sweep-f64");
   if (argc > 1 && std::string(argv[1]) == "--host-only") {
     bench_emitters();
     std::printf("cpp api (host only): %d checks passed, %d failed\n", g_pass, g_fail);

@@ -45,3 +45,51 @@ def test_cpp_bench_emitters_host():
     r = subprocess.run([BIN, "--host-only"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert " 0 failed" in r.stdout
+
+
+def _write_spec(path, d, keep_buffers=False):
+    with open(path, "w") as f:
+        f.write(f"x_param {d['x_param']}\ny_param {d['y_param']}\n")
+        f.write("xs " + " ".join(repr(float(x)) for x in d["xs"]) + "\n")
+        f.write("ys " + " ".join(repr(float(y)) for y in d["ys"]) + "\n")
+        for k in ("nn", "nm", "iter_max", "nssp"):
+            f.write(f"{k} {d[k]}\n")
+        f.write(f"typ {d.get('typ', 1)}\nseed {d.get('seed', 42)}\n")
+        f.write(f"per_cell_seed {int(d.get('per_cell_seed', False))}\nkeep_buffers {int(keep_buffers)}\n")
+
+
+def _golden_sweeps():
+    import json
+    with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+        return json.load(f)["sweeps"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("i", range(len(_golden_sweeps())))
+def test_cpp_sweep_grid_equals_reference(i, tmp_path):
+    """C++ sweep_grid<float> (sweep.hpp:249-326) on the batched device handle:
+    the labels CSV equals the reference's own (tests/golden/golden.json), and
+    with keep_buffers every cell's device statistics equal the host
+    classify_outcome over its snapshot buffer."""
+    case = _golden_sweeps()[i]
+    spec = tmp_path / "spec.txt"
+    _write_spec(spec, case["spec"], keep_buffers=True)
+    r = subprocess.run([BIN, "--sweep", str(spec)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout == case["labels_csv"]
+    assert " 0 mismatches" in r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_sweep_grid_cfg4_full_size(tmp_path):
+    """BASELINE cfg4 through the C++ API: 64 x 64 (Du, Dv) cells of 128^2 x 5000,
+    labels CSV byte-identical to the reference's (tests/golden/cfg4_labels.csv)."""
+    import numpy as np
+    spec = tmp_path / "cfg4.txt"
+    _write_spec(spec, {"x_param": "du", "xs": list(np.linspace(0.02, 0.70, 64)), "y_param": "dv",
+                       "ys": list(np.linspace(0.50, 1.20, 64)), "nn": 128, "nm": 128, "iter_max": 5000,
+                       "nssp": 5, "seed": 42})
+    r = subprocess.run([BIN, "--sweep", str(spec)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    with open(os.path.join(ROOT, "tests", "golden", "cfg4_labels.csv")) as f:
+        assert r.stdout == f.read()
