@@ -33,7 +33,6 @@ from typing import Callable, List, Optional
 
 import numpy as np
 
-from . import _lib
 from ._lib import RDCNN_FAST, RDCNN_STRICT, ParamsF32, ParamsF64, check, load
 
 DTYPES = {"single": np.float32, "double": np.float64}

@@ -12,7 +12,6 @@ import numpy as np
 import pytest
 
 import paper_2102_10340_b200 as fhn
-from paper_2102_10340_b200 import engine
 
 pytestmark = pytest.mark.gpu
 

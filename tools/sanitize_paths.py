@@ -5,8 +5,6 @@ fused peer-ring slab (world 1), the cluster kernel, device checksums and
 frame analysis."""
 import sys
 
-import numpy as np
-
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 import paper_2102_10340_b200 as fhn  # noqa: E402
 from paper_2102_10340_b200.slab import SlabStepper  # noqa: E402
