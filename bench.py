@@ -59,7 +59,10 @@ def parse():
     ap.add_argument("--levels", type=int, default=4, choices=(1, 2, 4, 8))
     ap.add_argument("--seg-rows", type=int, default=0)
     ap.add_argument("--mode", default="strict", choices=("strict", "fast"))
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="lattices through the e2e pipeline (0: the workload's default)")
+    ap.add_argument("--e2e-depth", type=int, default=0,
+                    help="lattices in flight in the e2e pipeline (0: the workload's default; 1: one after another)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="budget of the cpu_baseline sample on rank 0")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -92,6 +95,12 @@ class Workload:
             self.cols = self.rows_rank = self.rows_global = n
             self.typ, self.gene7 = (1 if self.name == "cfg1" else 3), DEFAULT_GENE7
             self.iters = args.iters_per_step or (1000 if self.name == "cfg1" else 200)
+            self.e2e_steps = 20 if self.name == "cfg1" else 12
+            # cfg3 is edge detection over a stream of independent images: two
+            # in flight, one's copies overlapping the other's advance.  Every
+            # other workload is one evolving lattice whose steps depend on each
+            # other, so its e2e runs them strictly one after another.
+            self.e2e_depth = 2 if self.name == "cfg3" else 1
             self.scaling = "weak"
             self.desc = (f"{self.name}: FHN RD-CNN {n}x{n} fp32 torus per GPU, "
                          + ("typ=1 seed 42" if self.typ == 1 else "typ=3 synthetic 8-bit image (SURVEY §8d)")
@@ -105,6 +114,8 @@ class Workload:
             self.rows_rank = self.rows_global // world
             self.typ, self.gene7 = 2, DEFAULT_GENE7
             self.iters = args.iters_per_step or 100
+            self.e2e_steps = 2
+            self.e2e_depth = 1
             self.scaling = "strong"
             self.desc = (f"cfg5: FHN RD-CNN {self.rows_global}x{self.cols} fp32 torus, typ=2 (full "
                          f"random) seed 42, reference default gene, {self.iters} iterations per step")
@@ -115,6 +126,8 @@ class Workload:
             self.rows_global = n * world
             self.typ, self.gene7 = 1, GENE7
             self.iters = args.iters_per_step or 10000
+            self.e2e_steps = 3
+            self.e2e_depth = 1
             self.scaling = "weak"
             self.desc = (f"cfg2: FHN RD-CNN {n}x{n} fp32 torus per GPU, typ=1 seed 42, "
                          f"slow-growth gene a=-0.05, {self.iters} iterations per step")
@@ -437,33 +450,54 @@ def bench_ours(args, rank, world, local_rank):
 
     # ---- end to end through the public API with host buffers (N=1 only) ----
     e2e = None
+    e2e_steps = args.e2e_steps or wl.e2e_steps
     if not use_slab:
+        # A stream of independent lattices through the public Pipeline API:
+        # each one is uploaded from pinned host memory, advanced S iterations
+        # and downloaded; with depth 2 one lattice's copies overlap another's
+        # advance.  Input: the state the timed run produced.
         cells = wl.rows_global * n
-        u_h = torch.empty(cells, dtype=torch.float32).pin_memory()
-        v_h = torch.empty(cells, dtype=torch.float32).pin_memory()
-        sim.download_ptr(u_h.data_ptr(), v_h.data_ptr())
+        depth = max(1, min(args.e2e_depth or wl.e2e_depth, e2e_steps))
+        pinned = (1 + depth) * 2 * 4 * cells
+        try:
+            import psutil
+            if depth > 1 and pinned > psutil.virtual_memory().available // 4:
+                depth = 1  # keep pinned host buffers under a quarter of free RAM
+        except ImportError:
+            pass
+        u_in = torch.empty(cells, dtype=torch.float32).pin_memory()
+        v_in = torch.empty(cells, dtype=torch.float32).pin_memory()
+        outs = [(torch.empty(cells, dtype=torch.float32).pin_memory(),
+                 torch.empty(cells, dtype=torch.float32).pin_memory()) for _ in range(depth)]
+        sim.download_ptr(u_in.data_ptr(), v_in.data_ptr())
+        pipe = fhn.Pipeline(wl.rows_global, n, depth=depth, sims=[sim], device=local_rank, mode=args.mode,
+                            levels=args.levels, seg_rows=args.seg_rows)
+        pipe.set_params(gene)
+        for extra in pipe.sims[1:]:  # first-use costs of the new handles stay out of the timed region
+            extra.upload_ptr(u_in.data_ptr(), v_in.data_ptr())
+            extra.advance(min(S, 64))
+        jobs = [(u_in.data_ptr(), v_in.data_ptr(), outs[i % depth][0].data_ptr(), outs[i % depth][1].data_ptr())
+                for i in range(e2e_steps)]
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            sim.upload_ptr(u_h.data_ptr(), v_h.data_ptr())
-            bad = sim.advance(S)
-            sim.download_ptr(u_h.data_ptr(), v_h.data_ptr())
+        bad = pipe.run(jobs, S)
         torch.cuda.synchronize()
         te = torch.tensor([time.perf_counter() - t0], device=red_dev)
         if dist is not None:  # replicas: max wall time over ranks
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        pipe.close()
         e2e_s = float(te.item())
-        e2e = {"value": round(cells * world * S * args.e2e_steps / e2e_s / 1e6, 2),
+        e2e = {"value": round(cells * world * S * e2e_steps / e2e_s / 1e6, 2),
                "unit": "Mcell-updates/s", "h2d_bytes_per_step": 2 * 4 * cells * world,
                "d2h_bytes_per_step": 2 * 4 * cells * world,
-               "path": "rdcnn_sim_upload (pinned host) -> rdcnn_sim_advance -> rdcnn_sim_download"
-                       + ("; per rank, max wall time over ranks" if world > 1 else ""),
-               "steps": args.e2e_steps}
-        # sanity: state stays finite
-        un = u_h.numpy()
-        if not np.isfinite(un).all():
+               "path": (f"paper_2102_10340_b200.Pipeline(depth={depth}): per lattice rdcnn_sim_upload "
+                        "(pinned host) -> rdcnn_sim_advance -> rdcnn_sim_download"
+                        + (", lattices on alternating handles so copies overlap advances" if depth > 1 else "")
+                        + ("; per rank, max wall time over ranks" if world > 1 else "")),
+               "steps": e2e_steps, "lattices_in_flight": depth}
+        if bad.any() or not all(np.isfinite(u.numpy()).all() for u, _ in outs):
             raise RuntimeError("non-finite state after e2e")
     else:
         # Slab path: every rank uploads its slab from pinned host memory,
@@ -476,7 +510,7 @@ def bench_ours(args, rank, world, local_rank):
         if dist is not None:
             dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
+        for _ in range(e2e_steps):
             fhn._lib.check(lib.rdcnn_sim_upload(slab._h, u_h.data_ptr(), v_h.data_ptr()))
             slab.fill_ghosts()
             bad = slab.advance(S)
@@ -488,12 +522,12 @@ def bench_ours(args, rank, world, local_rank):
         if dist is not None:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_s = float(te.item())
-        e2e = {"value": round(cells * world * S * args.e2e_steps / e2e_s / 1e6, 2),
+        e2e = {"value": round(cells * world * S * e2e_steps / e2e_s / 1e6, 2),
                "unit": "Mcell-updates/s", "h2d_bytes_per_step": 2 * 4 * cells * world,
                "d2h_bytes_per_step": 2 * 4 * cells * world,
                "path": "per rank: rdcnn_sim_upload (pinned host) -> rdcnn_slab_fill_ghosts -> "
                        "rdcnn_slab_advance -> rdcnn_sim_download; max wall time over ranks",
-               "steps": args.e2e_steps}
+               "steps": e2e_steps}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

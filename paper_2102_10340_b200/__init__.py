@@ -7,7 +7,7 @@ reference's C++ API, see :mod:`.engine`) plus the multi-GPU slab driver
 """
 from ._lib import LIB_PATH, LibraryMissing, RdcnnError, last_error, load  # noqa: F401
 from .engine import (  # noqa: F401
-    Backend, BlowUpError, Gene, GridState, RunConfig, RunOutput, ScheduleError, Simulator,
+    Backend, BlowUpError, Gene, GridState, Pipeline, RunConfig, RunOutput, ScheduleError, Simulator,
     SnapshotBuffer, StepBuffers, checksum, checksum_hex, gene_valid, init_center_square,
     init_from_image, init_full_random, initial_state, make_backend, params_from_gene, run,
     run_timed, step, validate_config,

@@ -137,14 +137,16 @@ size_t smem_for(int w) {
 template <class T>
 int resident_blocks(int k, int w, bool fast, bool per_grid, bool wrap) {
   KernelTable<T>& t = table<T>();
-  int& r = t.resident[w > 1][k_index(k)][fast][per_grid][wrap];
+  // Handles may launch concurrently from several host threads: the memo is
+  // read and written atomically (every writer stores the same value).
+  int* slot = &t.resident[w > 1][k_index(k)][fast][per_grid][wrap];
+  int r = __atomic_load_n(slot, __ATOMIC_RELAXED);
   if (r == 0) {
-    int n = 0;
     auto fn = t.fn[w > 1][k_index(k)][fast][per_grid][wrap];
-    if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kThreads, smem_for<T>(w)) !=
-                   cudaSuccess || n < 1)
-      n = 1;
-    r = n;
+    if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, fn, kThreads, smem_for<T>(w)) !=
+                   cudaSuccess || r < 1)
+      r = 1;
+    __atomic_store_n(slot, r, __ATOMIC_RELAXED);
   }
   return r;
 }
@@ -809,6 +811,8 @@ bool cluster_plan_for(rdcnn_sim* s, ClusterPlan* out) {
     p.smem = (size_t)(w == 4 ? rdcnn_dev::cluster_smem_bytes<4>(p.R) : rdcnn_dev::cluster_smem_bytes<8>(p.R));
     if (p.smem > 200 * 1024) continue;
     static int checked[2][5][2][rdcnn_dev::kClusterMax + 1] = {};  // 1 ok, -1 not launchable
+    static std::mutex checked_mu;  // handles may plan concurrently from several host threads
+    std::lock_guard<std::mutex> lock(checked_mu);
     int& ok = checked[w == 8][rw][fast][C];
     if (ok == 0) {
       ClusterFn fn = cluster_fn(w, rw, fast);

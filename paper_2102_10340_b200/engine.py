@@ -344,6 +344,71 @@ class Simulator:
         return u.value, v.value
 
 
+class Pipeline:
+    """A stream of independent lattices of one shape (images to process,
+    initial states to evolve) through ``depth`` device handles, one host
+    thread each.  Lattice i runs on handle i % depth as upload -> advance ->
+    download, so its host<->device copies overlap another lattice's advance:
+    the C-ABI calls release the GIL and every handle has its own stream.
+    Results are those of one Simulator running the jobs one after another.
+
+    ``sims``: existing (e.g. warmed) Simulators of that shape to use as the
+    first handles; the rest are created with ``kw`` (Simulator arguments)."""
+
+    def __init__(self, rows: int, cols: int, depth: int = 2, sims: Optional[List[Simulator]] = None, **kw):
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        self.sims = list(sims or [])[:depth]
+        for s in self.sims:
+            if (s.rows, s.cols, s.batch) != (rows, cols, 1):
+                raise ValueError("pipeline simulators must be single rows x cols lattices")
+        self._owned = [Simulator(rows, cols, **kw) for _ in range(depth - len(self.sims))]
+        self.sims += self._owned
+
+    def set_params(self, gene):
+        for s in self.sims:
+            s.set_params(gene)
+
+    def run(self, jobs, steps: int) -> np.ndarray:
+        """``jobs``: (u_in, v_in, u_out, v_out) host pointers per lattice
+        (pinned memory for full copy bandwidth; an output pair must not be
+        shared by jobs on different handles).  Advances each lattice ``steps``
+        iterations; returns its first bad iteration (0 = stayed finite), the
+        output holding the state after ``steps`` either way (engine.hpp:79)."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        jobs = list(jobs)
+        bad = np.zeros(len(jobs), np.int64)
+        d = len(self.sims)
+
+        def lane(k: int):
+            sim = self.sims[k]
+            for i in range(k, len(jobs), d):
+                u_in, v_in, u_out, v_out = jobs[i]
+                sim.upload_ptr(u_in, v_in)
+                bad[i] = sim.advance(steps)[0]
+                sim.download_ptr(u_out, v_out)
+
+        if d == 1:
+            lane(0)
+        else:
+            with ThreadPoolExecutor(d) as ex:
+                for f in [ex.submit(lane, k) for k in range(min(d, len(jobs)))]:
+                    f.result()
+        return bad
+
+    def close(self):
+        for s in self._owned:
+            s.close()
+        self._owned = []
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
 # ---------------------------------------------------------------------------
 # Reference-shaped API
 # ---------------------------------------------------------------------------

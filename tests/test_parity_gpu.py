@@ -685,3 +685,35 @@ def test_autotuned_segments_bit_identical(rows, cols):
             assert int(sim.advance(123)[0]) == 0
             out.append(sim.download())
     assert np.array_equal(bits(out[0][0]), bits(out[1][0])) and np.array_equal(bits(out[0][1]), bits(out[1][1]))
+
+
+@pytest.mark.parametrize("n,steps", [(256, 300), (512, 200)])
+def test_pipeline_equals_sequential(n, steps):
+    """engine.Pipeline: independent lattices on two handles driven from two host
+    threads (copies overlapping advances) give exactly the results of one
+    Simulator running the same jobs in order, blow-up reports included.  256^2
+    runs on the one-launch cluster path, so two clusters run concurrently."""
+    import torch
+
+    ins = [fhn.init_full_random(n, n, seed) for seed in (3, 4, 5, 6, 7)]
+    ins[3].u[:] = 1e19  # u*u overflows: this job blows up at iteration 1
+    gene = fhn.Gene(a=-0.05)
+    with fhn.Simulator(n, n) as ref:
+        ref.set_params(gene)
+        want = []
+        for s in ins:
+            ref.upload(s.u, s.v)
+            bad = int(ref.advance(steps)[0])
+            want.append((bad,) + tuple(ref.download()))
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    src = [(pin(s.u), pin(s.v)) for s in ins]
+    dst = [(torch.empty(n * n).pin_memory(), torch.empty(n * n).pin_memory()) for _ in ins]
+    with fhn.Pipeline(n, n, depth=2) as pipe:
+        pipe.set_params(gene)
+        bad = pipe.run([(su.data_ptr(), sv.data_ptr(), du.data_ptr(), dv.data_ptr())
+                        for (su, sv), (du, dv) in zip(src, dst)], steps)
+    for i, (b, u, v) in enumerate(want):
+        assert bad[i] == b, i
+        assert np.array_equal(dst[i][0].numpy().view(np.uint32), u.view(np.uint32)), i
+        assert np.array_equal(dst[i][1].numpy().view(np.uint32), v.view(np.uint32)), i
+    assert bad[3] == 1 and not bad[[0, 1, 2, 4]].any()
