@@ -786,14 +786,15 @@ std::vector<int> cluster_rw_order() {
 }
 
 // One cluster of C CTAs, each R = nw*RW rows (nw warps of RW rows), W =
-// cols/32 columns per lane (4 or 8): the most CTAs first.  Returns false
-// when the shape does not fit or the device cannot host the cluster (then
-// the wavefront kernel runs).
-bool cluster_plan_for(rdcnn_sim* s, ClusterPlan* out) {
-  if (s->slab || s->batch != 1 || s->elem != 4 || s->params_stride != 0 || s->cluster_mode < 0) return false;
-  if (s->cols % 128 != 0) return false;
+// cols/32 columns per lane (4 or 8), the most CTAs per RW: every launchable
+// plan, one per rows-per-warp candidate.  Empty when the shape does not fit
+// or the device cannot host the cluster (then the wavefront kernel runs).
+std::vector<ClusterPlan> cluster_plans(rdcnn_sim* s) {
+  std::vector<ClusterPlan> plans;
+  if (s->slab || s->batch != 1 || s->elem != 4 || s->params_stride != 0 || s->cluster_mode < 0) return plans;
+  if (s->cols % 128 != 0) return plans;
   const int w = s->cols / 32;
-  if (w != 4 && w != 8) return false;
+  if (w != 4 && w != 8) return plans;
   const bool fast = s->mode == RDCNN_FAST;
   for (int rw : cluster_rw_order()) {
     int C = 0;
@@ -836,10 +837,9 @@ bool cluster_plan_for(rdcnn_sim* s, ClusterPlan* out) {
       cudaGetLastError();
     }
     if (ok != 1) continue;
-    *out = p;
-    return true;
+    plans.push_back(p);
   }
-  return false;
+  return plans;
 }
 
 int cluster_advance(rdcnn_sim* s, const ClusterPlan& pl, long steps, long* first_bad, bool* fell_back) {
@@ -1039,14 +1039,89 @@ int advance_launches(rdcnn_sim* s, long steps, long* first_bad) {
   return RDCNN_OK;
 }
 
+// Rows per warp of the cluster kernel: more rows per warp amortise the
+// per-step exchange, more warps hide latency, and the best trade depends on
+// the shape (256^2: RW=4 72k vs RW=1 61k Mcell-updates/s; 128^2: RW=1 41k
+// vs RW=4 32k).  So the first long advance of a shape runs kTrial steps on
+// each candidate -- real progress of the advance, timed by its CUDA events
+// -- and the fastest is kept process-wide; later advances use it directly.
+using ClusterKey = std::tuple<int, int, int, int>;  // device, rows, cols, mode
+std::mutex g_cluster_mu;
+std::map<ClusterKey, int> g_cluster_rw;
+
+int cluster_advance_tuned(rdcnn_sim* s, const std::vector<ClusterPlan>& plans, long steps, long* first_bad,
+                          bool* fell_back) {
+  constexpr long kTrial = 128;
+  const ClusterKey key{s->device, s->rows, s->cols, s->mode};
+  int rw = 0;
+  {
+    std::lock_guard<std::mutex> lock(g_cluster_mu);
+    const auto it = g_cluster_rw.find(key);
+    if (it != g_cluster_rw.end()) rw = it->second;
+  }
+  auto plan_of = [&](int r) {
+    for (const ClusterPlan& p : plans)
+      if (p.RW == r) return p;
+    return plans[0];
+  };
+  if (rw != 0 || plans.size() == 1 || steps < (long)(plans.size() + 1) * kTrial)
+    return cluster_advance(s, rw ? plan_of(rw) : plans[0], steps, first_bad, fell_back);
+
+  long done = 0, launches = 0;
+  double ms = 0;
+  float best = 1e30f;
+  int best_rw = plans[0].RW;
+  bool all_ran = true;
+  for (const ClusterPlan& p : plans) {
+    long fb = 0;
+    const int rc = cluster_advance(s, p, kTrial, &fb, fell_back);
+    if (*fell_back) {  // this candidate could not be placed right now
+      *fell_back = false;
+      all_ran = false;
+      continue;
+    }
+    ms += s->last_ms;
+    launches += s->launches;
+    if (rc != RDCNN_OK) {  // blow-up inside a trial: exact, and the advance ends there
+      if (rc == RDCNN_EBLOWUP && first_bad) first_bad[0] = done + fb;
+      s->last_ms = ms;
+      s->launches = launches;
+      return rc;
+    }
+    done += kTrial;
+    if (s->last_ms < best) {
+      best = s->last_ms;
+      best_rw = p.RW;
+    }
+  }
+  if (done == 0) {  // no candidate could be placed: the wavefront path runs the whole advance
+    *fell_back = true;
+    return RDCNN_OK;
+  }
+  if (all_ran) {
+    std::lock_guard<std::mutex> lock(g_cluster_mu);
+    g_cluster_rw.emplace(key, best_rw);
+  }
+  long fb = 0;
+  int rc = cluster_advance(s, plan_of(best_rw), steps - done, &fb, fell_back);
+  if (*fell_back) {  // finish on the wavefront path
+    *fell_back = false;
+    rc = advance_launches<float>(s, steps - done, &fb);
+  }
+  s->last_ms += ms;
+  s->launches += launches;
+  if (first_bad) first_bad[0] = fb ? done + fb : 0;
+  return rc;
+}
+
 template <class T>
 int advance_impl(rdcnn_sim* s, long steps, long* first_bad) {
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   if constexpr (sizeof(T) == 4) {
-    ClusterPlan pl;
-    if (steps > 0 && cluster_plan_for(s, &pl)) {
+    const std::vector<ClusterPlan> plans = steps > 0 ? cluster_plans(s) : std::vector<ClusterPlan>{};
+    if (!plans.empty()) {
       bool fell_back = false;
-      const int rc = cluster_advance(s, pl, steps, first_bad, &fell_back);
+      const int rc = cluster_advance_tuned(s, plans, steps, first_bad, &fell_back);
       if (!fell_back) return rc;
     }
     if (s->cluster_mode > 0) return fail(RDCNN_EINVAL, "persistent cluster path required but %dx%d (batch %d) does not fit it",

@@ -41,11 +41,11 @@ def digest(sim, rows, cols):
 
 def test_cfg1_256_x1000(gold):
     c = gold["cfg1"]
-    with fhn.Simulator(256, 256) as sim:
+    with fhn.Simulator(256, 256, persistent=1) as sim:  # the cluster path, required
         sim.set_params(gene(c["gene7"]))
         sim.init(1, 42)
         assert int(sim.advance(c["iters"])[0]) == 0
-        assert sim.launch_count() == 1  # the cluster path
+        assert sim.launch_count() in (1, 4)  # one launch, or 3 rows-per-warp trials + the rest
         assert digest(sim, 256, 256) == c["checksum"]
 
 

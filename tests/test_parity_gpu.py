@@ -8,6 +8,8 @@ Bit-exact (strict mode) against:
     uniform preservation, slab == periodic).
 The reference's own test names are cited per test.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -70,12 +72,13 @@ def test_golden_cases_persistent_cluster(golden):
     used = 0
     for case in golden:
         r, c = case["rows"], case["cols"]
-        with fhn.Simulator(r, c) as sim:
+        fits = c in (128, 256) and r <= 256  # these shapes must take the cluster path (required below)
+        with fhn.Simulator(r, c, persistent=1 if fits else 0) as sim:
             sim.set_params(gene_from7(case["gene7"]))
             sim.init(case["typ"], case["seed"])
             bad = sim.advance(case["iters"])
             assert int(bad[0]) == case["bad_iter"], case["name"]
-            used += sim.launch_count() == 1 and case["iters"] > 4
+            used += fits and case["iters"] > 4
             if case["bad_iter"] == 0:
                 u, v = sim.download()
                 assert f"{fhn.checksum(fhn.GridState(r, c, u, v)):016x}" == case["checksum"], case["name"]
@@ -143,7 +146,7 @@ def test_persistent_cluster_path(oracle, rows, cols):
     with fhn.Simulator(rows, cols, persistent=1) as sim:
         sim.upload(u0, v0)
         assert int(sim.advance(iters)[0]) == 0
-        assert sim.launch_count() == 1
+        assert sim.launch_count() in (1, 4)  # one launch, or 3 rows-per-warp trials + the rest
         u, v = sim.download()
     assert np.array_equal(bits(u), bits(ou)) and np.array_equal(bits(v), bits(ov))
     # blow-up: checkerboard instability, the exact iteration and the state right after it
@@ -717,3 +720,44 @@ def test_pipeline_equals_sequential(n, steps):
         assert np.array_equal(dst[i][0].numpy().view(np.uint32), u.view(np.uint32)), i
         assert np.array_equal(dst[i][1].numpy().view(np.uint32), v.view(np.uint32)), i
     assert bad[3] == 1 and not bad[[0, 1, 2, 4]].any()
+
+
+_CLUSTER_TUNE_CASE = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2102_10340_b200 as fhn
+g = fhn.Gene(dt=float(sys.argv[2]))
+out = []
+for pers in (0, -1):  # 0: the cluster path (tunes rows-per-warp on this first advance); -1: wavefront
+    with fhn.Simulator(128, 128, persistent=pers) as sim:
+        sim.set_params(g)
+        sim.init(1, 42)
+        bad = int(sim.advance(1000)[0])
+        u, v = sim.download()
+        out.append((bad, sim.launch_count(), u.view(np.uint32).copy(), v.view(np.uint32).copy()))
+(b0, l0, u0, v0), (b1, _, u1, v1) = out
+assert b0 == b1 and np.array_equal(u0, u1) and np.array_equal(v0, v1), (b0, b1)
+print(b0, l0, f"{fhn.checksum(fhn.GridState(128, 128, u0.view(np.float32), v0.view(np.float32))):016x}")
+"""
+
+
+@pytest.mark.parametrize("dt,want_bad", [(0.26, 81), (0.25, 349), (0.249, 504), (0.248, 869), (0.247, 0)])
+def test_cluster_rows_per_warp_tuning_exact(dt, want_bad):
+    """The cluster path's first advance of a shape times each rows-per-warp
+    candidate on 128 real steps, then finishes on the fastest.  Blow-ups inside
+    a trial (81, 349) or after (504, 869) report the reference's iteration
+    (oracle/_ref, 128^2 typ=1 seed 42) with the wavefront path's exact state;
+    a finite run ends on the reference's checksum."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _CLUSTER_TUNE_CASE, root, repr(dt)], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    bad, launches, digest = r.stdout.split()
+    assert int(bad) == want_bad
+    if want_bad == 0 or want_bad > 3 * 128:
+        assert int(launches) >= 4  # three 128-step trials, then the rest on the winner
+    if want_bad == 0:
+        assert digest == "6684ada76ef62d08"
