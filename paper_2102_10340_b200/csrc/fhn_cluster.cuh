@@ -10,10 +10,11 @@
 //      also goes into the previous/next CTA's halo row by st.async, whose
 //      bytes are counted on the RECEIVER's mbarrier (complete_tx) -- the
 //      torus ring across the cluster;
-//   2. each warp arrives (release) on this parity's mbarrier, computes its
-//      interior rows (1..RW-2, registers only) and then waits on it: the
-//      barrier completes when all warps of the CTA have published and both
-//      halo rows have landed.  There is no per-step cluster barrier and no
+//   2. every thread arrives (release) on this parity's local mbarrier after
+//      its own stores, the warp computes its interior rows (1..RW-2,
+//      registers only) and then waits on it: the barrier completes when all
+//      threads of the CTA have published; the CTA's two edge warps also wait
+//      for both halo rows' bytes on the halo mbarrier.  There is no per-step cluster barrier and no
 //      GPU-scope fence: a CTA synchronises only with its ring neighbours;
 //   3. the edge rows: up/down rows from shared memory, left/right columns
 //      from warp shuffles (the row wraps around the warp: the torus column
@@ -231,12 +232,12 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
       v[r][k] = y.x; v[r][k + 1] = y.y; v[r][k + 2] = y.z; v[r][k + 3] = y.w;
     }
   }
-  // Per parity: lbar completes when all nw warps of this CTA have published
-  // (arrive, release); mbar when both halo rows' bytes have landed
+  // Per parity: lbar completes when all 32*nw threads of this CTA have
+  // published (arrive, release); mbar when both halo rows' bytes have landed
   // (complete_tx from the ring neighbours' st.async; armed by thread 0).
   if (threadIdx.x == 0) {
-    mbar_init(lbar, (unsigned)nw);
-    mbar_init(lbar + 8, (unsigned)nw);
+    mbar_init(lbar, (unsigned)(32 * nw));  // every thread releases its own exchange-row stores
+    mbar_init(lbar + 8, (unsigned)(32 * nw));
     mbar_init(mbar, 1);
     mbar_init(mbar + 8, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
   // and its two ring neighbours.  Write-after-read safety with one step of
   // slack: the rows of parity p are rewritten at step n+2 only by a writer
   // that has waited at step n+1 for data its readers publish after finishing
-  // step n (siblings: all nw arrivals; a neighbour: this CTA's edge row,
+  // step n (siblings: all 32*nw arrivals; a neighbour: this CTA's edge row,
   // published by the very warp that read the halo).
   Finite<float> fin;
   bool flagged = false;
@@ -260,11 +261,11 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
     if (RW > 1) publish_row<W>(my_last + par, u[RW - 1], v[RW - 1]);
     if (cta_first) publish_row_remote<W>(to_prev + par, u[0], v[0], mbar_prev + (mb - mbar));
     if (cta_last) publish_row_remote<W>(to_next + par, u[RW - 1], v[RW - 1], mbar_next + (mb - mbar));
-    __syncwarp();
-    if (lane == 0) {
-      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(lb) : "memory");
-      if (warp == 0) mbar_arrive_expect_tx(mb, 2u * kRow);  // arms the two halo rows' bytes
-    }
+    // Every thread arrives (release) after its own stores, so each reader's
+    // acquire-wait orders exactly the stores it reads -- no reliance on a
+    // warp barrier's cumulativity.
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(lb) : "memory");
+    if (warp == 0 && lane == 0) mbar_arrive_expect_tx(mb, 2u * kRow);  // arms the two halo rows' bytes
     // 2. interior rows need only this warp's registers: overlap the wait
     float un[RW][W], vn[RW][W];
 #pragma unroll

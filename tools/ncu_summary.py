@@ -57,6 +57,8 @@ def main():
     ap.add_argument("--levels", type=int, required=True, help="time levels per launch")
     ap.add_argument("--tag", required=True)
     ap.add_argument("--note", default="")
+    ap.add_argument("--secondary", action="store_true",
+                    help="not the bench kernel: leave profiles/ncu_summary.json (bench.py's traffic) alone")
     a = ap.parse_args()
 
     hdr, units, rows = raw(a.rep)
@@ -103,8 +105,9 @@ def main():
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"ncu_{a.tag}.json"), "w") as f:
         json.dump(d, f, indent=1)
-    with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
-        json.dump(d, f, indent=1)
+    if not a.secondary:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
+            json.dump(d, f, indent=1)
     print(json.dumps(d, indent=1))
 
 

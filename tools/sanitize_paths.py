@@ -1,8 +1,9 @@
 """Small runs of every kernel path, for compute-sanitizer (memcheck /
 racecheck / synccheck): wavefront K=1/2/4/8 at W=1/4 (odd and full-width
 shapes), batch with per-grid genes, fp64, fast mode, blow-up replay, the
-fused peer-ring slab (world 1), the cluster kernel, device checksums and
-frame analysis."""
+fused peer-ring slab (world 1), the cluster kernel (incl. its rows-per-warp
+trials), concurrent handles from host threads (engine.Pipeline), device
+checksums and frame analysis."""
 import sys
 
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
@@ -40,4 +41,13 @@ with fhn.Simulator(64, 128, persistent=1) as s:  # cluster path blow-up + re-run
     s.set_params(fhn.Gene(dt=100.0))
     s.init(2, 9)
     s.advance(20)
+with fhn.Simulator(64, 128, persistent=1) as s:  # cluster rows-per-warp trials (>= 4 x 128 steps)
+    s.init(2, 9)
+    s.advance(520)
+import numpy as np  # noqa: E402
+
+st = fhn.init_full_random(40, 128, 5)
+outs = [(np.empty(40 * 128, np.float32), np.empty(40 * 128, np.float32)) for _ in range(3)]
+with fhn.Pipeline(40, 128, depth=2, persistent=-1) as p:  # two handles driven from two host threads
+    p.run([(st.u.ctypes.data, st.v.ctypes.data, u.ctypes.data, v.ctypes.data) for u, v in outs], 9)
 print("sanitize paths done")
