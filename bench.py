@@ -242,19 +242,30 @@ def ncu_traffic():
     return d.get("dram_bytes_per_launch"), d.get("cell_updates_per_launch")
 
 
+def host_threads() -> int:
+    """Every host core this process may run on.  torchrun exports
+    OMP_NUM_THREADS=1 to each rank, so the reference's OpenMP default would be
+    one thread there; the reference arm passes this count explicitly to the
+    reference's Backend instead (backend.hpp:44-50, threads > 0)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        return os.cpu_count() or 1
+
+
 def cpu_baseline_sample(wl: "Workload", budget_s: float):
     """The reference's own parallel backend (oracle/_ref, reference headers
     compiled read-only) on a bounded prefix of the same workload."""
     from oracle.oracle import Reference
     ref = Reference()
-    threads = ref.max_threads()
+    threads = host_threads()
     R, C = wl.rows_global, wl.cols
     u, v = wl.ref_state(ref)
     # calibrate with 2 iterations, then size the sample to the budget
-    u, v, _, sec = ref.run_timed(R, C, u, v, 2, wl.gene7, backend="parallel")
+    u, v, _, sec = ref.run_timed(R, C, u, v, 2, wl.gene7, backend="parallel", threads=threads)
     per_iter = max(sec / 2, 1e-6)
     iters = int(max(2, min(2000, budget_s / per_iter)))
-    u, v, bad, sec = ref.run_timed(R, C, u, v, iters, wl.gene7, backend="parallel")
+    u, v, bad, sec = ref.run_timed(R, C, u, v, iters, wl.gene7, backend="parallel", threads=threads)
     value = R * C * iters / sec / 1e6
     return {"value": round(value, 2), "unit": "Mcell-updates/s", "cores": threads,
             "kind": "reference",
@@ -285,16 +296,16 @@ def bench_reference(args, rank, world):
     wl = Workload(args, world)
     ref = Reference()
     R, C = wl.rows_global, wl.cols  # the same global lattice our arm advances
-    threads = ref.max_threads()
+    threads = host_threads()
     u, v = wl.ref_state(ref)
     # size each step to ~2 s of CPU work so the whole run stays within minutes
-    u, v, _, sec = ref.run_timed(R, C, u, v, 2, wl.gene7, backend="parallel")
+    u, v, _, sec = ref.run_timed(R, C, u, v, 2, wl.gene7, backend="parallel", threads=threads)
     iters = int(max(1, min(wl.iters, 2.0 / max(sec / 2, 1e-6))))
     for _ in range(args.warmup):
-        u, v, _, _ = ref.run_timed(R, C, u, v, iters, wl.gene7, backend="parallel")
+        u, v, _, _ = ref.run_timed(R, C, u, v, iters, wl.gene7, backend="parallel", threads=threads)
     total = 0.0
     for _ in range(args.steps):
-        u, v, bad, sec = ref.run_timed(R, C, u, v, iters, wl.gene7, backend="parallel")
+        u, v, bad, sec = ref.run_timed(R, C, u, v, iters, wl.gene7, backend="parallel", threads=threads)
         total += sec
     value = R * C * iters * args.steps / total / 1e6
     sample = (f"reference parallel backend via run_timed (oracle/_ref = reference headers), "

@@ -13,9 +13,9 @@ BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_ste
              "scaling", "vs_baseline", "dtype", "data", "config"}
 
 
-def run_bench(*args, timeout=600):
+def run_bench(*args, timeout=600, env=None):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
-                       timeout=timeout, cwd=ROOT)
+                       timeout=timeout, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
     assert len(lines) == 1, r.stdout
@@ -29,6 +29,14 @@ def test_reference_arm_contract():
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "Mcell-updates/s"
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def test_reference_arm_uses_every_host_core():
+    """torchrun exports OMP_NUM_THREADS=1 to each rank; the reference arm must
+    still run the reference's parallel backend on every usable host core."""
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    d = run_bench("--impl", "reference", "--size", "64", "--steps", "1", "--warmup", "1", env=env)
+    assert d["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
 
 
 @pytest.mark.gpu
