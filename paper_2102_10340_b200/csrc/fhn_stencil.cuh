@@ -202,9 +202,12 @@ __device__ __forceinline__ void fold_finite(Finite<T>& f, const Row<W, T>& r) {
 template <int W, class T>
 __device__ __forceinline__ void store_row(T* __restrict__ u, T* __restrict__ v, size_t off,
                                           const Row<W, T>& r) {
-  if constexpr (W * sizeof(T) == 16 && sizeof(T) == 4) {
-    __stcs(reinterpret_cast<float4*>(u + off), make_float4(r.u[0], r.u[1], r.u[2], r.u[3]));
-    __stcs(reinterpret_cast<float4*>(v + off), make_float4(r.v[0], r.v[1], r.v[2], r.v[3]));
+  if constexpr (W * sizeof(T) % 16 == 0 && sizeof(T) == 4) {
+#pragma unroll
+    for (int c = 0; c < W; c += 4) {
+      __stcs(reinterpret_cast<float4*>(u + off + c), make_float4(r.u[c], r.u[c + 1], r.u[c + 2], r.u[c + 3]));
+      __stcs(reinterpret_cast<float4*>(v + off + c), make_float4(r.v[c], r.v[c + 1], r.v[c + 2], r.v[c + 3]));
+    }
   } else if constexpr (W * sizeof(T) == 16 && sizeof(T) == 8) {
     __stcs(reinterpret_cast<double2*>(u + off), make_double2(r.u[0], r.u[1]));
     __stcs(reinterpret_cast<double2*>(v + off), make_double2(r.v[0], r.v[1]));
@@ -267,9 +270,17 @@ template <int W, class T>
 __device__ __forceinline__ void stage_row(uint32_t dst, const T* __restrict__ u,
                                           const T* __restrict__ v, size_t off) {
   constexpr int B = int(sizeof(T)) * W;  // bytes per lane per plane
-  if constexpr (B == 16) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(u + off) : "memory");
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 32 * B), "l"(v + off) : "memory");
+  if constexpr (B % 16 == 0) {
+    // 16-byte chunks, chunk-major: chunk c of every lane at c*512 + lane*16,
+    // so each LDS.128 of a warp reads 512 contiguous bytes (dst is this
+    // lane's chunk-0 address; B == 16 is the plain per-lane layout).
+    constexpr int E = 16 / int(sizeof(T));
+#pragma unroll
+    for (int c = 0; c < B / 16; ++c) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 512 * c), "l"(u + off + E * c) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 32 * B + 512 * c), "l"(v + off + E * c)
+                   : "memory");
+    }
   } else {
     constexpr int E = int(sizeof(T));
 #pragma unroll
@@ -295,11 +306,16 @@ __device__ __forceinline__ void lds(uint32_t a, double& x) {
 template <int W, class T>
 __device__ __forceinline__ void read_staged(uint32_t src, Row<W, T>& r) {
   constexpr int B = int(sizeof(T)) * W;
-  if constexpr (B == 16 && sizeof(T) == 4) {
-    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
-                 : "=f"(r.u[0]), "=f"(r.u[1]), "=f"(r.u[2]), "=f"(r.u[3]) : "r"(src) : "memory");
-    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
-                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]) : "r"(src + 32 * B) : "memory");
+  if constexpr (B % 16 == 0 && sizeof(T) == 4) {
+#pragma unroll
+    for (int c = 0; c < W; c += 4) {
+      asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+                   : "=f"(r.u[c]), "=f"(r.u[c + 1]), "=f"(r.u[c + 2]), "=f"(r.u[c + 3]) : "r"(src + 128 * c) : "memory");
+      asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+                   : "=f"(r.v[c]), "=f"(r.v[c + 1]), "=f"(r.v[c + 2]), "=f"(r.v[c + 3])
+                   : "r"(src + 32 * B + 128 * c)
+                   : "memory");
+    }
   } else if constexpr (B == 16 && sizeof(T) == 8) {
     asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(r.u[0]), "=d"(r.u[1]) : "r"(src) : "memory");
     asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(r.v[0]), "=d"(r.v[1]) : "r"(src + 32 * B) : "memory");
@@ -418,9 +434,9 @@ constexpr int kCtaThreads = 32 * kWarpsPerCta;
 
 // Resident warps per SM the register budget is capped for: 16 warps
 // (<= 128 registers) for fp32 K <= 4 and fp64 K <= 2, else 8.
-template <int K, class T>
+template <int K, class T, int W = 16 / int(sizeof(T))>
 struct MinBlocks {
-  static constexpr int kWarps = (sizeof(T) == 4 ? K <= 4 : K <= 2) ? 16 : 8;
+  static constexpr int kWarps = (sizeof(T) * W <= 16 && (sizeof(T) == 4 ? K <= 4 : K <= 2)) ? 16 : 8;
   static constexpr int value = kWarps / kWarpsPerCta;
 };
 
@@ -528,11 +544,13 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
   const ptrdiff_t vout_delta = vout - uout;
 
   constexpr uint32_t kLaneBytes = uint32_t(sizeof(T)) * W;
+  // A lane's first chunk: lane*16 in the chunk-major layout (16-byte multiples), else lane*kLaneBytes.
+  constexpr uint32_t kLaneStride = kLaneBytes % 16 == 0 ? 16u : kLaneBytes;
   constexpr uint32_t kSlot = 2 * 32 * kLaneBytes;  // bytes of one staged row (u,v)
   constexpr bool kBulk = BulkStage<W, T>::value;
   constexpr uint32_t kWarpSmem = kStage * kSlot + (kBulk ? 64u : 0u);
   const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)wib * kWarpSmem +
-                        lane * kLaneBytes;
+                        lane * kLaneStride;
   // Bulk staging works on warp-uniform quantities only: the band row starts
   // at lane 0's column group; a band that wraps the torus edge has a second
   // piece starting at group 0.  Slot s's barrier is at mbar0 + 8*s.
@@ -565,7 +583,7 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
       ub += pitch;
       if (rows_left == 1) ub -= span;  // same wrap point as su (src_next)
     } else {
-      stage_row<W, T>(slot + lane * kLaneBytes, su, su + vdelta, 0);
+      stage_row<W, T>(slot + lane * kLaneStride, su, su + vdelta, 0);
     }
   };
 
@@ -587,7 +605,7 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
   // j+3 goes to slot ph of the other half.  Both half bases swap once per
   // group, so every slot address is a base plus a compile-time offset.
   // Half bases are warp-uniform; a lane reads its own chunk at + lane_off.
-  const uint32_t lane_off = lane * kLaneBytes;
+  const uint32_t lane_off = lane * kLaneStride;
   uint32_t half_now = ring0, half_other = ring0 + 3 * kSlot;
   uint32_t mb_now = mbar0, mb_other = mbar0 + 24u;  // their slots' barriers (bulk)
   uint32_t phase_now = 0, phase_other = 0;           // barrier phase of each half's next use
@@ -719,7 +737,7 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
 // stage those rows straight from the neighbour's input buffer (peer memory)
 // and publish completion -- the halo exchange is fused into the step.
 template <int K, int W, class T, bool kFast, bool kPerGrid, bool kPeer = false, bool kWrap = false>
-__global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T>::value)
+__global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T, W>::value)
     fhn_wavefront_kernel(const StepArgsT<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;

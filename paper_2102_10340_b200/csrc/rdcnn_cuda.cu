@@ -69,9 +69,14 @@ constexpr int kThreads = rdcnn_dev::kCtaThreads;  // threads per stencil CTA
 
 template <class T>
 struct Traits;
+#ifndef RDCNN_WIDE_F32
+// fp32 columns per lane of the wide instances.  8 was measured and rejected:
+// 212 registers -> 9 warps/SM, 507k vs 835k Mcell-updates/s at 4096^2.
+#define RDCNN_WIDE_F32 4
+#endif
 template <>
 struct Traits<float> {
-  static constexpr int kWide = 4;
+  static constexpr int kWide = RDCNN_WIDE_F32;
   static constexpr int kMaxLevels = 8;
 };
 template <>
