@@ -47,11 +47,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", default="cfg2", choices=("cfg2", "cfg5", "cfg1", "cfg3"),
+    ap.add_argument("--workload", default="cfg2", choices=("cfg2", "cfg5", "cfg1", "cfg3", "cfg4"),
                     help="cfg2 (default): a size x size torus per GPU, weak scaling; cfg5: ONE "
                          "size x size torus (default 32768) split over the N GPUs, strong scaling; "
                          "cfg1 (256^2 x 1000) / cfg3 (8192^2 image x 200): one lattice per GPU, "
-                         "independent replicas")
+                         "independent replicas; cfg4: the 64 x 64 (Du, Dv) sweep of 128^2 x 5000 "
+                         "lattices, one plane per GPU")
     ap.add_argument("--size", type=int, default=None,
                     help="cfg2: rows = cols per GPU (default 4096); cfg5: the lattice edge (32768)")
     ap.add_argument("--iters-per-step", type=int, default=None,
@@ -89,8 +90,21 @@ class Workload:
 
     def __init__(self, args, world: int):
         self.name = args.workload
-        self.replicas = self.name in ("cfg1", "cfg3")
-        if self.replicas:
+        self.replicas = self.name in ("cfg1", "cfg3", "cfg4")
+        self.batch = 1  # grids per GPU (cfg4: the sweep's cells)
+        if self.name == "cfg4":
+            n = args.size or 128
+            self.cols = self.rows_rank = self.rows_global = n
+            self.batch = 64 * 64
+            self.typ, self.gene7 = 1, DEFAULT_GENE7
+            self.iters = args.iters_per_step or 5000
+            self.e2e_steps, self.e2e_depth = 2, 1
+            self.scaling = "weak"
+            self.desc = (f"cfg4: FHN RD-CNN sweep of {self.batch} {n}x{n} fp32 tori per GPU, typ=1 seed 42, "
+                         "Du = linspace(0.02,0.70,64) x Dv = linspace(0.50,1.20,64) on the reference default "
+                         f"gene, {self.iters} iterations per step"
+                         + ("; independent planes, one per GPU" if world > 1 else ""))
+        elif self.replicas:
             n = args.size or (256 if self.name == "cfg1" else 8192)
             self.cols = self.rows_rank = self.rows_global = n
             self.typ, self.gene7 = (1 if self.name == "cfg1" else 3), DEFAULT_GENE7
@@ -132,9 +146,19 @@ class Workload:
             self.desc = (f"cfg2: FHN RD-CNN {n}x{n} fp32 torus per GPU, typ=1 seed 42, "
                          f"slow-growth gene a=-0.05, {self.iters} iterations per step")
 
+    def axes(self):
+        """cfg4's sweep axes: Du along x, Dv along y."""
+        import numpy as np
+        return list(np.linspace(0.02, 0.70, 64)), list(np.linspace(0.50, 1.20, 64))
+
     def gene(self, fhn):
         g = self.gene7
-        return fhn.Gene(dt=g[0], a=g[1], b=g[2], eps=g[3], c=g[4], Du=g[5], Dv=g[6])
+        base = fhn.Gene(dt=g[0], a=g[1], b=g[2], eps=g[3], c=g[4], Du=g[5], Dv=g[6])
+        if self.name != "cfg4":
+            return base
+        import dataclasses
+        xs, ys = self.axes()
+        return [dataclasses.replace(base, Du=float(x), Dv=float(y)) for y in ys for x in xs]
 
     def pixels(self):
         """cfg3 image: SURVEY §8d pattern (checker blocks 37x53 + a sine ramp), 8-bit."""
@@ -253,12 +277,35 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
+def ref_sweep_sample(wl: "Workload", ref, threads: int):
+    """cfg4 on the reference: its own sweep_grid with parallel_cells (OpenMP
+    over cells, sweep.hpp:293-295) on the first a x b cells of the plane, two
+    cells per host thread, the full iteration count.  Returns (cell-updates/s
+    in M, seconds, cells)."""
+    ref.set_threads(threads)
+    xs, ys = wl.axes()
+    want = max(4, 2 * threads)
+    a = min(len(xs), max(1, int(want ** 0.5)))
+    b = min(len(ys), max(1, -(-want // a)))
+    t0 = time.perf_counter()
+    ref.sweep_labels("du", xs[:a], "dv", ys[:b], gene7=wl.gene7, nn=wl.rows_global, nm=wl.cols,
+                     iter_max=wl.iters, nssp=5 if wl.iters % 5 == 0 else 1, seed=42, parallel_cells=True)
+    sec = time.perf_counter() - t0
+    return a * b * wl.rows_global * wl.cols * wl.iters / sec / 1e6, sec, a * b
+
+
 def cpu_baseline_sample(wl: "Workload", budget_s: float):
     """The reference's own parallel backend (oracle/_ref, reference headers
     compiled read-only) on a bounded prefix of the same workload."""
     from oracle.oracle import Reference
     ref = Reference()
     threads = host_threads()
+    if wl.name == "cfg4":
+        value, sec, ncells = ref_sweep_sample(wl, ref, threads)
+        return {"value": round(value, 2), "unit": "Mcell-updates/s", "cores": threads, "kind": "reference",
+                "sample": f"reference sweep_grid (oracle/_ref, parallel_cells, {threads} OpenMP threads) on "
+                          f"{ncells} cells of the plane, {wl.rows_global}x{wl.cols} x {wl.iters} iterations "
+                          f"each, snapshots + classifier included ({sec:.2f} s)"}
     R, C = wl.rows_global, wl.cols
     u, v = wl.ref_state(ref)
     # calibrate with 2 iterations, then size the sample to the budget
@@ -289,6 +336,33 @@ def cpu_model():
 # reference arm
 # ---------------------------------------------------------------------------
 
+def bench_reference_sweep(args, wl, ref, threads, world):
+    """cfg4 reference arm: each step = the reference sweep_grid on a bounded
+    sub-plane (two cells per host thread, full 128^2 x 5000 each)."""
+    for _ in range(args.warmup):
+        ref_sweep_sample(wl, ref, threads)
+    total, work = 0.0, 0.0
+    for _ in range(args.steps):
+        value, sec, ncells = ref_sweep_sample(wl, ref, threads)
+        total += sec
+        work += value * sec
+    value = work / total
+    sample = (f"reference sweep_grid (oracle/_ref, parallel_cells) on {ncells} cells of the plane per step, "
+              f"{wl.rows_global}x{wl.cols} x {wl.iters} iterations each, {threads} threads on {cpu_model()}")
+    line = {
+        "impl": "reference", "metric": "Mcell-updates/s", "value": round(value, 2),
+        "unit": "Mcell-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": wl.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl.desc, "rows": wl.rows_global, "cols": wl.cols, "grids": wl.batch},
+        "cpu_baseline": {"value": round(value, 2), "unit": "Mcell-updates/s", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": round(value, 2), "unit": "Mcell-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def bench_reference(args, rank, world):
     if rank != 0:
         return
@@ -297,6 +371,9 @@ def bench_reference(args, rank, world):
     ref = Reference()
     R, C = wl.rows_global, wl.cols  # the same global lattice our arm advances
     threads = host_threads()
+    if wl.name == "cfg4":
+        bench_reference_sweep(args, wl, ref, threads, world)
+        return
     u, v = wl.ref_state(ref)
     # size each step to ~2 s of CPU work so the whole run stays within minutes
     u, v, _, sec = ref.run_timed(R, C, u, v, 2, wl.gene7, backend="parallel", threads=threads)
@@ -357,8 +434,8 @@ def bench_ours(args, rank, world, local_rank):
 
     launches = 0
     if (world == 1 and not args.slab) or wl.replicas:
-        sim = fhn.Simulator(wl.rows_global, n, device=local_rank, mode=args.mode, levels=args.levels,
-                            seg_rows=args.seg_rows)
+        sim = fhn.Simulator(wl.rows_global, n, batch=wl.batch, device=local_rank, mode=args.mode,
+                            levels=args.levels, seg_rows=args.seg_rows)
         sim.set_params(gene)
         if wl.typ == 3:
             sim.init_image(wl.pixels(), 1.0)
@@ -370,23 +447,39 @@ def bench_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
+        # A state smaller than L2 (cfg1) would stay cached between steps: write
+        # a 256 MiB buffer before every step, outside its own timed events.
+        flush = (torch.empty(256 * 2**20, dtype=torch.uint8, device=f"cuda:{local_rank}")
+                 if 2 * 8 * wl.rows_rank * n * wl.batch <= 126e6 else None)
         with ClockSampler(local_rank) as clocks:
             ev0 = torch.cuda.Event(enable_timing=True)
             ev1 = torch.cuda.Event(enable_timing=True)
-            ev0.record(stream)
+            t_ms = 0.0
+            if flush is None:
+                ev0.record(stream)
             for _ in range(args.steps):
+                if flush is not None:
+                    flush.zero_()
+                    torch.cuda.synchronize()
+                    ev0.record(stream)
                 bad = sim.advance(S)
+                if flush is not None:
+                    ev1.record(stream)
+                    torch.cuda.synchronize()
+                    t_ms += ev0.elapsed_time(ev1)
                 launches += sim.launch_count()
-                if bad[0]:
-                    raise RuntimeError(f"blow-up at iteration {bad[0]}")
-            ev1.record(stream)
-            torch.cuda.synchronize()
-        t = torch.tensor([ev0.elapsed_time(ev1)], device=red_dev)
+                if bad.any():
+                    raise RuntimeError(f"blow-up at iteration {int(bad[bad > 0].min())}")
+            if flush is None:
+                ev1.record(stream)
+                torch.cuda.synchronize()
+                t_ms = ev0.elapsed_time(ev1)
+        t = torch.tensor([t_ms], device=red_dev)
         if dist is not None:  # replicas: the job takes as long as its slowest GPU
             dist.barrier()
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
-        cells_global = wl.rows_global * n * (world if wl.replicas else 1)
+        cells_global = wl.rows_global * n * wl.batch * (world if wl.replicas else 1)
     else:
         from paper_2102_10340_b200.slab import SlabStepper
         rows_global = wl.rows_global
@@ -429,7 +522,7 @@ def bench_ours(args, rank, world, local_rank):
 
     # ---- roofline of the dominant kernel (the K-level wavefront stencil) ----
     peaks, peak_kind = measured_peaks()
-    per_rank_cells = wl.rows_rank * n
+    per_rank_cells = wl.rows_rank * n * wl.batch
     use_slab = (world > 1 or args.slab) and not wl.replicas
     transport = slab.transport if use_slab else None
     levels = args.levels
@@ -462,7 +555,47 @@ def bench_ours(args, rank, world, local_rank):
     # ---- end to end through the public API with host buffers (N=1 only) ----
     e2e = None
     e2e_steps = args.e2e_steps or wl.e2e_steps
-    if not use_slab:
+    if wl.name == "cfg4":
+        # The whole sweep through the public API: the cells' initial states
+        # uploaded from pinned host memory, S iterations with nssp=5 device
+        # snapshots, the regime classifier on the device, the cells' final u
+        # planes and labels back to the host (paper_2102_10340_b200.sweep.sweep_grid).
+        from paper_2102_10340_b200.sweep import SweepSpec, sweep_grid
+        cells = wl.rows_global * n
+        u_in = torch.empty(wl.batch, cells, dtype=torch.float32).pin_memory()
+        v_in = torch.empty(wl.batch, cells, dtype=torch.float32).pin_memory()
+        st = fhn.init_center_square(wl.rows_global, n, 42)
+        u_in[:] = torch.from_numpy(st.u)
+        v_in[:] = torch.from_numpy(st.v)
+        xs, ys = wl.axes()
+        g7 = wl.gene7
+        spec = SweepSpec(x_param="du", x_values=xs, y_param="dv", y_values=ys,
+                         base_gene=fhn.Gene(dt=g7[0], a=g7[1], b=g7[2], eps=g7[3], c=g7[4], Du=g7[5], Dv=g7[6]),
+                         base_config=fhn.RunConfig(init_mode=1, nn=wl.rows_global, nm=n, iter_max=S,
+                                                   nssp=5 if S % 5 == 0 else 1, seed=42))
+        sim.close()  # the sweep makes its own batched handle
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            res = sweep_grid(spec, device=local_rank, levels=args.levels, initial=(u_in.numpy(), v_in.numpy()))
+        torch.cuda.synchronize()
+        te = torch.tensor([time.perf_counter() - t0], device=red_dev)
+        if dist is not None:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        e2e = {"value": round(cells * wl.batch * world * S * e2e_steps / e2e_s / 1e6, 2),
+               "unit": "Mcell-updates/s", "h2d_bytes_per_step": 2 * 4 * cells * wl.batch * world,
+               "d2h_bytes_per_step": (4 * cells * wl.batch + 8 * wl.batch + len(res.labels_csv)) * world,
+               "path": "paper_2102_10340_b200.sweep.sweep_grid(spec, initial=host states): upload, advance with "
+                       "nssp device snapshots, device classifier statistics and digests, the cells' final u "
+                       "planes (what the reference keeps per cell, sweep.hpp:318) + labels CSV back"
+                       + ("; per rank, max wall time over ranks" if world > 1 else ""),
+               "steps": e2e_steps, "lattices_in_flight": wl.batch}
+        if any(c.blew_up for c in res.cells):
+            raise RuntimeError("blow-up in the cfg4 sweep")
+    elif not use_slab:
         # A stream of independent lattices through the public Pipeline API:
         # each one is uploaded from pinned host memory, advanced S iterations
         # and downloaded; with depth 2 one lattice's copies overlap another's
@@ -565,7 +698,9 @@ def bench_ours(args, rank, world, local_rank):
                 "mode": args.mode,
                 "l2": (f"double-buffered state {2 * 8 * per_rank_cells / 2**20:.0f} MiB/GPU "
                        + ("> 126 MB L2 (no flush needed)" if 2 * 8 * per_rank_cells > 126e6
-                          else "fits in L2: small-size run, not a reported number")),
+                          else "fits in L2: a 256 MiB buffer is written before every step, each step "
+                               "timed on its own")),
+                **({"grids": wl.batch} if wl.batch > 1 else {}),
                 "parallelism": (f"slab{world}" if use_slab else f"replicas{world}" if world > 1 else "single"),
                 **({"transport": transport} if use_slab else {}),
             },

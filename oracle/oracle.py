@@ -153,6 +153,11 @@ class Reference:
     def max_threads(self) -> int:
         return int(self.L.ref_max_threads())
 
+    def set_threads(self, n: int) -> None:
+        """OpenMP threads for the reference's regions without an explicit count
+        (the parallel_cells sweep loop); torchrun presets OMP_NUM_THREADS=1."""
+        self.L.ref_set_threads(int(n))
+
     def init(self, typ: int, rows: int, cols: int, seed: int):
         u = np.zeros(rows * cols, np.float32)
         v = np.zeros(rows * cols, np.float32)

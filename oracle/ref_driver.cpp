@@ -262,6 +262,16 @@ int ref_init_image_f32(const char* path, double ka, int* rows, int* cols, float*
   }
 }
 
+/* OpenMP threads for the reference's own parallel regions that take no
+ * explicit count (sweep.hpp:293 parallel_cells); torchrun presets 1. */
+void ref_set_threads(int n) {
+#if defined(_OPENMP)
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 int ref_max_threads(void) {
 #if defined(_OPENMP)
   return omp_get_max_threads();

@@ -138,12 +138,6 @@ def validate_sweep_spec(spec: SweepSpec):
         raise ValueError("sweep value lists must be non-empty")
 
 
-def _set(g: Gene, name: str, value: float) -> Gene:
-    g = dataclasses.replace(g)
-    setattr(g, GENE_FIELDS[name], float(value))
-    return g
-
-
 def classify(frame_mins, frame_maxs, counts, cells: int, cc: ClassifierConfig, final_range: float) -> RegimeResult:
     """classify_outcome (sweep.hpp:77-112) from per-frame statistics."""
     res = RegimeResult()
@@ -168,10 +162,12 @@ def classify(frame_mins, frame_maxs, counts, cells: int, cc: ClassifierConfig, f
 def labels_csv(res: SweepResult) -> str:
     """sweep.hpp:227-247."""
     out = ["x_value,y_value,label,final_range,final_active_fraction,checksum\n"]
+    xs = [format_double(x) for x in res.x_values]  # each axis value formatted once
+    ys = [format_double(y) for y in res.y_values]
     for yi in range(len(res.y_values)):
         for xi in range(len(res.x_values)):
             c = res.at(yi, xi)
-            line = f"{format_double(c.x_value)},{format_double(c.y_value)},{c.outcome.label},"
+            line = f"{xs[xi]},{ys[yi]},{c.outcome.label},"
             if c.blew_up:
                 out.append(line + ",,\n")
                 continue
@@ -181,7 +177,7 @@ def labels_csv(res: SweepResult) -> str:
 
 
 def _run_cells(cells: List[SweepCell], idx0: int, spec: SweepSpec, base: RunConfig,
-               image: Optional[np.ndarray], device: int, levels: int) -> None:
+               image: Optional[np.ndarray], device: int, levels: int, initial=None) -> None:
     """Runs `cells` (global indices idx0..) as one batched handle on `device`
     and fills in their outcomes (sweep.hpp:296-326)."""
     B, rows, cols = len(cells), base.nn, base.nm
@@ -192,7 +188,10 @@ def _run_cells(cells: List[SweepCell], idx0: int, spec: SweepSpec, base: RunConf
     sim.set_params([c.gene for c in cells])
     # initial states (init.hpp:67-82); the shared-seed default runs on the device
     sweeps_ka = "ka" in (spec.x_param, spec.y_param)
-    if base.init_mode in (1, 2) and not spec.per_cell_seed:
+    if initial is not None:  # caller-supplied states, cells idx0.. of a (cells, rows*cols) pair
+        u0, v0 = initial
+        sim.upload(u0[idx0:idx0 + B], v0[idx0:idx0 + B])
+    elif base.init_mode in (1, 2) and not spec.per_cell_seed:
         sim.init(base.init_mode, base.seed)
     elif base.init_mode == 3 and not sweeps_ka:
         sim.init_image(image, spec.base_gene.ka)
@@ -233,26 +232,30 @@ def _run_cells(cells: List[SweepCell], idx0: int, spec: SweepSpec, base: RunConf
     thr = spec.classifier.activity_rel * final_range
     counts = np.stack([sim.frame_active(f, meds[f], thr) for f in range(F)])  # [F, B]
     digests = sim.checksums()  # per grid, on the device
-    fu, fv = sim.download()
-    fu = fu.reshape(B, -1)
-    fv = fv.reshape(B, -1)
+    # The cells keep their final u plane (sweep.hpp:318): the last snapshot
+    # slot holds exactly it, so only u comes back, and each cell gets a view.
     frames_u = [sim.frame_download(f).reshape(B, -1) for f in range(F)] if spec.keep_buffers else None
+    fu = frames_u[-1] if frames_u is not None else sim.frame_download(F - 1).reshape(B, -1)
     for idx, c in enumerate(cells):
         if c.blew_up:
             continue
         c.outcome = classify(mins[:, idx], maxs[:, idx], counts[:, idx], rows * cols, spec.classifier,
                              float(final_range[idx]))
         c.digest = int(digests[idx])
-        c.final_u = fu[idx].copy()
+        c.final_u = fu[idx]
         if frames_u is not None:
-            c.buffer = [fr[idx].copy() for fr in frames_u]
+            c.buffer = [fr[idx] for fr in frames_u]
     sim.close()
 
 
 def sweep_grid(spec: SweepSpec, image: Optional[np.ndarray] = None, device: int = 0,
-               levels: int = 4, devices: Optional[List[int]] = None) -> SweepResult:
+               levels: int = 4, devices: Optional[List[int]] = None, initial=None) -> SweepResult:
     """sweep_grid (sweep.hpp:255-326) as one batched device run, or with
-    `devices`, the cells split in contiguous chunks over several GPUs."""
+    `devices`, the cells split in contiguous chunks over several GPUs.
+
+    ``initial``: optional (u, v) host arrays of shape (cells, rows*cols), the
+    cells' initial states in sweep order (y outer, x inner), uploaded instead
+    of drawing them from the seed (e.g. to sweep from an evolved state)."""
     validate_sweep_spec(spec)
     base = dataclasses.replace(spec.base_config)
     issues = validate_config(base, spec.base_gene)
@@ -267,26 +270,33 @@ def sweep_grid(spec: SweepSpec, image: Optional[np.ndarray] = None, device: int 
             raise ValueError("typ=3 requires an image")
         base.nn, base.nm = int(image.shape[0]), int(image.shape[1])
     cells: List[SweepCell] = []
+    fx, fy = GENE_FIELDS[spec.x_param], GENE_FIELDS[spec.y_param]
     for y in spec.y_values:
         for x in spec.x_values:
-            g = _set(_set(spec.base_gene, spec.x_param, x), spec.y_param, y)
+            g = dataclasses.replace(spec.base_gene, **{fx: float(x), fy: float(y)})
             if not gene_valid(g):
                 raise ValueError(f"sweep cell gene invalid at {spec.x_param}={format_double(x)} "
                                  f"{spec.y_param}={format_double(y)}")
             cells.append(SweepCell(x_value=float(x), y_value=float(y), gene=g))
 
+    if initial is not None:
+        n = len(spec.x_values) * len(spec.y_values)
+        u0, v0 = (np.asarray(a).reshape(n, -1) for a in initial)
+        if u0.shape[1] != base.nn * base.nm or v0.shape != u0.shape:
+            raise ValueError(f"initial states must be ({n}, {base.nn * base.nm}) arrays")
+        initial = (u0, v0)
     devs = list(devices) if devices else [device]
     bounds = np.linspace(0, len(cells), len(devs) + 1).astype(int)
     jobs = [(cells[lo:hi], int(lo), dev) for lo, hi, dev in zip(bounds[:-1], bounds[1:], devs) if hi > lo]
     if len(jobs) == 1:
-        _run_cells(jobs[0][0], jobs[0][1], spec, base, image, jobs[0][2], levels)
+        _run_cells(jobs[0][0], jobs[0][1], spec, base, image, jobs[0][2], levels, initial)
     elif jobs:
         # Replicas only: independent cells, no exchange; the C-ABI
         # calls release the GIL, so the devices advance concurrently.
         from concurrent.futures import ThreadPoolExecutor
 
         with ThreadPoolExecutor(len(jobs)) as ex:
-            list(ex.map(lambda j: _run_cells(j[0], j[1], spec, base, image, j[2], levels), jobs))
+            list(ex.map(lambda j: _run_cells(j[0], j[1], spec, base, image, j[2], levels, initial), jobs))
     rows, cols = base.nn, base.nm
     res = SweepResult(list(spec.x_values), list(spec.y_values), spec.x_param, spec.y_param, rows, cols, cells)
     res.labels_csv = labels_csv(res)

@@ -129,3 +129,22 @@ def test_sweep_split_over_devices_identical(per_cell_seed):
     assert [c.digest for c in split.cells] == [c.digest for c in one.cells]
     assert [c.blowup_iteration for c in split.cells] == [c.blowup_iteration for c in one.cells]
     assert any(c.blew_up for c in one.cells)
+
+
+@pytest.mark.gpu
+def test_sweep_from_supplied_initial_states():
+    """sweep_grid(initial=(u, v)): uploading exactly the states the seed would
+    draw gives the reference's labels CSV byte for byte; other states change it."""
+    case = golden_sweeps()[0]
+    spec = spec_from(case["spec"])
+    d = case["spec"]
+    n = len(d["xs"]) * len(d["ys"])
+    st = fhn.init_center_square(d["nn"], d["nm"], d.get("seed", 42))
+    u = np.tile(st.u, (n, 1))
+    v = np.tile(st.v, (n, 1))
+    assert sweep_grid(spec, initial=(u, v)).labels_csv == case["labels_csv"]
+    u2 = u.copy()
+    u2[:, :] = fhn.init_full_random(d["nn"], d["nm"], 5).u
+    assert sweep_grid(spec, initial=(u2, v)).labels_csv != case["labels_csv"]
+    with pytest.raises(ValueError):
+        sweep_grid(spec, initial=(u[:, :-1], v[:, :-1]))

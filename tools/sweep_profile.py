@@ -23,7 +23,7 @@ def timed(name, fn):
 
 
 for name in ("advance", "frame_capture", "frame_stats", "frame_active", "download", "init", "set_params",
-             "frames_reserve", "frame_download"):
+             "frames_reserve", "frame_download", "upload", "__init__", "close"):
     setattr(Simulator, name, timed(name, getattr(Simulator, name)))
 sw.classify = timed("classify", sw.classify)
 for name in ("checksums",):
@@ -36,9 +36,11 @@ cfg.iter_max = 5000
 cfg.nssp = 5
 spec = sw.SweepSpec("du", list(np.linspace(0.02, 0.70, side)), "dv", list(np.linspace(0.50, 1.20, side)),
                     base_config=cfg)
-t0 = time.perf_counter()
-res = sw.sweep_grid(spec)
-wall = time.perf_counter() - t0
+for rep in range(2):  # the second sweep is the one reported (first-use costs excluded)
+    T.clear()
+    t0 = time.perf_counter()
+    res = sw.sweep_grid(spec)
+    wall = time.perf_counter() - t0
 labels = {}
 for c in res.cells:
     labels[c.outcome.label] = labels.get(c.outcome.label, 0) + 1
