@@ -110,11 +110,12 @@ class Workload:
             self.typ, self.gene7 = (1 if self.name == "cfg1" else 3), DEFAULT_GENE7
             self.iters = args.iters_per_step or (1000 if self.name == "cfg1" else 200)
             self.e2e_steps = 20 if self.name == "cfg1" else 12
-            # cfg3 is edge detection over a stream of independent images: two
-            # in flight, one's copies overlapping the other's advance.  Every
-            # other workload is one evolving lattice whose steps depend on each
+            # cfg3 is edge detection over a stream of independent images:
+            # three in flight, so one's upload and another's download overlap
+            # a third's advance (depth 2/3/4: 637k/798k/805k).  Every other
+            # workload is one evolving lattice whose steps depend on each
             # other, so its e2e runs them strictly one after another.
-            self.e2e_depth = 2 if self.name == "cfg3" else 1
+            self.e2e_depth = 3 if self.name == "cfg3" else 1
             self.scaling = "weak"
             self.desc = (f"{self.name}: FHN RD-CNN {n}x{n} fp32 torus per GPU, "
                          + ("typ=1 seed 42" if self.typ == 1 else "typ=3 synthetic 8-bit image (SURVEY §8d)")

@@ -59,11 +59,11 @@ def test_our_arm_slab_contract():
 
 @pytest.mark.gpu
 def test_our_arm_image_stream_e2e():
-    """cfg3 (edge detection over a stream of images): the e2e runs two images in
-    flight through engine.Pipeline; cfg2 (one evolving lattice) runs one."""
+    """cfg3 (edge detection over a stream of images): the e2e runs three images
+    in flight through engine.Pipeline; cfg2 (one evolving lattice) runs one."""
     d = run_bench("--workload", "cfg3", "--size", "512", "--steps", "2", "--warmup", "3",
                   "--iters-per-step", "20", "--no-cpu-baseline", "--e2e-steps", "4")
-    assert d["e2e"]["lattices_in_flight"] == 2 and d["e2e"]["steps"] == 4 and d["e2e"]["value"] > 0
+    assert d["e2e"]["lattices_in_flight"] == 3 and d["e2e"]["steps"] == 4 and d["e2e"]["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 2 * 4 * 512 * 512
     d = run_bench("--size", "512", "--steps", "2", "--warmup", "3", "--iters-per-step", "40",
                   "--no-cpu-baseline", "--e2e-steps", "2")
