@@ -147,6 +147,16 @@ class Workload:
             self.desc = (f"cfg2: FHN RD-CNN {n}x{n} fp32 torus per GPU, typ=1 seed 42, "
                          f"slow-growth gene a=-0.05, {self.iters} iterations per step")
 
+    def published(self):
+        """the paper's fastest published implementation of this
+        step (PyCUDA on a Tesla P100, 10 000 iterations, Mcells/s) at this
+        lattice edge, or None when it publishes none at this size."""
+        table = {256: 1941.0, 512: 7581.0, 1024: 13059.0, 2048: 14198.0, 4096: 14545.0}
+        if self.name in ("cfg2", "cfg1") and self.cols in table and self.rows_rank == self.cols:
+            return table[self.cols], (f"PyCUDA {self.cols}^2 x 10000 iterations on a Tesla P100-PCIE, "
+                                      f"{table[self.cols]:.0f} Mcells/s (BASELINE.md §1, PAPER.md:271-274)")
+        return None, None
+
     def axes(self):
         """cfg4's sweep axes: Du along x, Dv along y."""
         import numpy as np
@@ -682,12 +692,15 @@ def bench_ours(args, rank, world, local_rank):
             cpu = {"value": None, "unit": "Mcell-updates/s", "cores": None, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    published, vs_basis = wl.published()
+    vs_baseline = round(value / published, 2) if published else None
     if rank == 0:
         line = {
             "metric": "Mcell-updates/s", "value": round(value, 2), "unit": "Mcell-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t_ms / args.steps, 3), "higher_is_better": True,
-            "scaling": wl.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": wl.scaling, "vs_baseline": vs_baseline, "dtype": "f32", "data": "synthetic",
+            **({"vs_baseline_basis": vs_basis} if vs_basis else {}),
             "config": {
                 "workload": (wl.desc
                              + (f"; global {wl.rows_global}x{n} row-slabbed ({wl.rows_rank} rows per "
