@@ -180,6 +180,58 @@ __device__ __forceinline__ void cluster_row(const float (&uu)[W], const float (&
   }
 }
 
+// Strict cell update (fhn_cell) split at the exchange wait: the part that
+// needs only the warp's own rows -- the row's left/right sum, plus the row
+// below when it is the warp's own, and both reaction terms -- runs before
+// the wait; the rest after it.  Same operations in the same order
+// (kernels.hpp:63-72, model.hpp:37-56), so bit-identical to fhn_cell.
+struct EdgePre {
+  float su, sv, f1, f2;
+};
+
+template <bool kDnOwn>
+__device__ __forceinline__ void cell_pre(float uc, float vc, float ur, float ul, float vr, float vl, float ud,
+                                         float vd, const ParamsT<float>& p, float neg_eps, EdgePre& e) {
+  e.su = add_rn(ur, ul);
+  e.sv = add_rn(vr, vl);
+  if constexpr (kDnOwn) {
+    e.su = add_rn(e.su, ud);
+    e.sv = add_rn(e.sv, vd);
+  }
+  e.f1 = sub_rn(mul_rn(uc, sub_rn(p.c, div3_rn(mul_rn(uc, uc)))), vc);
+  e.f2 = mul_rn(neg_eps, add_rn(sub_rn(uc, mul_rn(p.b, vc)), p.a));
+}
+
+template <bool kDnOwn>
+__device__ __forceinline__ void cell_post(float uc, float vc, float ud, float vd, float uu, float vu,
+                                          const EdgePre& e, const ParamsT<float>& p, float& un, float& vn) {
+  float su = e.su, sv = e.sv;
+  if constexpr (!kDnOwn) {
+    su = add_rn(su, ud);
+    sv = add_rn(sv, vd);
+  }
+  const float lap_u = fma_rn(-4.0f, uc, add_rn(su, uu));  // as fhn_cell: exact when 4*uc is finite
+  const float lap_v = sub_rn(add_rn(sv, vu), mul_rn(4.0f, vc));
+  un = add_rn(uc, mul_rn(p.dt, add_rn(e.f1, mul_rn(p.du, lap_u))));
+  vn = add_rn(vc, mul_rn(p.dt, add_rn(e.f2, mul_rn(p.dv, lap_v))));
+}
+
+// Pre-wait half of one edge row: left/right by shuffles, as cluster_row.
+template <int W, bool kDnOwn>
+__device__ __forceinline__ void edge_pre(const float (&uc)[W], const float (&vc)[W], const float (&ud)[W],
+                                         const float (&vd)[W], EdgePre (&e)[W], const ParamsT<float>& p,
+                                         float neg_eps, int lane_l, int lane_r) {
+  const float ul = __shfl_sync(kFull, uc[W - 1], lane_l);
+  const float ur = __shfl_sync(kFull, uc[0], lane_r);
+  const float vl = __shfl_sync(kFull, vc[W - 1], lane_l);
+  const float vr = __shfl_sync(kFull, vc[0], lane_r);
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    cell_pre<kDnOwn>(uc[k], vc[k], k < W - 1 ? uc[k + 1] : ur, k > 0 ? uc[k - 1] : ul, k < W - 1 ? vc[k + 1] : vr,
+                     k > 0 ? vc[k - 1] : vl, ud[k], vd[k], p, neg_eps, e[k]);
+  }
+}
+
 // W columns per lane, RW consecutive rows per warp, R = warps * RW rows per CTA.
 template <int RW>
 struct ClusterThreads {  // launch bound: 4-row warps keep ~200 registers
@@ -273,10 +325,34 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
       cluster_row<W, kFast>(u[r - 1], v[r - 1], u[r], v[r], u[r + 1], v[r + 1], un[r], vn[r], p, neg_eps, lane_l,
                             lane_r);
     const unsigned phase = (unsigned)((done >> 1) & 1);
+    // 2b. strict mode: the edge rows' own-row half before the wait
+    EdgePre e_top[W], e_bot[W];
+    if constexpr (!kFast) {
+      if constexpr (RW == 1) {
+        edge_pre<W, false>(u[0], v[0], u[0], v[0], e_top, p, neg_eps, lane_l, lane_r);
+      } else {
+        edge_pre<W, true>(u[0], v[0], u[1], v[1], e_top, p, neg_eps, lane_l, lane_r);
+        edge_pre<W, false>(u[RW - 1], v[RW - 1], u[RW - 1], v[RW - 1], e_bot, p, neg_eps, lane_l, lane_r);
+      }
+    }
     mbar_wait_parity_cta(lb, phase);
     if (cta_first || cta_last) mbar_wait_parity(mb, phase);
     // 3. edge rows with the neighbours' rows from shared memory
-    {
+    if constexpr (!kFast) {
+      float ua[W], va[W], ub[W], vb[W];
+      read_row<W>(above + par, ua, va);
+      read_row<W>(below + par, ub, vb);
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        if constexpr (RW == 1) {
+          cell_post<false>(u[0][k], v[0][k], ub[k], vb[k], ua[k], va[k], e_top[k], p, un[0][k], vn[0][k]);
+        } else {
+          cell_post<true>(u[0][k], v[0][k], 0.0f, 0.0f, ua[k], va[k], e_top[k], p, un[0][k], vn[0][k]);
+          cell_post<false>(u[RW - 1][k], v[RW - 1][k], ub[k], vb[k], u[RW - 2][k], v[RW - 2][k], e_bot[k], p,
+                           un[RW - 1][k], vn[RW - 1][k]);
+        }
+      }
+    } else {
       float ua[W], va[W], ub[W], vb[W];
       read_row<W>(above + par, ua, va);
       read_row<W>(below + par, ub, vb);
