@@ -48,6 +48,8 @@ def test_our_arm_contract():
     assert d["e2e"]["h2d_bytes_per_step"] == 2 * 4 * 512 * 512 and d["e2e"]["value"] > 0
     assert d["gpu_launches"] > 0 and "sm_mhz" in d["clocks"]
     assert d["config"]["workload"].startswith("cfg2")
+    # BASELINE.md §1 publishes PyCUDA/P100 at N=512 (7581 Mcells/s): vs_baseline is value / that
+    assert d["vs_baseline"] == pytest.approx(d["value"] / 7581.0, rel=1e-3) and "P100" in d["vs_baseline_basis"]
 
 
 @pytest.mark.gpu
