@@ -585,6 +585,10 @@ def bench_ours(args, rank, world, local_rank):
                          base_config=fhn.RunConfig(init_mode=1, nn=wl.rows_global, nm=n, iter_max=S,
                                                    nssp=5 if S % 5 == 0 else 1, seed=42))
         sim.close()  # the sweep makes its own batched handle
+        # One untimed sweep: the batched handle it creates (device state and
+        # snapshot frames) is kept for the next sweep of the same shape, as
+        # every other e2e here runs on warmed handles.
+        sweep_grid(spec, device=local_rank, levels=args.levels, initial=(u_in.numpy(), v_in.numpy()))
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
@@ -628,9 +632,9 @@ def bench_ours(args, rank, world, local_rank):
         pipe = fhn.Pipeline(wl.rows_global, n, depth=depth, sims=[sim], device=local_rank, mode=args.mode,
                             levels=args.levels, seg_rows=args.seg_rows)
         pipe.set_params(gene)
-        for extra in pipe.sims[1:]:  # first-use costs of the new handles stay out of the timed region
+        for extra in pipe.sims[1:]:  # first-use costs (incl. the graph capture) stay out of the timed region
             extra.upload_ptr(u_in.data_ptr(), v_in.data_ptr())
-            extra.advance(min(S, 64))
+            extra.advance(S)
         jobs = [(u_in.data_ptr(), v_in.data_ptr(), outs[i % depth][0].data_ptr(), outs[i % depth][1].data_ptr())
                 for i in range(e2e_steps)]
         torch.cuda.synchronize()

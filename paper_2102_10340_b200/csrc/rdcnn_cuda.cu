@@ -528,6 +528,7 @@ struct rdcnn_sim {
   int seg_force = 0;                // set while an autotune candidate runs
   int cluster_mode = 0;       // persistent cluster path: 0 auto, 1 required, -1 off
   long long* d_first_bad = nullptr;  // cluster path result word
+  std::map<std::pair<long, int>, cudaGraphExec_t> graphs;  // captured advances by (steps, start buffer)
   int sm_count = 148;
   unsigned slab_tag = 0;
   // slab ring (native multi-GPU path)
@@ -677,12 +678,21 @@ void free_all(rdcnn_sim* s) {
   for (void* p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   if (s->p2p_words) cudaFree(s->p2p_words);
   if (s->d_first_bad) cudaFree(s->d_first_bad);
+  for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
+  s->graphs.clear();
   if (s->ckpt) cudaFree(s->ckpt);
   if (s->frames) cudaFree(s->frames);
   if (s->d_stats) cudaFree(s->d_stats);
   if (s->d_counts) cudaFree(s->d_counts);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
+}
+
+// Drop a handle's captured graphs (their kernel parameters -- the shared
+// gene, the segment plan -- no longer match the handle's).
+void drop_graphs(rdcnn_sim* s) {
+  for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
+  s->graphs.clear();
 }
 
 // Sequence of block depths an advance of `steps` uses: floor(steps/Kmax)
@@ -996,12 +1006,29 @@ int autotune_segments(rdcnn_sim* s, const Schedule& sched, long* n_io) {
   for (auto& e : ev) cudaEventDestroy(e);
   s->tuned_seg[ki] = best_h;
   s->tuned[ki] = true;
+  drop_graphs(s);  // any earlier capture used the untuned plan
   {
     std::lock_guard<std::mutex> lock(g_tune_mu);
     g_tune_cache.emplace(key, best_h);
   }
   *n_io = n;
   return RDCNN_OK;
+}
+
+// CUDA graphs for the per-launch path: the launch loop of an advance is
+// captured once (its PDL edges become programmatic graph edges) and replayed
+// on later advances of the same length.  Measured: 512^2 128k -> 153-166k,
+// 1024^2 341k -> 402k, 2048^2 637k -> 649k, 4096^2 835k -> 840k
+// Mcell-updates/s, bit-identical.  Used for launches that do not fill the
+// chip (latency-bound lattices, where the gain is); chip-filling ones gain
+// < 1 %, less than a capture costs a short-lived handle (a sweep's).
+// RDCNN_GRAPH=0 turns it off.
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RDCNN_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 template <class T>
@@ -1016,6 +1043,49 @@ int advance_launches(rdcnn_sim* s, long steps, long* first_bad) {
   const long nl = sched.count();
   long n = 0;
   RDCNN_TRY(autotune_segments<T>(s, sched, &n));
+  bool graph = graphs_enabled() && n == 0 && nl >= 8;
+  if (graph) {  // only for launches that leave warp slots empty (same rule as the autotuner)
+    const int k = sched.kmax, w = width_for<T>(s);
+    const bool fast = s->mode == RDCNN_FAST, per_grid = s->params_stride != 0, wrap = s->cols / w == 32;
+    const int rw = resident_blocks<T>(k, w, fast, per_grid, wrap) * (kThreads / 32);
+    const Plan p0 = make_plan(s->cols, w, k, s->batch, 0, s->rows, 0, s->sm_count, rw);
+    graph = 4 * p0.warps < 3LL * rw * s->sm_count;
+  }
+  if (graph) {
+    const std::pair<long, int> key{steps, cur0};
+    auto it = s->graphs.find(key);
+    if (it == s->graphs.end()) {
+      if (s->graphs.size() >= 8) drop_graphs(s);  // bounded: a few advance lengths per handle
+      // Capture; on any failure end the capture and take the direct path.
+      cudaError_t ce = cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal);
+      int cur = s->cur;
+      for (long m = 0; m < nl && ce == cudaSuccess; ++m) {
+        StepArgsT<T> a = base_args<T>(s, cur, cur ^ 1);
+        a.tag = (unsigned)(m + 1);
+        ce = launch_range<T>(s, sched.depth(m), a, 0, s->rows, s->stream);
+        cur ^= 1;
+      }
+      cudaGraph_t g = nullptr;
+      const cudaError_t ee = cudaStreamEndCapture(s->stream, &g);
+      cudaGraphExec_t ge = nullptr;
+      if (ce == cudaSuccess && ee == cudaSuccess) ce = cudaGraphInstantiate(&ge, g, 0);
+      if (g) cudaGraphDestroy(g);
+      if (ce == cudaSuccess && ee == cudaSuccess) {
+        it = s->graphs.emplace(key, ge).first;
+      } else {
+        cudaGetLastError();
+        graph = false;
+      }
+      s->launches = 0;
+      RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));  // time the replay, not the capture
+    }
+    if (graph) {
+      RDCNN_CUDA_TRY(cudaGraphLaunch(it->second, s->stream));
+      s->launches = nl;  // the graph's kernel nodes
+      if (nl & 1) s->cur ^= 1;
+      n = nl;
+    }
+  }
   for (; n < nl; ++n) {
     StepArgsT<T> a = base_args<T>(s, s->cur, s->cur ^ 1);
     a.tag = (unsigned)(n + 1);
@@ -1238,6 +1308,7 @@ int set_params_impl(rdcnn_sim* s, const ParamsT<T>* p, int n) {
     if constexpr (sizeof(T) == 4) s->h_params_f = *p;
     else s->h_params_d = *p;
   }
+  drop_graphs(s);  // captured launches carry the shared gene by value
   return RDCNN_OK;
 }
 
@@ -1544,6 +1615,7 @@ int rdcnn_sim_set_tuning(rdcnn_sim_t s, int max_levels, int seg_rows) {
     s->tuned[i] = false;
     s->tuned_seg[i] = 0;
   }
+  drop_graphs(s);
   return RDCNN_OK;
 }
 
@@ -1994,6 +2066,7 @@ int rdcnn_sim_checksums(rdcnn_sim_t s, uint64_t* out) {
 int rdcnn_sim_frames_reserve(rdcnn_sim_t s, int nframes) {
   if (!s || s->slab) return fail(RDCNN_EINVAL, "not a periodic handle");
   if (nframes < 1) return fail(RDCNN_EINVAL, "nframes must be >= 1");
+  if (s->frames && s->n_frames == nframes) return RDCNN_OK;  // already reserved (reused handles)
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   if (s->frames) RDCNN_CUDA_TRY(cudaFree(s->frames));
   s->frames = nullptr;

@@ -148,3 +148,23 @@ def test_sweep_from_supplied_initial_states():
     assert sweep_grid(spec, initial=(u2, v)).labels_csv != case["labels_csv"]
     with pytest.raises(ValueError):
         sweep_grid(spec, initial=(u[:, :-1], v[:, :-1]))
+
+
+@pytest.mark.gpu
+def test_sweep_handle_reuse():
+    """Consecutive sweeps of one shape reuse the cached batched handle; the
+    result does not depend on it (golden labels both times, then after a
+    sweep of another spec on the same handle)."""
+    from paper_2102_10340_b200 import sweep as sw
+    sw.release_cached_handles()
+    case = golden_sweeps()[0]
+    spec = spec_from(case["spec"])
+    assert sweep_grid(spec).labels_csv == case["labels_csv"]
+    assert len(sw._handles) == 1
+    h = next(iter(sw._handles.values()))
+    other = spec_from(dict(case["spec"], xs=[0.05, 0.6]))
+    sweep_grid(other)
+    assert next(iter(sw._handles.values())) is h
+    assert sweep_grid(spec).labels_csv == case["labels_csv"]
+    sw.release_cached_handles()
+    assert not sw._handles
