@@ -2,7 +2,8 @@
 racecheck / synccheck): wavefront K=1/2/4/8 at W=1/4 (odd and full-width
 shapes), batch with per-grid genes, fp64, fast mode, blow-up replay, the
 fused peer-ring slab (world 1), the cluster kernel (incl. its rows-per-warp
-trials), concurrent handles from host threads (engine.Pipeline), device
+trials), CUDA-graph capture and replay, concurrent handles from host threads
+(engine.Pipeline), device
 checksums and frame analysis."""
 import sys
 
@@ -41,6 +42,10 @@ with fhn.Simulator(64, 128, persistent=1) as s:  # cluster path blow-up + re-run
     s.set_params(fhn.Gene(dt=100.0))
     s.init(2, 9)
     s.advance(20)
+with fhn.Simulator(96, 96, persistent=-1) as s:  # CUDA-graph capture, then replay (under-filled launches)
+    s.init(2, 4)
+    s.advance(64)
+    s.advance(64)
 with fhn.Simulator(64, 128, persistent=1) as s:  # cluster rows-per-warp trials (>= 4 x 128 steps)
     s.init(2, 9)
     s.advance(520)
