@@ -761,3 +761,27 @@ def test_cluster_rows_per_warp_tuning_exact(dt, want_bad):
         assert int(launches) >= 4  # three 128-step trials, then the rest on the winner
     if want_bad == 0:
         assert digest == "6684ada76ef62d08"
+
+
+def test_graph_replay_invalidated_by_new_params(oracle):
+    """Latency-bound advances replay a captured CUDA graph; set_params must drop
+    it (the shared gene is a kernel parameter).  512^2 (under-filled): gene A
+    captured then replayed, gene B, gene A again -- bit-exact against the oracle
+    run with the same gene switches."""
+    n, it = 512, 64
+    ga = fhn.Gene(a=-0.05)
+    gb = fhn.Gene(a=-0.3, Du=0.2, Dv=0.9)
+    seven = lambda g: [g.dt, g.a, g.b, g.eps, g.c, g.Du, g.Dv]  # noqa: E731
+    u0, v0 = oracle.init(2, n, n, 11)
+    with fhn.Simulator(n, n, persistent=-1) as sim:
+        sim.upload(u0, v0)
+        u, v = u0, v0
+        prev = None
+        for g in (ga, ga, gb, gb, ga):  # capture, replay, (new gene) capture, replay, capture
+            if g is not prev:
+                sim.set_params(g)
+                prev = g
+            assert int(sim.advance(it)[0]) == 0
+            u, v, _ = oracle.run(n, n, u, v, it, seven(g))
+        du, dv = sim.download()
+    assert np.array_equal(bits(du), bits(u)) and np.array_equal(bits(dv), bits(v))
