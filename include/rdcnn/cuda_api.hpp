@@ -1240,22 +1240,40 @@ SweepResult<T> sweep_grid(const SweepSpec& spec) {
   const int B = int(res.cells.size()), rows = base.nn, cols = base.nm;
   const size_t n = size_t(rows) * cols, nb = size_t(B);
   const Backend& be = base.backend;
-  rdcnn_sim_t raw = nullptr;
-  int rc;
-  if constexpr (sizeof(T) == 4) {
-    rc = rdcnn_sim_create(rows, cols, B, be.device, be.mode, &raw);
-  } else {
-    if (be.mode != RDCNN_STRICT) throw std::invalid_argument("fp64 runs in strict mode only");
-    rc = rdcnn_sim_create_f64(rows, cols, B, be.device, &raw);
-  }
-  if (rc == RDCNN_ECUDA && std::strstr(rdcnn_last_error(), "out of memory")) throw std::bad_alloc();
-  detail::check(rc, "rdcnn_sim_create (sweep batch)");
+  // The batched handle is kept (per thread) for the next sweep of the same
+  // shape: creating and destroying one allocates and frees the whole batch
+  // and its snapshot frames, which the driver made cost up to seconds.
   struct Del {
     void operator()(rdcnn_sim_t h) const { rdcnn_sim_destroy(h); }
   };
-  const std::unique_ptr<rdcnn_sim, Del> h(raw);
-  detail::check(rdcnn_sim_set_tuning(h.get(), sizeof(T) == 8 ? std::min(be.levels, 4) : be.levels, 0),
-                "rdcnn_sim_set_tuning");
+  struct Cached {
+    std::array<int, 6> key{};
+    std::unique_ptr<rdcnn_sim, Del> h;
+  };
+  static thread_local Cached cached;
+  const std::array<int, 6> key{rows, cols, B, be.device, be.mode, be.levels};
+  if (!cached.h || cached.key != key) {
+    cached.h.reset();
+    rdcnn_sim_t raw = nullptr;
+    int rc;
+    if constexpr (sizeof(T) == 4) {
+      rc = rdcnn_sim_create(rows, cols, B, be.device, be.mode, &raw);
+    } else {
+      if (be.mode != RDCNN_STRICT) throw std::invalid_argument("fp64 runs in strict mode only");
+      rc = rdcnn_sim_create_f64(rows, cols, B, be.device, &raw);
+    }
+    if (rc == RDCNN_ECUDA && std::strstr(rdcnn_last_error(), "out of memory")) throw std::bad_alloc();
+    detail::check(rc, "rdcnn_sim_create (sweep batch)");
+    cached.h.reset(raw);
+    cached.key = key;
+    detail::check(rdcnn_sim_set_tuning(raw, sizeof(T) == 8 ? std::min(be.levels, 4) : be.levels, 0),
+                  "rdcnn_sim_set_tuning");
+  }
+  rdcnn_sim* const h_raw = cached.h.get();
+  struct View {  // the calls below take h.get()
+    rdcnn_sim* p;
+    rdcnn_sim* get() const { return p; }
+  } const h{h_raw};
 
   // Per-grid genes, narrowed like make_params<T> (model.hpp:24-32).
   if constexpr (sizeof(T) == 4) {

@@ -504,6 +504,12 @@ int run_sweep_file(const char* path, bool f64) {
   }
   const auto res = sweep_grid<float>(spec);
   std::fputs(res.labels_csv.c_str(), stdout);
+  // A second sweep of the same shape runs on the cached batched handle.
+  const auto again = sweep_grid<float>(spec);
+  if (again.labels_csv != res.labels_csv) {
+    std::fprintf(stderr, "second sweep on the cached handle differs\n");
+    return 1;
+  }
   return spec.keep_buffers ? check_cells(res) : 0;
 }
 
