@@ -239,10 +239,17 @@ class Simulator:
     def set_params(self, genes):
         kind = ParamsF64 if self._f64 else ParamsF32
         genes = [genes] if isinstance(genes, (Gene, ParamsF32, ParamsF64)) else list(genes)
+        fn = self._lib.rdcnn_sim_set_params_f64 if self._f64 else self._lib.rdcnn_sim_set_params
+        if len(genes) > 1 and all(isinstance(g, Gene) for g in genes):
+            # Batches (sweeps): the kernel-order vectors narrowed in one pass,
+            # round-to-nearest like make_params<float> (model.hpp:24-32).
+            vec = np.array([g.to_vector() for g in genes], np.float64)
+            arr = np.ascontiguousarray(vec if self._f64 else vec.astype(np.float32))
+            check(fn(self._h, ctypes.cast(arr.ctypes.data, ctypes.POINTER(kind)), len(genes)))
+            return
         arr = (kind * len(genes))()
         for k, g in enumerate(genes):
             arr[k] = g if isinstance(g, kind) else params_from_gene(g, self.precision)
-        fn = self._lib.rdcnn_sim_set_params_f64 if self._f64 else self._lib.rdcnn_sim_set_params
         check(fn(self._h, arr, len(genes)))
 
     # state transfer

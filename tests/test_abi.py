@@ -131,3 +131,24 @@ def test_no_gpu_means_loud_failure():
     with pytest.raises(_lib.RdcnnError) as e:
         fhn.Simulator(16, 16)
     assert e.value.code == 3
+
+
+def test_batch_gene_narrowing_equals_c_abi():
+    """Simulator.set_params narrows batches of genes with numpy (one pass);
+    it must equal the C-ABI's per-gene make_params<float> narrowing
+    (rdcnn_params_from_gene, model.hpp:24-32) bit for bit."""
+    import numpy as np
+
+    import paper_2102_10340_b200 as fhn
+    from paper_2102_10340_b200.engine import ParamsF32, params_from_gene
+
+    rng = np.random.default_rng(7)
+    genes = [fhn.Gene(a=float(rng.normal()), b=float(rng.normal()), eps=float(rng.normal() * 0.1),
+                      c=float(rng.normal()), Du=float(abs(rng.normal())), Dv=float(abs(rng.normal())),
+                      dt=float(abs(rng.normal()) * 0.1)) for _ in range(500)]
+    genes += [fhn.Gene(Du=x) for x in np.linspace(0.02, 0.70, 64)]
+    vec = np.array([g.to_vector() for g in genes]).astype(np.float32)
+    fields = [f for f, _ in ParamsF32._fields_]
+    ref = np.array([[getattr(params_from_gene(g), f) for f in fields] for g in genes], np.float32)
+    assert fields == ["dt", "a", "b", "eps", "c", "du", "dv"]
+    assert np.array_equal(vec.view(np.uint32), ref.view(np.uint32))
