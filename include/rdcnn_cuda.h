@@ -269,7 +269,9 @@ uint64_t rdcnn_checksum_f64(const double* u, const double* v, size_t cells);
 /* ---- self-test of the device arithmetic -------------------------------------
  * Sweeps all 2^32 fp32 bit patterns x on the device and counts those where
  * div3_rn(x) differs from IEEE x/3 (finite x) or is finite (non-finite x);
- * domain 0: every x, domain 1: x = u*u for every u.  */
+ * domain 0: every x, domain 1: x = u*u for every u; domain 2: the gated
+ * two-op quotient of strict fp32 launches (fhn_stencil.cuh div3_rn2) inside
+ * RN(c - x/3) at c = +-2^-90 and c = 1, every x >= +0 (0 mismatches).  */
 int rdcnn_selftest_div3(int device, int domain, uint64_t* mismatches,
                         uint32_t* first_bad);
 /* fp64: `samples` inputs spanning every exponent (and their squares) against

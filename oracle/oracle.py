@@ -60,6 +60,8 @@ class Oracle:
         L.orc_laplacian5_f64.argtypes = [c_void_p, c_int, c_int, c_int, c_int]
         L.div3_sweep.restype = c_uint64
         L.div3_sweep.argtypes = [c_uint64, c_uint64, ctypes.POINTER(c_uint32)]
+        L.div3_two_op_sweep.restype = c_uint64
+        L.div3_two_op_sweep.argtypes = [c_int, ctypes.POINTER(c_uint32), ctypes.POINTER(c_uint32)]
         self.L = L
 
     def params(self, gene7=DEFAULT_GENE7) -> np.ndarray:
@@ -126,6 +128,13 @@ class Oracle:
         first = c_uint32(0)
         n = self.L.div3_sweep(lo, hi, ctypes.byref(first))
         return int(n), int(first.value)
+
+    def div3_two_op_sweep(self, mode: int):
+        """(mismatches, smallest, largest bad pattern) of the gated 2-op x/3
+        over every x >= +0: mode 0 the raw quotient, mode 1 RN(c - x/3)."""
+        lo, hi = c_uint32(0), c_uint32(0)
+        n = self.L.div3_two_op_sweep(mode, ctypes.byref(lo), ctypes.byref(hi))
+        return int(n), int(lo.value), int(hi.value)
 
 
 class Reference:

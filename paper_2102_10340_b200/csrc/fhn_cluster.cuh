@@ -175,7 +175,7 @@ __device__ __forceinline__ void cluster_row(const float (&uu)[W], const float (&
     const float u_r = k < W - 1 ? uc[k + 1] : ur;
     const float v_l = k > 0 ? vc[k - 1] : vl;
     const float v_r = k < W - 1 ? vc[k + 1] : vr;
-    fhn_cell<float, kFast>(uc[k], vc[k], u_r, u_l, ud[k], uu[k], v_r, v_l, vd[k], vu[k], p, neg_eps, un[k],
+    fhn_cell<float, kFast ? kFastArith : kStrictArith>(uc[k], vc[k], u_r, u_l, ud[k], uu[k], v_r, v_l, vd[k], vu[k], p, neg_eps, un[k],
                            vn[k]);
   }
 }

@@ -90,8 +90,8 @@ int k_index(int k) { return k == 1 ? 0 : k == 2 ? 1 : k == 4 ? 2 : 3; }
 template <class T>
 struct KernelTable {
   using Fn = void (*)(StepArgsT<T>);
-  Fn fn[2][4][2][2][2] = {};        // [wide][k][fast][per_grid][wrap]
-  int resident[2][4][2][2][2] = {};
+  Fn fn[2][4][3][2][2] = {};        // [wide][k][arith][per_grid][wrap]
+  int resident[2][4][3][2][2] = {};
 };
 
 template <class T, int W, int KI, int FI, int PI>
@@ -99,8 +99,8 @@ void fill_one(KernelTable<T>& t) {
   constexpr int K = 1 << KI;
   if constexpr (K <= Traits<T>::kMaxLevels && (FI == 0 || sizeof(T) == 4))
   {
-    t.fn[W > 1][KI][FI][PI][0] = &rdcnn_dev::fhn_wavefront_kernel<K, W, T, FI == 1, PI == 1, false, false>;
-    t.fn[W > 1][KI][FI][PI][1] = &rdcnn_dev::fhn_wavefront_kernel<K, W, T, FI == 1, PI == 1, false, true>;
+    t.fn[W > 1][KI][FI][PI][0] = &rdcnn_dev::fhn_wavefront_kernel<K, W, T, FI, PI == 1, false, false>;
+    t.fn[W > 1][KI][FI][PI][1] = &rdcnn_dev::fhn_wavefront_kernel<K, W, T, FI, PI == 1, false, true>;
   }
 }
 
@@ -110,6 +110,8 @@ void fill_k(KernelTable<T>& t) {
   fill_one<T, W, KI, 0, 1>(t);
   fill_one<T, W, KI, 1, 0>(t);
   fill_one<T, W, KI, 1, 1>(t);
+  fill_one<T, W, KI, 2, 0>(t);
+  fill_one<T, W, KI, 2, 1>(t);
 }
 
 template <class T, int W>
@@ -140,14 +142,14 @@ size_t smem_for(int w) {
 
 // Resident CTAs per SM of one instance (cached; occupancy is immutable).
 template <class T>
-int resident_blocks(int k, int w, bool fast, bool per_grid, bool wrap) {
+int resident_blocks(int k, int w, int arith, bool per_grid, bool wrap) {
   KernelTable<T>& t = table<T>();
   // Handles may launch concurrently from several host threads: the memo is
   // read and written atomically (every writer stores the same value).
-  int* slot = &t.resident[w > 1][k_index(k)][fast][per_grid][wrap];
+  int* slot = &t.resident[w > 1][k_index(k)][arith][per_grid][wrap];
   int r = __atomic_load_n(slot, __ATOMIC_RELAXED);
   if (r == 0) {
-    auto fn = t.fn[w > 1][k_index(k)][fast][per_grid][wrap];
+    auto fn = t.fn[w > 1][k_index(k)][arith][per_grid][wrap];
     if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, fn, kThreads, smem_for<T>(w)) !=
                    cudaSuccess || r < 1)
       r = 1;
@@ -197,22 +199,22 @@ cudaError_t launch_pdl(void (*fn)(Args), unsigned blocks, size_t smem, cudaStrea
 // Fused peer-exchange instances (fp32 slabs, shared gene): [wide][k][fast].
 struct PeerTable {
   using Fn = void (*)(StepArgsT<float>);
-  Fn fn[2][4][2][2] = {};  // [wide][k][fast][wrap]
-  int resident[2][4][2][2] = {};
+  Fn fn[2][4][3][2] = {};  // [wide][k][arith][wrap]
+  int resident[2][4][3][2] = {};
 };
 
 template <int W, int KI, int FI>
 void fill_peer_one(PeerTable& t) {
-  t.fn[W > 1][KI][FI][0] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI == 1, false, true, false>;
-  t.fn[W > 1][KI][FI][1] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI == 1, false, true, true>;
+  t.fn[W > 1][KI][FI][0] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI, false, true, false>;
+  t.fn[W > 1][KI][FI][1] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI, false, true, true>;
 }
 
 template <int W>
 void fill_peer_w(PeerTable& t) {
-  fill_peer_one<W, 0, 0>(t); fill_peer_one<W, 0, 1>(t);
-  fill_peer_one<W, 1, 0>(t); fill_peer_one<W, 1, 1>(t);
-  fill_peer_one<W, 2, 0>(t); fill_peer_one<W, 2, 1>(t);
-  fill_peer_one<W, 3, 0>(t); fill_peer_one<W, 3, 1>(t);
+  fill_peer_one<W, 0, 0>(t); fill_peer_one<W, 0, 1>(t); fill_peer_one<W, 0, 2>(t);
+  fill_peer_one<W, 1, 0>(t); fill_peer_one<W, 1, 1>(t); fill_peer_one<W, 1, 2>(t);
+  fill_peer_one<W, 2, 0>(t); fill_peer_one<W, 2, 1>(t); fill_peer_one<W, 2, 2>(t);
+  fill_peer_one<W, 3, 0>(t); fill_peer_one<W, 3, 1>(t); fill_peer_one<W, 3, 2>(t);
 }
 
 PeerTable& peer_table() {
@@ -225,12 +227,12 @@ PeerTable& peer_table() {
   return t;
 }
 
-int peer_resident_blocks(int k, int w, bool fast, bool wrap) {
+int peer_resident_blocks(int k, int w, int arith, bool wrap) {
   PeerTable& t = peer_table();
-  int& r = t.resident[w > 1][k_index(k)][fast][wrap];
+  int& r = t.resident[w > 1][k_index(k)][arith][wrap];
   if (r == 0) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, t.fn[w > 1][k_index(k)][fast][wrap], kThreads,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, t.fn[w > 1][k_index(k)][arith][wrap], kThreads,
                                                       smem_for<float>(w)) != cudaSuccess || n < 1)
       n = 1;
     r = n;
@@ -239,11 +241,11 @@ int peer_resident_blocks(int k, int w, bool fast, bool wrap) {
 }
 
 template <class T>
-cudaError_t launch_stencil(int k, int w, bool fast, bool per_grid, bool wrap, const StepArgsT<T>& a,
+cudaError_t launch_stencil(int k, int w, int arith, bool per_grid, bool wrap, const StepArgsT<T>& a,
                            long long warps, cudaStream_t s, bool full) {
   if (warps <= 0) return cudaSuccess;
   if (k != 1 && k != 2 && k != 4 && k != 8) return cudaErrorInvalidValue;
-  auto fn = table<T>().fn[w > 1][k_index(k)][fast][per_grid][wrap];
+  auto fn = table<T>().fn[w > 1][k_index(k)][arith][per_grid][wrap];
   if (!fn) return cudaErrorInvalidValue;
   const long long blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
   return launch_pdl(fn, (unsigned)blocks, smem_for<T>(w), s, a, full);
@@ -397,9 +399,23 @@ __global__ void div3_selftest_kernel(int domain, unsigned long long* count, unsi
     const unsigned bits = (unsigned)k;
     float x = __uint_as_float(bits);
     if (domain == 1) x = __fmul_rn(x, x);
+    if (domain == 2) x = __uint_as_float(bits & 0x7FFFFFFFu);
     const float want = __fdiv_rn(x, 3.0f);
-    const float got = rdcnn_dev::div3_rn(x);
-    const bool ok = isfinite(x) ? __float_as_uint(got) == __float_as_uint(want) : !isfinite(got);
+    bool ok;
+    if (domain == 2) {
+      // The gated 2-op quotient inside RN(c - x/3) at the gate boundary
+      // c = +-2^-90 and at c = 1 (fhn_stencil.cuh div3_rn2).
+      const float q2 = rdcnn_dev::div3_rn2(x);
+      ok = true;
+      const float cs[3] = {__uint_as_float(0x12800000u), __uint_as_float(0x92800000u), 1.0f};
+      for (int j = 0; j < 3; ++j) {
+        const float a = __fsub_rn(cs[j], q2), b = __fsub_rn(cs[j], want);
+        if (isfinite(a) != isfinite(b) || (isfinite(a) && __float_as_uint(a) != __float_as_uint(b))) ok = false;
+      }
+    } else {
+      const float got = rdcnn_dev::div3_rn(x);
+      ok = isfinite(x) ? __float_as_uint(got) == __float_as_uint(want) : !isfinite(got);
+    }
     if (!ok) {
       ++local;
       first = min(first, bits);
@@ -515,6 +531,8 @@ struct rdcnn_sim {
   ParamsT<float> h_params_f{};   // the shared gene (params_stride == 0)
   ParamsT<double> h_params_d{};
   int params_stride = 0;
+  bool div2_ok = true;      // every gene has |c| >= 2^-90: the 2-op x/3 instance is exact
+  int arith_override = -1;  // RDCNN_DIV3 / tests: force the 3-op (0) or 2-op (2) strict instance
   unsigned* d_flags = nullptr;  // batch words (+1 scratch for replays)
   unsigned* h_flags = nullptr;  // pinned mirror
   cudaStream_t stream = nullptr;
@@ -579,6 +597,25 @@ int width_for(const rdcnn_sim* s) {
   return (s->cols % Traits<T>::kWide == 0 && (!bulk || s->cols / Traits<T>::kWide >= 32)) ? Traits<T>::kWide : 1;
 }
 
+// Arithmetic instance of a launch: fast mode, or strict with the 2-op x/3
+// when every gene of the handle passes its gate (fhn_stencil.cuh div3_rn2),
+// else strict with the 3-op x/3.  fp64 always takes the 3-op strict path.
+template <class T>
+int arith_for(const rdcnn_sim* s) {
+  if (s->mode == RDCNN_FAST) return rdcnn_dev::kFastArith;
+  if (sizeof(T) != 4) return rdcnn_dev::kStrictArith;
+  if (s->arith_override >= 0) return s->arith_override == 2 && s->div2_ok ? rdcnn_dev::kStrictDiv2 : rdcnn_dev::kStrictArith;
+  return s->div2_ok ? rdcnn_dev::kStrictDiv2 : rdcnn_dev::kStrictArith;
+}
+
+// The gate of the 2-op x/3: |c| >= 2^-90 (false for NaN).
+template <class T>
+bool div2_gate(const ParamsT<T>* p, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!(std::fabs((double)p[i].c) >= 0x1p-90)) return false;
+  return true;
+}
+
 template <class T>
 StepArgsT<T> base_args(rdcnn_sim* s, int in_buf, int out_buf) {
   StepArgsT<T> a{};
@@ -613,10 +650,10 @@ template <class T>
 cudaError_t launch_range(rdcnn_sim* s, int k, StepArgsT<T> a, int row_begin, int row_end,
                          cudaStream_t st) {
   const int w = width_for<T>(s);
-  const bool fast = s->mode == RDCNN_FAST;
+  const int arith = arith_for<T>(s);
   const bool per_grid = a.params_stride != 0;
   const bool wrap = s->cols / w == 32;  // full-width bands (make_plan: halo 0)
-  const int rw = resident_blocks<T>(k, w, fast, per_grid, wrap) * (kThreads / 32);
+  const int rw = resident_blocks<T>(k, w, arith, per_grid, wrap) * (kThreads / 32);
   Plan p = make_plan(s->cols, w, k, a.batch, row_begin, row_end, seg_for(s, k, row_begin, row_end), s->sm_count, rw);
   if (p.warps == 0) return cudaSuccess;
   a.row_begin = row_begin;
@@ -627,13 +664,16 @@ cudaError_t launch_range(rdcnn_sim* s, int k, StepArgsT<T> a, int row_begin, int
   a.band_groups = p.band_groups;
   a.halo_groups = p.halo;
   ++s->launches;
-  return launch_stencil<T>(k, w, fast, per_grid, wrap, a, p.warps, st,
+  return launch_stencil<T>(k, w, arith, per_grid, wrap, a, p.warps, st,
                            4 * p.warps >= 3LL * rw * s->sm_count);
 }
 
 int alloc_common(rdcnn_sim* s) {
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   s->sm_count = sm_count_for(s->device);
+  // A/B and tests: RDCNN_DIV3=3 pins the 3-op x/3 strict instance, =2 the
+  // gated 2-op one (still subject to its gate); unset: automatic.
+  if (const char* e = std::getenv("RDCNN_DIV3")) s->arith_override = e[0] == '3' ? 0 : 2;
   RDCNN_CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   RDCNN_CUDA_TRY(cudaEventCreate(&s->ev0));
   RDCNN_CUDA_TRY(cudaEventCreate(&s->ev1));
@@ -947,8 +987,8 @@ int autotune_segments(rdcnn_sim* s, const Schedule& sched, long* n_io) {
   }();
   if (off || s->slab || s->seg_rows > 0 || s->tuned[ki]) return RDCNN_OK;
   const int w = width_for<T>(s);
-  const bool fast = s->mode == RDCNN_FAST, per_grid = s->params_stride != 0, wrap = s->cols / w == 32;
-  const int rw = resident_blocks<T>(k, w, fast, per_grid, wrap) * (kThreads / 32);
+  const bool per_grid = s->params_stride != 0, wrap = s->cols / w == 32;
+  const int rw = resident_blocks<T>(k, w, arith_for<T>(s), per_grid, wrap) * (kThreads / 32);
   const Plan p0 = make_plan(s->cols, w, k, s->batch, 0, s->rows, 0, s->sm_count, rw);
   if (4 * p0.warps >= 3LL * rw * s->sm_count) {  // fills the chip: the plan is right
     s->tuned[ki] = true;
@@ -1046,8 +1086,8 @@ int advance_launches(rdcnn_sim* s, long steps, long* first_bad) {
   bool graph = graphs_enabled() && n == 0 && nl >= 8;
   if (graph) {  // only for launches that leave warp slots empty (same rule as the autotuner)
     const int k = sched.kmax, w = width_for<T>(s);
-    const bool fast = s->mode == RDCNN_FAST, per_grid = s->params_stride != 0, wrap = s->cols / w == 32;
-    const int rw = resident_blocks<T>(k, w, fast, per_grid, wrap) * (kThreads / 32);
+    const bool per_grid = s->params_stride != 0, wrap = s->cols / w == 32;
+    const int rw = resident_blocks<T>(k, w, arith_for<T>(s), per_grid, wrap) * (kThreads / 32);
     const Plan p0 = make_plan(s->cols, w, k, s->batch, 0, s->rows, 0, s->sm_count, rw);
     graph = 4 * p0.warps < 3LL * rw * s->sm_count;
   }
@@ -1304,6 +1344,7 @@ int set_params_impl(rdcnn_sim* s, const ParamsT<T>* p, int n) {
   RDCNN_CUDA_TRY(cudaMemcpyAsync(s->d_params, p, sizeof(ParamsT<T>) * (size_t)n, cudaMemcpyHostToDevice, s->stream));
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
   s->params_stride = (n == 1) ? 0 : 1;
+  s->div2_ok = div2_gate<T>(p, n);
   if (n == 1) {
     if constexpr (sizeof(T) == 4) s->h_params_f = *p;
     else s->h_params_d = *p;
@@ -1345,9 +1386,9 @@ int peer_block(rdcnn_sim* s, int k, unsigned tag, cudaStream_t st) {
   a.ready = s->p2p_words;
   a.seq = s->p2p_seq;
   const int w = width_for<float>(s);
-  const bool fast = s->mode == RDCNN_FAST;
+  const int arith = arith_for<float>(s);
   const bool wrap = s->cols / w == 32;
-  const int rw = peer_resident_blocks(k, w, fast, wrap) * (kThreads / 32);
+  const int rw = peer_resident_blocks(k, w, arith, wrap) * (kThreads / 32);
   const Plan p = make_plan(s->cols, w, k, 1, 0, s->rows, s->seg_rows, s->sm_count, rw);
   a.row_begin = 0;
   a.row_end = s->rows;
@@ -1359,7 +1400,7 @@ int peer_block(rdcnn_sim* s, int k, unsigned tag, cudaStream_t st) {
   const int h = p.seg_rows, S = s->rows, g = s->ghost;
   a.n_top = p.n_bands * std::min(p.n_segs, (g + h - 1) / h);  // segments with r0 < g
   a.n_bot = p.n_bands * (p.n_segs - (S - g) / h);             // segments with r0 + h > S - g
-  auto fn = peer_table().fn[w > 1][k_index(k)][fast][wrap];
+  auto fn = peer_table().fn[w > 1][k_index(k)][arith][wrap];
   RDCNN_CUDA_TRY(launch_pdl(fn, (unsigned)p.warps, smem_for<float>(w), st, a, 4 * p.warps >= 3LL * rw * s->sm_count));
   ++s->launches;
   ++s->p2p_seq;
@@ -1625,11 +1666,10 @@ int rdcnn_sim_trace_launch(rdcnn_sim_t s, int levels, unsigned long long* host_t
   if (levels != 1 && levels != 2 && levels != 4 && levels != 8) return fail(RDCNN_EINVAL, "bad levels");
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   const int w = s->elem == 4 ? width_for<float>(s) : width_for<double>(s);
-  const bool fast = s->mode == RDCNN_FAST;
   const bool per_grid = s->params_stride != 0;
   const bool wrap = s->cols / w == 32;
-  const int rw = (s->elem == 4 ? resident_blocks<float>(levels, w, fast, per_grid, wrap)
-                               : resident_blocks<double>(levels, w, fast, per_grid, wrap)) * (kThreads / 32);
+  const int rw = (s->elem == 4 ? resident_blocks<float>(levels, w, arith_for<float>(s), per_grid, wrap)
+                               : resident_blocks<double>(levels, w, arith_for<double>(s), per_grid, wrap)) * (kThreads / 32);
   const Plan p = make_plan(s->cols, w, levels, s->batch, 0, s->rows, seg_for(s, levels, 0, s->rows), s->sm_count, rw);
   *n_warps = p.warps;
   if (p.warps > cap) return fail(RDCNN_EINVAL, "trace needs %lld entries", (long long)p.warps);
@@ -2161,7 +2201,7 @@ uint64_t rdcnn_checksum_f64(const double* u, const double* v, size_t cells) {
 }
 
 int rdcnn_selftest_div3(int device, int domain, uint64_t* mismatches, uint32_t* first_bad) {
-  if (!mismatches || !first_bad || (domain != 0 && domain != 1))
+  if (!mismatches || !first_bad || domain < 0 || domain > 2)
     return fail(RDCNN_EINVAL, "bad arguments");
   RDCNN_CUDA_TRY(cudaSetDevice(device));
   unsigned long long* d_count = nullptr;

@@ -171,6 +171,18 @@ def test_div3_exhaustive_cpu(oracle):
     assert (n, first) == (1, 0x80000000)
 
 
+def test_div3_two_op_gate_cpu(oracle):
+    """The gated 2-op x/3 of the strict fp32 kernel (fhn_stencil.cuh div3_rn2),
+    over every x >= +0: the raw quotient differs from IEEE x/3 only on
+    [2^-125, 2^-123]; the composite RN(c - x/3) of model.hpp:39 is identical
+    for c = +-2^-90 (the gate) and c = 1 on every input."""
+    n, lo, hi = oracle.div3_two_op_sweep(0)
+    assert n == 5592406
+    assert lo == 0x01000000 and hi == 0x02000000  # 2^-125 .. 2^-123
+    n, lo, hi = oracle.div3_two_op_sweep(1)
+    assert n == 0, (n, hex(lo), hex(hi))
+
+
 def test_baseline_golden_fixture_consistent(oracle):
     """tests/golden/baseline_golden.json (the reference's own full-size runs
     of the BASELINE configs, replayed on the B200 by test_baseline_gpu.py):

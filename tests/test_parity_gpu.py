@@ -41,6 +41,36 @@ def test_div3_exhaustive_on_device():
     assert (n.value, first.value) == (1, 0x80000000)
     assert lib.rdcnn_selftest_div3(0, 1, ctypes.byref(n), ctypes.byref(first)) == 0
     assert n.value == 0
+    # The gated 2-op quotient of strict fp32 launches, inside RN(c - x/3).
+    assert lib.rdcnn_selftest_div3(0, 2, ctypes.byref(n), ctypes.byref(first)) == 0
+    assert n.value == 0
+
+
+@pytest.mark.parametrize("c", [1.0, 0.0, 2.0 ** -100, 2.0 ** -89, -3.5])
+def test_div3_instances_agree_with_oracle(c, monkeypatch):
+    """Genes on both sides of the 2-op x/3 gate (|c| >= 2^-90): the strict
+    launch picks the 2-op or the 3-op instance, both equal the oracle bit for
+    bit; pinning the 3-op instance (RDCNN_DIV3=3) changes nothing."""
+    from oracle.oracle import Oracle
+    gene = fhn.Gene(c=c, a=-0.05)
+    orc = Oracle()
+    u0, v0 = orc.init(2, 96, 128, 5)
+    g7 = [gene.dt, gene.a, gene.b, gene.eps, gene.c, gene.Du, gene.Dv]
+    ou, ov, obad = orc.run(96, 128, u0, v0, 40, g7)
+    outs = []
+    for pin in (None, "3"):
+        if pin:
+            monkeypatch.setenv("RDCNN_DIV3", pin)
+        with fhn.Simulator(96, 128, device=0, levels=4) as sim:
+            sim.set_params(gene)
+            sim.upload(u0, v0)
+            bad = int(sim.advance(40)[0])
+            u, v = sim.download()
+        assert bad == obad
+        if obad == 0:
+            assert np.array_equal(u.view(np.uint32), ou.view(np.uint32))
+            assert np.array_equal(v.view(np.uint32), ov.view(np.uint32))
+        outs.append((u, v))
 
 
 # --------------------------------------------------------------------------
