@@ -53,6 +53,7 @@ struct StepArgsT {
   int rows;               // lattice rows (periodic) or slab rows (ghosted)
   int cols;               // lattice cols (W divides cols)
   int pitch;              // elements between consecutive rows
+  long long pitch_b;      // the same in bytes (kernel-param operand of the pointer steps)
   int periodic;           // 1: rows wrap mod rows; 0: ghost rows present
   int ghost;              // ghosted mode: ghost rows above row 0 in the buffer
   int row_begin, row_end; // output rows computed by this launch
@@ -287,6 +288,9 @@ __device__ __forceinline__ int wrap_index(int x, int n) {
 // distance 3 ticks (thousands of cycles at 16 warps/SM).  Each lane copies and later reads back only its
 // own W columns of each plane, so no cross-lane synchronisation is needed
 // beyond the lane's own cp.async.wait_group.
+#ifndef RDCNN_L0REG
+#define RDCNN_L0REG 1
+#endif
 constexpr int kStage = 6;
 constexpr int kPrefetch = 3;
 
@@ -550,9 +554,11 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
       jump = delta(next0, local_end);
     }
   }
+  // The row step adds a kernel-parameter operand (no register, no rescale);
+  // the wrap is a rarely taken branch, not predicated selects every tick.
   auto src_next = [&]() {
-    su += pitch;
-    if (--rows_left == 0) {
+    su = reinterpret_cast<const T*>(reinterpret_cast<const char*>(su) + a.pitch_b);
+    if (__builtin_expect(--rows_left == 0, 0)) {
       if constexpr (kPeer) {
         su += jump;
         rows_left = rows_left2;
@@ -622,6 +628,9 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
   }
 
   Row<W, T> win[K > 1 ? K - 1 : 1][3];
+#if RDCNN_L0REG
+  Row<W, T> l0[3];
+#endif
   Finite<T> fin;
   const bool store = owner && frozen == 0u;
   // The 6-slot ring is two halves of 3: tick j lives in slot j % 6, i.e.
@@ -653,11 +662,11 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
         } else {
           Row<W, T> o;
           level_row<W, T, kArith, kWrap>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
-          if (store) {
-            store_row<W, T>(du, du + vout_delta, 0, o);
-            fold_finite<W, T>(fin, o);
-          }
-          du += pitch;
+          // Folded on every lane (non-storing lanes are cleared at the end),
+          // so the store is the only guarded instruction.
+          fold_finite<W, T>(fin, o);
+          if (store) store_row<W, T>(du, du + vout_delta, 0, o);
+          du = reinterpret_cast<T*>(reinterpret_cast<char*>(du) + a.pitch_b);
         }
       }
     }
@@ -676,20 +685,31 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
     if constexpr (kBulk) {
       if (kSteady || j < n_load) bulk_wait(mb_now + 8u * ph, phase_now);
     }
+#if RDCNN_L0REG
+    // Level-0 rows kept in a 3-slot register ring: each staged row is read
+    // from shared memory once (tick j -> slot j % 3), ticks 0 and 1 included.
+    if (kSteady || j < n_load) {
+      if constexpr (!kBulk) stage_wait<kPrefetch>();
+      read_staged<W, T>(lane_off + half_now + ph * kSlot, l0[ph]);
+    }
+    if (kSteady || (j >= 2 && j < n_load)) {
+      const Row<W, T>& up = l0[(ph + 1) % 3];
+      const Row<W, T>& ce = l0[(ph + 2) % 3];
+      const Row<W, T>& dn = l0[ph];
+#else
     if (kSteady || (j >= 2 && j < n_load)) {
       if constexpr (!kBulk) stage_wait<kPrefetch>();
       Row<W, T> up, ce, dn;
       read_staged<W, T>(lane_off + (ph >= 2 ? half_now + (ph - 2) * kSlot : half_other + (ph + 1) * kSlot), up);
       read_staged<W, T>(lane_off + (ph >= 1 ? half_now + (ph - 1) * kSlot : half_other + 2 * kSlot), ce);
       read_staged<W, T>(lane_off + half_now + ph * kSlot, dn);
+#endif
       if constexpr (K == 1) {
         Row<W, T> o;
         level_row<W, T, kArith, kWrap>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
-        if (store) {
-          store_row<W, T>(du, du + vout_delta, 0, o);
-          fold_finite<W, T>(fin, o);
-        }
-        du += pitch;
+        fold_finite<W, T>(fin, o);
+        if (store) store_row<W, T>(du, du + vout_delta, 0, o);
+        du = reinterpret_cast<T*>(reinterpret_cast<char*>(du) + a.pitch_b);
       } else {
         level_row<W, T, kArith, kWrap>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
       }
@@ -735,6 +755,7 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
     }
   }
 
+  if (!store) fin = Finite<T>{};  // halo lanes and frozen grids never flag
   return fin.bad_in_warp();
 }
 

@@ -627,6 +627,7 @@ StepArgsT<T> base_args(rdcnn_sim* s, int in_buf, int out_buf) {
   a.rows = s->rows;
   a.cols = s->cols;
   a.pitch = s->pitch;
+  a.pitch_b = (long long)s->pitch * (long long)sizeof(T);
   a.periodic = s->slab ? 0 : 1;
   a.ghost = s->slab ? s->ghost : 0;
   a.batch = s->batch;
