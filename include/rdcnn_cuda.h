@@ -228,6 +228,53 @@ int rdcnn_slab_step_fused(rdcnn_sim_t sim, int k, void* stream);
 int rdcnn_slab_checkpoint_enable(rdcnn_sim_t sim, int on);
 int rdcnn_slab_restore(rdcnn_sim_t sim);
 
+/* ---- in-process multi-device ring ------------------------------------------
+ * One global_rows x cols torus split into n row slabs in ONE process, slab r
+ * on CUDA device devices[r] (entries may repeat: slabs sharing a GPU run
+ * their blocks interleaved on one stream).  Slab r owns rows
+ * [offset_r, offset_r + rows_r), rows_r = global_rows/n (+1 for the first
+ * global_rows % n slabs), each >= 2*ghost.  The halo exchange is the fused
+ * peer ring above (edge warps read the neighbours' rows in place over NVLink
+ * peer access); one host thread per device drives its slabs; no NCCL, no
+ * torch.distributed.  Replaces the row-band parallelism of
+ * kern::step_parallel (kernels.hpp:153-174) across GPUs (the
+ * devices[]/n_devices create of §8b).
+ *
+ * rdcnn_ring_advance reports the reference's exact iteration
+ * (engine.hpp:79, BlowUpError(iter+1)) and leaves the post-blow-up state
+ * (engine.hpp:103-104): the first block of each advance tees its input into
+ * a per-slab checkpoint; on a flag every slab restores it, re-advances to
+ * the first bad block and steps one level at a time.  With
+ * rdcnn_ring_set_exact(ring, 0) it reports the first iteration of the first
+ * bad block instead. */
+typedef struct rdcnn_ring* rdcnn_ring_t;
+int rdcnn_ring_create(int global_rows, int cols, const int* devices, int n_devices,
+                      int ghost, int mode, rdcnn_ring_t* out);
+void rdcnn_ring_destroy(rdcnn_ring_t ring);
+/* Slab r's handle (owned by the ring; slab-mode entry points only), its
+ * first global row, its row count and device.  Any output may be NULL. */
+int rdcnn_ring_slab(rdcnn_ring_t ring, int r, rdcnn_sim_t* slab, int* row_offset,
+                    int* rows, int* device);
+int rdcnn_ring_set_params(rdcnn_ring_t ring, const rdcnn_params_f32* p);
+/* Time levels per block: 1, 2, 4 or 8, at most ghost (default ghost). */
+int rdcnn_ring_set_levels(rdcnn_ring_t ring, int max_levels);
+int rdcnn_ring_set_exact(rdcnn_ring_t ring, int on);
+/* typ 1 or 2 over the global lattice (init_center_square / init_full_random). */
+int rdcnn_ring_init(rdcnn_ring_t ring, int typ, uint64_t seed);
+/* Global row-major planes (global_rows*cols each), split by slab. */
+int rdcnn_ring_upload(rdcnn_ring_t ring, const float* u, const float* v);
+int rdcnn_ring_download(rdcnn_ring_t ring, float* u, float* v);
+int rdcnn_ring_advance(rdcnn_ring_t ring, long steps, long* first_bad_iter);
+/* Device time of the last advance: max over devices (CUDA events). */
+int rdcnn_ring_elapsed_ms(rdcnn_ring_t ring, double* ms);
+int rdcnn_ring_launch_count(rdcnn_ring_t ring, long* n);
+/* Profiling: one block of `levels` on every slab with per-warp tracing;
+ * out receives n entries of 6 words {slab, start ns, end ns, smid, ns the
+ * warp waited for its neighbours' ready words, bytes it staged from peer
+ * memory} (cap entries at most).  Advances the state by `levels`. */
+int rdcnn_ring_trace_block(rdcnn_ring_t ring, int levels, unsigned long long* out,
+                           long long cap, long long* n);
+
 /* ---- snapshot store and analysis (batched sweeps, frames) ----------------
  * Replaces the host-side post-processing of sweep.hpp:48-112 and
  * frame.hpp:28-66 for device-resident runs.  A handle reserves `nframes`

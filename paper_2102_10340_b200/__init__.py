@@ -12,5 +12,6 @@ from .engine import (  # noqa: F401
     init_from_image, init_full_random, initial_state, make_backend, params_from_gene, run,
     run_timed, step, validate_config,
 )
+from .slab import Ring  # noqa: F401
 
 __version__ = "0.1.0"

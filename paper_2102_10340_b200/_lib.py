@@ -92,6 +92,21 @@ SIGNATURES = {
     "rdcnn_slab_step_fused": (c_int, [c_void_p, c_int, c_void_p]),
     "rdcnn_slab_checkpoint_enable": (c_int, [c_void_p, c_int]),
     "rdcnn_slab_restore": (c_int, [c_void_p]),
+    "rdcnn_ring_create": (c_int, [c_int, c_int, POINTER(c_int), c_int, c_int, c_int, POINTER(c_void_p)]),
+    "rdcnn_ring_destroy": (None, [c_void_p]),
+    "rdcnn_ring_slab": (c_int, [c_void_p, c_int, POINTER(c_void_p), POINTER(c_int), POINTER(c_int),
+                                POINTER(c_int)]),
+    "rdcnn_ring_set_params": (c_int, [c_void_p, POINTER(ParamsF32)]),
+    "rdcnn_ring_set_levels": (c_int, [c_void_p, c_int]),
+    "rdcnn_ring_set_exact": (c_int, [c_void_p, c_int]),
+    "rdcnn_ring_init": (c_int, [c_void_p, c_int, c_uint64]),
+    "rdcnn_ring_upload": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "rdcnn_ring_download": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "rdcnn_ring_advance": (c_int, [c_void_p, c_long, POINTER(c_long)]),
+    "rdcnn_ring_elapsed_ms": (c_int, [c_void_p, POINTER(c_double)]),
+    "rdcnn_ring_launch_count": (c_int, [c_void_p, POINTER(c_long)]),
+    "rdcnn_ring_trace_block": (c_int, [c_void_p, c_int, c_void_p, ctypes.c_longlong,
+                                       POINTER(ctypes.c_longlong)]),
     "rdcnn_sim_checksums": (c_int, [c_void_p, c_void_p]),
     "rdcnn_sim_frames_reserve": (c_int, [c_void_p, c_int]),
     "rdcnn_sim_frame_capture": (c_int, [c_void_p, c_int]),

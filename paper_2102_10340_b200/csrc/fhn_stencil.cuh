@@ -82,9 +82,30 @@ struct StepArgsT {
   const unsigned* ready;  // [2] this rank's "top / bottom ghosts delivered" words
   unsigned seq;           // block number: this block's ghosts are in when ready[] >= seq
   int n_top, n_bot;       // warps whose segment touches the top / bottom `ghost` rows
-  // Profiling only (rdcnn_sim_trace_launch): per warp {start ns, end ns, smid}.
+  // Checkpoint tee (kTee instances, the first block of a slab advance): the
+  // owned level-0 rows this launch reads are also stored here (same layout
+  // as u_in), so the advance's input survives for an exact blow-up replay
+  // without a separate device copy.
+  T* tee_u;
+  // Profiling only (rdcnn_sim_trace_launch / rdcnn_ring_trace_block): per
+  // warp {start ns, end ns, smid} (trace_stride 3), plus {ns spent waiting
+  // for the neighbours' ready words, bytes staged from peer memory}
+  // (trace_stride 5, kPeer instances).
   unsigned long long* trace;
+  int trace_stride;
 };
+
+// Per-warp profile of one block (kPeer traces).
+struct BlockStats {
+  unsigned long long wait_ns = 0;
+  unsigned long long peer_bytes = 0;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 using StepArgs = StepArgsT<float>;
 
 // ---------------------------------------------------------------------------
@@ -472,11 +493,13 @@ struct MinBlocks {
 // returns whether a stored value was non-finite (folded over the warp).
 // (A persistent variant that looped over blocks, each warp waiting only for
 // its 8 neighbours, measured 2.5 % slower than launches + PDL: profiles/.)
-template <int K, int W, class T, int kArith, bool kPerGrid, bool kPeer, bool kWrap>
+template <int K, int W, class T, int kArith, bool kPerGrid, bool kPeer, bool kWrap, bool kTee>
 __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned char* smem_raw, int lane, int wib,
                                                 int g, int band, int seg, unsigned frozen,
                                                 const T* __restrict__ u_in_b, const T* __restrict__ v_in_b,
-                                                T* __restrict__ u_out_b, T* __restrict__ v_out_b) {
+                                                T* __restrict__ u_out_b, T* __restrict__ v_out_b,
+                                                BlockStats& stats) {
+  static_assert(!kTee || (kPeer && RDCNN_L0REG), "the checkpoint tee is a slab (kPeer) feature");
   // Shared gene: read straight from the kernel-parameter bank.  Per-grid
   // genes (sweeps) come from global memory once per warp.
   const ParamsT<T> p = kPerGrid ? a.params[g] : a.shared;
@@ -514,8 +537,16 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
   if constexpr (kPeer) {
     top_edge = r0 < a.ghost;
     bot_edge = r0 + h > a.rows - a.ghost;
+    const bool tracing = a.trace != nullptr && (top_edge || bot_edge);
+    const unsigned long long t0 = tracing ? globaltimer() : 0ull;
     if (top_edge) wait_ready(a.ready + 0, a.seq);
     if (bot_edge) wait_ready(a.ready + 1, a.seq);
+    if (tracing) {
+      stats.wait_ns = globaltimer() - t0;
+      // Level-0 rows beyond the slab: rows r0-K .. r0+h+K-1 outside [0, rows).
+      const int beyond = max(0, K - r0) + max(0, r0 + h + K - a.rows);
+      stats.peer_bytes = (unsigned long long)beyond * 32ull * 2ull * W * sizeof(T);
+    }
   }
 
   // Running source row (wraps on the torus; never in ghosted slabs) and
@@ -572,6 +603,10 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
   };
   T* du = uout + (size_t)(a.periodic ? r0 : r0 + a.ghost) * pitch;
   const ptrdiff_t vout_delta = vout - uout;
+  // Checkpoint tee: the owned rows r0 .. r0+h-1 (level-0 rows of ticks
+  // K .. K+h-1) go to the same place in a.tee_u.
+  T* dc = nullptr;
+  if constexpr (kTee) dc = a.tee_u + (size_t)g * (size_t)a.grid_stride + (size_t)grp * W + (size_t)(r0 + a.ghost) * pitch;
 
   constexpr uint32_t kLaneBytes = uint32_t(sizeof(T)) * W;
   // A lane's first chunk: lane*16 in the chunk-major layout (16-byte multiples), else lane*kLaneBytes.
@@ -691,6 +726,12 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
     if (kSteady || j < n_load) {
       if constexpr (!kBulk) stage_wait<kPrefetch>();
       read_staged<W, T>(lane_off + half_now + ph * kSlot, l0[ph]);
+      if constexpr (kTee) {
+        if (j >= K && j < K + h) {
+          if (store) store_row<W, T>(dc, dc + vdelta, 0, l0[ph]);
+          dc = reinterpret_cast<T*>(reinterpret_cast<char*>(dc) + a.pitch_b);
+        }
+      }
     }
     if (kSteady || (j >= 2 && j < n_load)) {
       const Row<W, T>& up = l0[(ph + 1) % 3];
@@ -781,7 +822,8 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
 // whose segment reaches beyond it first wait for the neighbour's word, then
 // stage those rows straight from the neighbour's input buffer (peer memory)
 // and publish completion -- the halo exchange is fused into the step.
-template <int K, int W, class T, int kArith, bool kPerGrid, bool kPeer = false, bool kWrap = false>
+template <int K, int W, class T, int kArith, bool kPerGrid, bool kPeer = false, bool kWrap = false,
+          bool kTee = false>
 __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T, W>::value)
     fhn_wavefront_kernel(const StepArgsT<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -810,8 +852,9 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T, W>::value)
   const unsigned fl = a.flags != nullptr ? *(volatile unsigned*)(a.flags + g) : 0u;
   const unsigned frozen = fl != 0u && fl != a.tag;
 
-  const bool bad = wavefront_block<K, W, T, kArith, kPerGrid, kPeer, kWrap>(
-      a, smem_raw, lane, wib, g, band, seg, frozen, a.u_in, a.v_in, a.u_out, a.v_out);
+  BlockStats stats;
+  const bool bad = wavefront_block<K, W, T, kArith, kPerGrid, kPeer, kWrap, kTee>(
+      a, smem_raw, lane, wib, g, band, seg, frozen, a.u_in, a.v_in, a.u_out, a.v_out, stats);
 
   if (bad && lane == 0 && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);
   if (a.trace != nullptr && lane == 0) {
@@ -819,9 +862,14 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T, W>::value)
     unsigned smid;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    a.trace[3 * warp_id] = t_start;
-    a.trace[3 * warp_id + 1] = t_end;
-    a.trace[3 * warp_id + 2] = smid;
+    unsigned long long* tr = a.trace + (size_t)a.trace_stride * (size_t)warp_id;
+    tr[0] = t_start;
+    tr[1] = t_end;
+    tr[2] = smid;
+    if (a.trace_stride >= 5) {
+      tr[3] = stats.wait_ns;
+      tr[4] = stats.peer_bytes;
+    }
   }
 
 }

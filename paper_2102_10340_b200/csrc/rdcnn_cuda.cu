@@ -199,14 +199,16 @@ cudaError_t launch_pdl(void (*fn)(Args), unsigned blocks, size_t smem, cudaStrea
 // Fused peer-exchange instances (fp32 slabs, shared gene): [wide][k][fast].
 struct PeerTable {
   using Fn = void (*)(StepArgsT<float>);
-  Fn fn[2][4][3][2] = {};  // [wide][k][arith][wrap]
-  int resident[2][4][3][2] = {};
+  Fn fn[2][4][3][2][2] = {};  // [wide][k][arith][wrap][tee]
+  int resident[2][4][3][2][2] = {};
 };
 
 template <int W, int KI, int FI>
 void fill_peer_one(PeerTable& t) {
-  t.fn[W > 1][KI][FI][0] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI, false, true, false>;
-  t.fn[W > 1][KI][FI][1] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI, false, true, true>;
+  t.fn[W > 1][KI][FI][0][0] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI, false, true, false>;
+  t.fn[W > 1][KI][FI][1][0] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI, false, true, true>;
+  t.fn[W > 1][KI][FI][0][1] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI, false, true, false, true>;
+  t.fn[W > 1][KI][FI][1][1] = &rdcnn_dev::fhn_wavefront_kernel<1 << KI, W, float, FI, false, true, true, true>;
 }
 
 template <int W>
@@ -227,12 +229,12 @@ PeerTable& peer_table() {
   return t;
 }
 
-int peer_resident_blocks(int k, int w, int arith, bool wrap) {
+int peer_resident_blocks(int k, int w, int arith, bool wrap, bool tee) {
   PeerTable& t = peer_table();
-  int& r = t.resident[w > 1][k_index(k)][arith][wrap];
+  int& r = t.resident[w > 1][k_index(k)][arith][wrap][tee];
   if (r == 0) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, t.fn[w > 1][k_index(k)][arith][wrap], kThreads,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, t.fn[w > 1][k_index(k)][arith][wrap][tee], kThreads,
                                                       smem_for<float>(w)) != cudaSuccess || n < 1)
       n = 1;
     r = n;
@@ -1374,9 +1376,21 @@ int slab_step_impl(rdcnn_sim* s, int k, cudaStream_t st, bool boundary) {
 // the neighbours' ghost rows of the output buffer and signals them.  Stream
 // order alone covers the local dependencies (block n+1 reads what block n
 // wrote); the cross-rank ones are the in-kernel ready words.
-int peer_block(rdcnn_sim* s, int k, unsigned tag, cudaStream_t st) {
+// The band/segment plan of one fused peer-ring block (every owned row).
+Plan peer_plan(rdcnn_sim* s, int k, bool tee) {
+  const int w = width_for<float>(s);
+  const bool wrap = s->cols / w == 32;
+  const int rw = peer_resident_blocks(k, w, arith_for<float>(s), wrap, tee) * (kThreads / 32);
+  return make_plan(s->cols, w, k, 1, 0, s->rows, s->seg_rows, s->sm_count, rw);
+}
+
+int peer_block(rdcnn_sim* s, int k, unsigned tag, cudaStream_t st, float* tee = nullptr,
+               unsigned long long* trace = nullptr) {
   StepArgsT<float> a = base_args<float>(s, s->cur, s->cur ^ 1);
   a.tag = tag;
+  a.tee_u = tee;
+  a.trace = trace;
+  a.trace_stride = 5;
   const int ib = s->cur;  // the neighbours' INPUT buffers (all ranks run the same blocks)
   const size_t pitch = (size_t)s->pitch;
   a.peer_top = static_cast<const float*>(s->peer_buf[0][ib]) + (size_t)(s->ghost + s->peer_rows[0]) * pitch;
@@ -1389,8 +1403,8 @@ int peer_block(rdcnn_sim* s, int k, unsigned tag, cudaStream_t st) {
   const int w = width_for<float>(s);
   const int arith = arith_for<float>(s);
   const bool wrap = s->cols / w == 32;
-  const int rw = peer_resident_blocks(k, w, arith, wrap) * (kThreads / 32);
-  const Plan p = make_plan(s->cols, w, k, 1, 0, s->rows, s->seg_rows, s->sm_count, rw);
+  const int rw = peer_resident_blocks(k, w, arith, wrap, tee != nullptr) * (kThreads / 32);
+  const Plan p = peer_plan(s, k, tee != nullptr);
   a.row_begin = 0;
   a.row_end = s->rows;
   a.seg_rows = p.seg_rows;
@@ -1401,7 +1415,7 @@ int peer_block(rdcnn_sim* s, int k, unsigned tag, cudaStream_t st) {
   const int h = p.seg_rows, S = s->rows, g = s->ghost;
   a.n_top = p.n_bands * std::min(p.n_segs, (g + h - 1) / h);  // segments with r0 < g
   a.n_bot = p.n_bands * (p.n_segs - (S - g) / h);             // segments with r0 + h > S - g
-  auto fn = peer_table().fn[w > 1][k_index(k)][arith][wrap];
+  auto fn = peer_table().fn[w > 1][k_index(k)][arith][wrap][tee != nullptr];
   RDCNN_CUDA_TRY(launch_pdl(fn, (unsigned)p.warps, smem_for<float>(w), st, a, 4 * p.warps >= 3LL * rw * s->sm_count));
   ++s->launches;
   ++s->p2p_seq;
@@ -1680,11 +1694,13 @@ int rdcnn_sim_trace_launch(rdcnn_sim_t s, int levels, unsigned long long* host_t
   if (s->elem == 4) {
     StepArgsT<float> a = base_args<float>(s, s->cur, s->cur ^ 1);
     a.trace = d;
+    a.trace_stride = 3;
     a.tag = 1;
     rc = launch_range<float>(s, levels, a, 0, s->rows, s->stream) == cudaSuccess ? RDCNN_OK : RDCNN_ECUDA;
   } else {
     StepArgsT<double> a = base_args<double>(s, s->cur, s->cur ^ 1);
     a.trace = d;
+    a.trace_stride = 3;
     a.tag = 1;
     rc = launch_range<double>(s, levels, a, 0, s->rows, s->stream) == cudaSuccess ? RDCNN_OK : RDCNN_ECUDA;
   }
@@ -2018,12 +2034,16 @@ int rdcnn_slab_advance(rdcnn_sim_t s, long steps, long* first_bad) {
   s->slab_tag = 0;
   RDCNN_CUDA_TRY(cudaMemsetAsync(s->d_flags, 0, sizeof(unsigned), s->stream));
   const Schedule sched = make_schedule(steps, s->max_levels);
-  if (s->ckpt)  // the input of this advance, for an exact blow-up replay
+  // The input of this advance, for an exact blow-up replay: the fused peer
+  // ring tees it from its first block's level-0 reads (no extra pass over
+  // HBM); the NCCL ring copies it.
+  if (s->ckpt && !s->p2p)
     RDCNN_CUDA_TRY(cudaMemcpyAsync(s->ckpt, s->buf[s->cur], s->buf_elems * s->elem, cudaMemcpyDeviceToDevice,
                                    s->stream));
   RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
   for (long n = 0; n < sched.count() && s->p2p; ++n)
-    RDCNN_TRY(peer_block(s, sched.depth(n), (unsigned)(n + 1), s->stream));
+    RDCNN_TRY(peer_block(s, sched.depth(n), (unsigned)(n + 1), s->stream,
+                         n == 0 ? static_cast<float*>(s->ckpt) : nullptr));
   for (long n = 0; n < sched.count() && !s->p2p; ++n) {
     const int k = sched.depth(n);
     RDCNN_TRY(slab_step_impl<float>(s, k, s->stream, true));
@@ -2245,3 +2265,5 @@ int rdcnn_selftest_div3_f64(int device, uint64_t samples, uint64_t* mismatches, 
 }
 
 }  // extern "C"
+
+#include "ring.cuh"

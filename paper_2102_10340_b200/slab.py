@@ -1,4 +1,4 @@
-"""Row-slab sharding of one large torus across GPUs (one process per GPU).
+"""Row-slab sharding of one large torus across GPUs.
 
 Each rank owns ``rows // world`` consecutive rows of the global lattice
 (SURVEY.md §8e); rank r-1 is above, r+1 below, and the ring is periodic
@@ -6,14 +6,25 @@ Each rank owns ``rows // world`` consecutive rows of the global lattice
 kernels.hpp:46-47).  Column wrap stays inside each slab.  Two native
 transports advance a block of ``k <= ghost`` time levels:
 
-* ``p2p`` (default): ONE fused launch per block.  The warps that produce the
-  first/last ``ghost`` rows also store them straight into the neighbours'
-  ghost rows over peer memory (CUDA IPC mappings over NVLink; plain pointers
-  in-process) and publish a "delivered" word with a release store; the
-  neighbours' edge warps acquire it before reading their ghosts.  Interior
-  warps never wait, so the exchange overlaps the step tile by tile.
-* ``nccl``: boundary kernel -> NCCL send/recv of the edge rows on a comm
-  stream, overlapped with the interior kernel; wait; swap.
+* ``p2p`` (default): ONE fused launch per block.  The warps whose level-0
+  rows reach beyond the slab first acquire the neighbour's ready word, then
+  stage those rows straight from the neighbour's INPUT buffer over peer
+  memory (CUDA IPC mappings over NVLink; plain pointers in-process), and
+  finally publish their own word with a release store ("my edge rows of
+  this block are written, and I have finished reading yours").  Nothing is
+  copied into ghost rows; interior warps never wait, so the exchange
+  overlaps the step tile by tile.
+* ``nccl``: boundary kernel -> NCCL send/recv of the edge rows into the
+  ghost rows on a comm stream, overlapped with the interior kernel; wait;
+  swap.
+
+Two ways to run it:
+
+* :class:`Ring` -- ONE process drives every slab (``rdcnn_ring_*`` in the
+  C-ABI): one host thread per device, in-process peer pointers, the exact
+  blow-up replay in native code.  ``bench.py --gpus N`` without torchrun.
+* :class:`SlabStepper` -- one process per GPU (torchrun), descriptors
+  shared through torch.distributed, CUDA IPC between the processes.
 
 Arithmetic per cell is unchanged, so the result is bit-identical to the
 single-GPU periodic run at any world size.
@@ -37,6 +48,121 @@ class _CudaRows:
         self.__cuda_array_interface__ = {
             "shape": (rows, width), "typestr": "<f4", "data": (int(ptr), False), "version": 2,
         }
+
+
+class Ring:
+    """One torus of ``global_rows x cols`` split into row slabs in THIS
+    process (rdcnn_ring_*): slab r on ``devices[r]`` (entries may repeat),
+    the fused peer halo exchange between them, one host thread per device,
+    and the exact blow-up iteration.  Same surface as ``engine.Simulator``
+    for one fp32 lattice (``advance`` returns ``first_bad[1]``)."""
+
+    def __init__(self, global_rows: int, cols: int, devices, ghost: int = 4, mode: str = "strict",
+                 levels: Optional[int] = None, exact: bool = True):
+        self._lib = load()
+        devs = [int(d) for d in devices]
+        if not devs:
+            raise ValueError("a ring needs at least one device")
+        if mode not in ("strict", "fast"):
+            raise ValueError(f"unknown mode {mode}")
+        self.rows, self.cols, self.batch = int(global_rows), int(cols), 1
+        self.devices, self.ghost, self.mode = devs, int(ghost), mode
+        self.precision = "single"
+        import numpy as np
+        self.dtype = np.dtype(np.float32)
+        arr = (ctypes.c_int * len(devs))(*devs)
+        h = ctypes.c_void_p()
+        check(self._lib.rdcnn_ring_create(self.rows, self.cols, arr, len(devs), self.ghost,
+                                          RDCNN_FAST if mode == "fast" else RDCNN_STRICT, ctypes.byref(h)))
+        self._h = h
+        if levels is not None:
+            self.set_levels(levels)
+        check(self._lib.rdcnn_ring_set_exact(self._h, 1 if exact else 0))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.rdcnn_ring_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def slab(self, r: int):
+        """(row_offset, rows, device) of slab r."""
+        off, rows, dev = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        check(self._lib.rdcnn_ring_slab(self._h, int(r), None, ctypes.byref(off), ctypes.byref(rows),
+                                        ctypes.byref(dev)))
+        return off.value, rows.value, dev.value
+
+    def set_levels(self, levels: int):
+        check(self._lib.rdcnn_ring_set_levels(self._h, int(levels)))
+
+    def set_params(self, gene):
+        from .engine import params_from_gene
+        p = gene if isinstance(gene, _lib.ParamsF32) else params_from_gene(gene)
+        check(self._lib.rdcnn_ring_set_params(self._h, ctypes.byref(p)))
+
+    def init(self, typ: int, seed: int):
+        check(self._lib.rdcnn_ring_init(self._h, int(typ), ctypes.c_uint64(seed)))
+
+    def upload(self, u, v):
+        import numpy as np
+        u = np.ascontiguousarray(u, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        if u.size != self.rows * self.cols or v.size != self.rows * self.cols:
+            raise ValueError("upload size does not match rows*cols")
+        check(self._lib.rdcnn_ring_upload(self._h, u.ctypes.data, v.ctypes.data))
+
+    def upload_ptr(self, u_ptr: int, v_ptr: int):
+        check(self._lib.rdcnn_ring_upload(self._h, ctypes.c_void_p(u_ptr), ctypes.c_void_p(v_ptr)))
+
+    def download(self, u=None, v=None):
+        import numpy as np
+        n = self.rows * self.cols
+        u = np.empty(n, np.float32) if u is None else u
+        v = np.empty(n, np.float32) if v is None else v
+        check(self._lib.rdcnn_ring_download(self._h, u.ctypes.data, v.ctypes.data))
+        return u, v
+
+    def download_ptr(self, u_ptr: int, v_ptr: int):
+        check(self._lib.rdcnn_ring_download(self._h, ctypes.c_void_p(u_ptr), ctypes.c_void_p(v_ptr)))
+
+    def advance(self, steps: int):
+        """Advance every slab; returns first_bad[1]: the exact 1-based
+        iteration of the first non-finite value anywhere (0 = finite)."""
+        import numpy as np
+        bad = ctypes.c_long()
+        check(self._lib.rdcnn_ring_advance(self._h, int(steps), ctypes.byref(bad)))
+        return np.array([bad.value], dtype=np.int64)
+
+    def elapsed_ms(self) -> float:
+        ms = ctypes.c_double()
+        check(self._lib.rdcnn_ring_elapsed_ms(self._h, ctypes.byref(ms)))
+        return ms.value
+
+    def launch_count(self) -> int:
+        n = ctypes.c_long()
+        check(self._lib.rdcnn_ring_launch_count(self._h, ctypes.byref(n)))
+        return n.value
+
+    def trace_block(self, levels: int = 4):
+        """One traced block on every slab: an (n, 6) uint64 array of
+        {slab, start ns, end ns, smid, wait ns, peer bytes} per warp."""
+        import numpy as np
+        cap = 1 << 20
+        out = np.zeros((cap, 6), np.uint64)
+        n = ctypes.c_longlong()
+        check(self._lib.rdcnn_ring_trace_block(self._h, int(levels), out.ctypes.data, cap, ctypes.byref(n)))
+        return out[: n.value].copy()
 
 
 def ring_neighbours(rank: int, world: int):
