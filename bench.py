@@ -69,6 +69,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slab", action="store_true",
                     help="run the multi-GPU slab path even at N=1 (a world-1 ring)")
+    ap.add_argument("--devices", default=None,
+                    help="single-process multi-GPU run (no torchrun): comma-separated CUDA ordinals, one "
+                         "row slab each, e.g. 0,1,2,3 (default for --gpus N without torchrun: 0..N-1); "
+                         "repeating an ordinal puts several slabs on one GPU (functional tests only)")
+    ap.add_argument("--ring", action="store_true",
+                    help="run the slab workloads through the in-process ring (rdcnn_ring_*) even at N=1")
     ap.add_argument("--transport", default="auto", choices=("auto", "p2p", "nccl"),
                     help="slab halo exchange: fused peer stores in the step kernel (p2p), NCCL, "
                          "or auto (p2p unless a rank cannot map its neighbours' memory)")
@@ -193,6 +199,38 @@ class Workload:
         finally:
             os.unlink(path)
         return u, v
+
+def config_dict(wl: "Workload", args, world: int, use_slab: bool, transport):
+    """The line's ``config``: the workload both arms measure (the reference
+    arm prints the same dict; its bounded sample is described in its
+    cpu_baseline.sample)."""
+    n = wl.cols
+    per_rank_cells = wl.rows_rank * n * wl.batch
+    return {
+        "workload": (wl.desc
+                     + (f"; global {wl.rows_global}x{n} row-slabbed ({wl.rows_rank} rows per "
+                        f"GPU), halo exchange: "
+                        + ("fused peer reads in the step kernel" if transport == "p2p"
+                           else "NCCL send/recv overlapped with the interior kernel")
+                        if use_slab else "")),
+        "rows": wl.rows_global, "cols": n, "iterations_per_step": wl.iters, "levels_per_launch": args.levels,
+        "mode": args.mode,
+        "l2": (f"double-buffered state {2 * 8 * per_rank_cells / 2**20:.0f} MiB/GPU "
+               + ("> 126 MB L2 (no flush needed)" if 2 * 8 * per_rank_cells > 126e6
+                  else "fits in L2: a 256 MiB buffer is written before every step, each step "
+                       "timed on its own")),
+        **({"grids": wl.batch} if wl.batch > 1 else {}),
+        "parallelism": (f"slab{world}" if use_slab else f"replicas{world}" if world > 1 else "single"),
+        **({"transport": transport} if use_slab else {}),
+    }
+
+
+def predicted_layout(wl: "Workload", args, world: int):
+    """(use_slab, transport) our arm will use for this workload."""
+    use_slab = (world > 1 or args.slab or args.ring or bool(args.devices)) and not wl.replicas
+    transport = ("p2p" if args.transport == "auto" else args.transport) if use_slab else None
+    return use_slab, transport
+
 
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -365,9 +403,9 @@ def bench_reference_sweep(args, wl, ref, threads, world):
         "unit": "Mcell-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": wl.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": wl.desc, "rows": wl.rows_global, "cols": wl.cols, "grids": wl.batch},
+        "config": config_dict(wl, args, world, *predicted_layout(wl, args, world)),
         "cpu_baseline": {"value": round(value, 2), "unit": "Mcell-updates/s", "cores": threads,
-                         "kind": "reference", "sample": sample},
+                         "kind": "reference", "sample": sample, "cells_per_step_sampled": ncells},
         "e2e": {"value": round(value, 2), "unit": "Mcell-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -403,10 +441,12 @@ def bench_reference(args, rank, world):
         "unit": "Mcell-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": wl.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": wl.desc.replace(f"{wl.iters} iterations", f"{iters} iterations")
-                   + (f"; global {R}x{C}" if world > 1 else ""), "rows": R, "cols": C},
+        "config": config_dict(wl, args, world, *predicted_layout(wl, args, world)),
         "cpu_baseline": {"value": round(value, 2), "unit": "Mcell-updates/s", "cores": threads,
-                         "kind": "reference", "sample": sample},
+                         "kind": "reference", "sample": sample, "iterations_per_step_sampled": iters,
+                         "iterations_timed": f"{args.warmup * iters + 3}..{(args.warmup + args.steps) * iters + 2} "
+                                             "of the run (1-based), after 2 calibration iterations and the "
+                                             "warmup steps"},
         "e2e": {"value": round(value, 2), "unit": "Mcell-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -417,7 +457,10 @@ def bench_reference(args, rank, world):
 # our arm
 # ---------------------------------------------------------------------------
 
-def bench_ours(args, rank, world, local_rank):
+def bench_ours(args, rank, world, local_rank, ring_devices=None):
+    """Our arm.  ``ring_devices``: the single-process multi-GPU mode -- one
+    process drives every slab through the in-process ring (rdcnn_ring_*, one
+    host thread per device); world = len(ring_devices)."""
     import numpy as np
     import torch
 
@@ -436,7 +479,10 @@ def bench_ours(args, rank, world, local_rank):
     S = wl.iters
     gene = wl.gene(fhn)
     dist = None
-    if world > 1:
+    ring = None
+    if ring_devices is not None and wl.replicas:
+        raise SystemExit(f"{wl.name} runs independent replicas: launch N > 1 under torch.distributed.run")
+    if world > 1 and ring_devices is None:
         import torch.distributed as dist
         if one_dev:
             dist.init_process_group("gloo")
@@ -444,7 +490,26 @@ def bench_ours(args, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     launches = 0
-    if (world == 1 and not args.slab) or wl.replicas:
+    if ring_devices is not None:
+        # One process, N row slabs (rdcnn_ring_*): every device's blocks are
+        # enqueued by its own host thread; ring.elapsed_ms() is the max over
+        # the devices' CUDA-event times of each advance.
+        ring = fhn.Ring(wl.rows_global, n, ring_devices, ghost=args.levels, mode=args.mode)
+        ring.set_params(gene)
+        ring.init(wl.typ, 42)
+        for _ in range(args.warmup):
+            ring.advance(S)
+        torch.cuda.synchronize()
+        with ClockSampler(ring_devices[0]) as clocks:
+            t_ms = 0.0
+            for _ in range(args.steps):
+                bad = ring.advance(S)
+                t_ms += ring.elapsed_ms()
+                launches += ring.launch_count()
+                if bad.any():
+                    raise RuntimeError(f"blow-up at iteration {int(bad[0])}")
+        cells_global = wl.rows_global * n
+    elif (world == 1 and not args.slab) or wl.replicas:
         sim = fhn.Simulator(wl.rows_global, n, batch=wl.batch, device=local_rank, mode=args.mode,
                             levels=args.levels, seg_rows=args.seg_rows)
         sim.set_params(gene)
@@ -534,13 +599,13 @@ def bench_ours(args, rank, world, local_rank):
     # ---- roofline of the dominant kernel (the K-level wavefront stencil) ----
     peaks, peak_kind = measured_peaks()
     per_rank_cells = wl.rows_rank * n * wl.batch
-    use_slab = (world > 1 or args.slab) and not wl.replicas
-    transport = slab.transport if use_slab else None
+    use_slab = (world > 1 or args.slab or ring is not None) and not wl.replicas
+    transport = "p2p" if ring is not None else slab.transport if use_slab else None
     levels = args.levels
-    # One K-level block = one launch on the per-launch path; the persistent
-    # wavefront kernel runs every block of an advance in one launch, so the
-    # unit is the block (iterations / K), measured live by the CUDA events.
-    blocks_per_rank = max(S * args.steps // levels, 1)
+    # One K-level block = one launch per slab; slabs sharing a device (the
+    # one-GPU functional ring) run their launches one after another.
+    slabs_per_device = (max(ring_devices.count(d) for d in ring_devices) if ring is not None else 1)
+    blocks_per_rank = max(S * args.steps // levels, 1) * slabs_per_device
     avg_launch_s = (t_ms / 1e3) / blocks_per_rank
     alg_bytes_per_launch = BYTES_PER_CELL_UPDATE * per_rank_cells * levels
     achieved_gbs = alg_bytes_per_launch / avg_launch_s / 1e9
@@ -548,8 +613,22 @@ def bench_ours(args, rank, world, local_rank):
     if traffic_units != per_rank_cells * levels:
         traffic = None  # the committed capture is of another launch size
     sm_mhz = clock_info.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    max_mhz = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak_tops = 148 * 128 * sm_mhz * 1e6 / 1e12  # FP32 lanes x clock (non-FMA ops)
+    fp32_peak_max = 148 * 128 * max_mhz * 1e6 / 1e12
     fp32_achieved = value * 1e6 * FLOPS_PER_CELL_UPDATE / world / 1e12
+    devices_used = len(set(ring_devices)) if ring is not None else world
+    if ring is not None:
+        fp32_achieved = value * 1e6 * FLOPS_PER_CELL_UPDATE / devices_used / 1e12
+    # Measured DRAM traffic of the dominant kernel (committed ncu capture of
+    # one launch of this size) over the live average launch time.
+    dram = None
+    if traffic:
+        dram_gbs = traffic / avg_launch_s / 1e9
+        dram = {"achieved_gbs": round(dram_gbs, 1), "frac": round(dram_gbs / peaks["hbm_gbs"], 4),
+                "bytes_per_cell_update": round(traffic / (per_rank_cells * levels), 3),
+                "basis": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one launch "
+                         "(profiles/ncu_summary.json) / live average launch time"}
     roofline = {
         "bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": peaks["hbm_gbs"],
         "unit": "GB/s", "frac": round(achieved_gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
@@ -560,7 +639,12 @@ def bench_ours(args, rank, world, local_rank):
                  "so frac > 1 is expected and the FP32 pipe is the binding roof (see fp32)"),
         "fp32": {"achieved_tops": round(fp32_achieved, 2), "peak_tops": round(fp32_peak_tops, 2),
                  "frac": round(fp32_achieved / fp32_peak_tops, 4),
-                 "basis": "27 FP32 ops per cell-update; peak = 148 SM x 128 lanes x median SM clock"},
+                 "peak_tops_at_max_clock": round(fp32_peak_max, 2),
+                 "frac_at_max_clock": round(fp32_achieved / fp32_peak_max, 4),
+                 "basis": (f"27 FP32 ops per cell-update (reference arithmetic; strict mode issues 27 with "
+                           f"the gated 2-op x/3); peak = 148 SM x 128 lanes x SM clock: median under load "
+                           f"({sm_mhz:.0f} MHz) for frac, sm_max ({max_mhz:.0f} MHz) for frac_at_max_clock")},
+        **({"dram": dram} if dram else {}),
     }
 
     # ---- end to end through the public API with host buffers (N=1 only) ----
@@ -610,6 +694,32 @@ def bench_ours(args, rank, world, local_rank):
                "steps": e2e_steps, "lattices_in_flight": wl.batch}
         if any(c.blew_up for c in res.cells):
             raise RuntimeError("blow-up in the cfg4 sweep")
+    elif ring is not None:
+        # The whole torus through the public Ring API from pinned host
+        # memory: upload (split into the slabs) -> advance -> download.
+        cells = wl.rows_global * n
+        u_h = torch.empty(cells, dtype=torch.float32).pin_memory()
+        v_h = torch.empty(cells, dtype=torch.float32).pin_memory()
+        ring.download_ptr(u_h.data_ptr(), v_h.data_ptr())
+        dev_ms = 0.0
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            ring.upload_ptr(u_h.data_ptr(), v_h.data_ptr())
+            bad = ring.advance(S)
+            dev_ms += ring.elapsed_ms()
+            ring.download_ptr(u_h.data_ptr(), v_h.data_ptr())
+            if bad.any():
+                raise RuntimeError(f"blow-up in e2e ring run at iteration {int(bad[0])}")
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": round(cells * S * e2e_steps / e2e_s / 1e6, 2),
+               "unit": "Mcell-updates/s", "h2d_bytes_per_step": 2 * 4 * cells,
+               "d2h_bytes_per_step": 2 * 4 * cells,
+               "path": "paper_2102_10340_b200.Ring: rdcnn_ring_upload (pinned host, split into the slabs) -> "
+                       "rdcnn_ring_advance -> rdcnn_ring_download",
+               "steps": e2e_steps, "lattices_in_flight": 1,
+               "wall_ms_per_step": round(e2e_s * 1e3 / e2e_steps, 3),
+               "device_ms_per_step": round(dev_ms / e2e_steps, 3),
+               "copy_and_host_ms_per_step": round((e2e_s * 1e3 - dev_ms) / e2e_steps, 3)}
     elif not use_slab:
         # A stream of independent lattices through the public Pipeline API:
         # each one is uploaded from pinned host memory, advanced S iterations
@@ -646,8 +756,13 @@ def bench_ours(args, rank, world, local_rank):
         te = torch.tensor([time.perf_counter() - t0], device=red_dev)
         if dist is not None:  # replicas: max wall time over ranks
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        dev_ms = float(np.sum(pipe.last_device_ms))
         pipe.close()
         e2e_s = float(te.item())
+        split = {"wall_ms_per_step": round(e2e_s * 1e3 / e2e_steps, 3),
+                 "device_ms_per_step": round(dev_ms / e2e_steps, 3)}
+        if depth == 1:  # strictly sequential: the rest is the copies (and host calls)
+            split["copy_and_host_ms_per_step"] = round((e2e_s * 1e3 - dev_ms) / e2e_steps, 3)
         e2e = {"value": round(cells * world * S * e2e_steps / e2e_s / 1e6, 2),
                "unit": "Mcell-updates/s", "h2d_bytes_per_step": 2 * 4 * cells * world,
                "d2h_bytes_per_step": 2 * 4 * cells * world,
@@ -655,7 +770,7 @@ def bench_ours(args, rank, world, local_rank):
                         "(pinned host) -> rdcnn_sim_advance -> rdcnn_sim_download"
                         + (", lattices on alternating handles so copies overlap advances" if depth > 1 else "")
                         + ("; per rank, max wall time over ranks" if world > 1 else "")),
-               "steps": e2e_steps, "lattices_in_flight": depth}
+               "steps": e2e_steps, "lattices_in_flight": depth, **split}
         if bad.any() or not all(np.isfinite(u.numpy()).all() for u, _ in outs):
             raise RuntimeError("non-finite state after e2e")
     else:
@@ -669,10 +784,12 @@ def bench_ours(args, rank, world, local_rank):
         if dist is not None:
             dist.barrier()
         t0 = time.perf_counter()
+        dev_ms = 0.0
         for _ in range(e2e_steps):
             fhn._lib.check(lib.rdcnn_sim_upload(slab._h, u_h.data_ptr(), v_h.data_ptr()))
             slab.fill_ghosts()
             bad = slab.advance(S)
+            dev_ms += slab.elapsed_ms()
             fhn._lib.check(lib.rdcnn_sim_download(slab._h, u_h.data_ptr(), v_h.data_ptr()))
             if bad:
                 raise RuntimeError(f"blow-up in e2e slab run near iteration {bad}")
@@ -686,7 +803,8 @@ def bench_ours(args, rank, world, local_rank):
                "d2h_bytes_per_step": 2 * 4 * cells * world,
                "path": "per rank: rdcnn_sim_upload (pinned host) -> rdcnn_slab_fill_ghosts -> "
                        "rdcnn_slab_advance -> rdcnn_sim_download; max wall time over ranks",
-               "steps": e2e_steps}
+               "steps": e2e_steps, "wall_ms_per_step": round(e2e_s * 1e3 / e2e_steps, 3),
+               "device_ms_per_step (rank 0)": round(dev_ms / e2e_steps, 3)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -701,27 +819,12 @@ def bench_ours(args, rank, world, local_rank):
     if rank == 0:
         line = {
             "metric": "Mcell-updates/s", "value": round(value, 2), "unit": "Mcell-updates/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": devices_used, "steps": args.steps, "warmup": args.warmup,
+            **({"slabs": world, "devices": ring_devices} if ring is not None else {}),
             "ms_per_step": round(t_ms / args.steps, 3), "higher_is_better": True,
             "scaling": wl.scaling, "vs_baseline": vs_baseline, "dtype": "f32", "data": "synthetic",
             **({"vs_baseline_basis": vs_basis} if vs_basis else {}),
-            "config": {
-                "workload": (wl.desc
-                             + (f"; global {wl.rows_global}x{n} row-slabbed ({wl.rows_rank} rows per "
-                                f"GPU), halo exchange: "
-                                + ("fused peer stores in the step kernel" if transport == "p2p"
-                                   else "NCCL send/recv overlapped with the interior kernel")
-                                if use_slab else "")),
-                "rows": wl.rows_global, "cols": n, "iterations_per_step": S, "levels_per_launch": levels,
-                "mode": args.mode,
-                "l2": (f"double-buffered state {2 * 8 * per_rank_cells / 2**20:.0f} MiB/GPU "
-                       + ("> 126 MB L2 (no flush needed)" if 2 * 8 * per_rank_cells > 126e6
-                          else "fits in L2: a 256 MiB buffer is written before every step, each step "
-                               "timed on its own")),
-                **({"grids": wl.batch} if wl.batch > 1 else {}),
-                "parallelism": (f"slab{world}" if use_slab else f"replicas{world}" if world > 1 else "single"),
-                **({"transport": transport} if use_slab else {}),
-            },
+            "config": config_dict(wl, args, world, use_slab, transport),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -741,12 +844,17 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and "WORLD_SIZE" in os.environ:
         world = int(os.environ["WORLD_SIZE"])
+    ring_devices = None
+    if "RANK" not in os.environ and (args.gpus > 1 or args.devices or args.ring):
+        # Single-process multi-GPU: one process drives every slab through the
+        # in-process ring (rdcnn_ring_*), one host thread per device.
+        ring_devices = ([int(d) for d in args.devices.split(",")] if args.devices
+                        else list(range(args.gpus)))
+        world = len(ring_devices)
     if args.impl == "reference":
         bench_reference(args, rank, world)
         return
-    if world > 1 and "RANK" not in os.environ:
-        sys.exit("for --gpus N > 1 launch under torch.distributed.run (one process per GPU)")
-    bench_ours(args, rank, world, local_rank)
+    bench_ours(args, rank, world, local_rank, ring_devices)
 
 
 if __name__ == "__main__":

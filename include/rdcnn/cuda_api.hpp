@@ -371,6 +371,12 @@ struct Backend {
   int device = 0;                // CUDA ordinal
   int mode = RDCNN_STRICT;       // RDCNN_STRICT (bit-exact) or RDCNN_FAST
   int levels = 4;                // time levels fused per launch (1, 2, 4, 8)
+  // Two or more entries: the lattice is split into row slabs, slab r on
+  // CUDA device devices[r] (entries may repeat), halos exchanged by the
+  // fused peer ring (rdcnn_ring_*, fp32).  Empty or one entry: one device.
+  // The multi-GPU counterpart of the reference's row-band parallelism
+  // (kernels.hpp:153-174).
+  std::vector<int> devices;
   bool exact_order() const { return kind != BackendKind::Shift && mode == RDCNN_STRICT; }
 };
 
@@ -428,13 +434,44 @@ inline void check(int rc, const char* what) {
     throw CudaError(rc, std::string(what) + ": " + rdcnn_last_error());
 }
 
-// One device lattice of element type T (fp32, or fp64 in strict mode).
+// What a device lattice was created for: a handle is reused only for the
+// same device(s), arithmetic mode and fusion depth.
+struct SimKey {
+  int device = 0, mode = RDCNN_STRICT, levels = 4;
+  std::vector<int> devices;
+  bool operator==(const SimKey&) const = default;
+};
+
+inline SimKey sim_key(const Backend& b) {
+  SimKey k{b.device, b.mode, b.levels, {}};
+  if (b.devices.size() >= 2) k.devices = b.devices;
+  return k;
+}
+
+// One lattice of element type T (fp32, or fp64 in strict mode) on one
+// device, or -- when the backend names two or more devices -- row slabs of
+// it on several (fp32 only; rdcnn_ring_*).
 template <class T>
 class Sim {
   static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>);
 
  public:
-  Sim(int rows, int cols, const Backend& b) : rows_(rows), cols_(cols) {
+  Sim(int rows, int cols, const Backend& b) : rows_(rows), cols_(cols), key_(sim_key(b)) {
+    if (!key_.devices.empty()) {
+      if constexpr (sizeof(T) != 4) {
+        throw std::invalid_argument("multi-device row slabs run fp32 lattices only");
+      } else {
+        rdcnn_ring_t r = nullptr;
+        const int ghost = b.levels;
+        const int rc = rdcnn_ring_create(rows, cols, key_.devices.data(), int(key_.devices.size()), ghost,
+                                         b.mode, &r);
+        if (rc == RDCNN_ECUDA && std::strstr(rdcnn_last_error(), "out of memory")) throw std::bad_alloc();
+        if (rc == RDCNN_EINVAL) throw std::invalid_argument(rdcnn_last_error());
+        check(rc, "rdcnn_ring_create");
+        ring_.reset(r);
+        return;
+      }
+    }
     rdcnn_sim_t h = nullptr;
     int rc;
     if constexpr (sizeof(T) == 4) {
@@ -453,42 +490,68 @@ class Sim {
   }
   void set_gene(const Gene& g) {
     const auto v = gene_to_vector(g);
+    if (gene_set_ && v == gene_) return;  // unchanged: keep captured launches
+    gene_ = v;
+    gene_set_ = true;
     if constexpr (sizeof(T) == 4) {
       rdcnn_params_f32 p;
       rdcnn_params_from_gene(v.data(), &p);
-      check(rdcnn_sim_set_params(h_.get(), &p, 1), "rdcnn_sim_set_params");
+      if (ring_) check(rdcnn_ring_set_params(ring_.get(), &p), "rdcnn_ring_set_params");
+      else check(rdcnn_sim_set_params(h_.get(), &p, 1), "rdcnn_sim_set_params");
     } else {
       const rdcnn_params_f64 p{v[0], v[1], v[2], v[3], v[4], v[5], v[6]};
       check(rdcnn_sim_set_params_f64(h_.get(), &p, 1), "rdcnn_sim_set_params_f64");
     }
   }
   void upload(const GridState<T>& s) {
-    if constexpr (sizeof(T) == 4)
-      check(rdcnn_sim_upload(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_upload");
-    else
+    if constexpr (sizeof(T) == 4) {
+      if (ring_) check(rdcnn_ring_upload(ring_.get(), s.u.data(), s.v.data()), "rdcnn_ring_upload");
+      else check(rdcnn_sim_upload(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_upload");
+    } else {
       check(rdcnn_sim_upload_f64(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_upload_f64");
+    }
   }
   void download(GridState<T>& s) {
-    if constexpr (sizeof(T) == 4)
-      check(rdcnn_sim_download(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_download");
-    else
+    if constexpr (sizeof(T) == 4) {
+      if (ring_) check(rdcnn_ring_download(ring_.get(), s.u.data(), s.v.data()), "rdcnn_ring_download");
+      else check(rdcnn_sim_download(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_download");
+    } else {
       check(rdcnn_sim_download_f64(h_.get(), s.u.data(), s.v.data()), "rdcnn_sim_download_f64");
+    }
   }
-  // Returns the 1-based bad iteration within this call, or 0.
+  // Returns the 1-based bad iteration within this call, or 0 (exact on a
+  // multi-device ring too: rdcnn_ring_advance replays the bad block).
   long advance(long steps) {
     long bad = 0;
-    check(rdcnn_sim_advance(h_.get(), steps, &bad), "rdcnn_sim_advance");
+    if (ring_) check(rdcnn_ring_advance(ring_.get(), steps, &bad), "rdcnn_ring_advance");
+    else check(rdcnn_sim_advance(h_.get(), steps, &bad), "rdcnn_sim_advance");
     return bad;
+  }
+  // Device time of the last advance (max over devices for a ring).
+  double elapsed_ms() const {
+    double ms = 0;
+    if (ring_) check(rdcnn_ring_elapsed_ms(ring_.get(), &ms), "rdcnn_ring_elapsed_ms");
+    else check(rdcnn_sim_elapsed_ms(h_.get(), &ms), "rdcnn_sim_elapsed_ms");
+    return ms;
   }
   int rows() const { return rows_; }
   int cols() const { return cols_; }
+  bool multi_device() const { return bool(ring_); }
+  const SimKey& key() const { return key_; }
 
  private:
   struct Del {
     void operator()(rdcnn_sim_t h) const { rdcnn_sim_destroy(h); }
   };
+  struct RingDel {
+    void operator()(rdcnn_ring_t r) const { rdcnn_ring_destroy(r); }
+  };
   std::unique_ptr<rdcnn_sim, Del> h_;
+  std::unique_ptr<rdcnn_ring, RingDel> ring_;
   int rows_, cols_;
+  SimKey key_;
+  std::array<double, 7> gene_{};
+  bool gene_set_ = false;
 };
 
 }  // namespace detail
@@ -518,9 +581,15 @@ struct StepBuffers {
 
 namespace detail {
 
+// The buffers' device lattice for backend b: created on first use and
+// re-created when b names another device set, mode or fusion depth (the
+// host front buffer is uploaded on every call, so nothing is lost).
 template <class T>
 Sim<T>& device_for(StepBuffers<T>& bufs, const Backend& b) {
-  if (!bufs.device) bufs.device = std::make_shared<Sim<T>>(bufs.rows(), bufs.cols(), b);
+  if (!bufs.device || !(bufs.device->key() == sim_key(b))) {
+    bufs.device.reset();
+    bufs.device = std::make_shared<Sim<T>>(bufs.rows(), bufs.cols(), b);
+  }
   return *bufs.device;
 }
 
@@ -564,7 +633,8 @@ bool step(StepBuffers<T>& bufs, const M& model, const Backend& backend) {
 #if defined(__CUDACC__)
     detail::require_cuda(backend);
     const bool ok = cuda_model::step_device<M, T>(bufs.front.u.data(), bufs.front.v.data(), bufs.back.u.data(),
-                                                  bufs.back.v.data(), bufs.rows(), bufs.cols(), model);
+                                                  bufs.back.v.data(), bufs.rows(), bufs.cols(), model,
+                                                  backend.device);
     bufs.swap();
     return ok;
 #else
@@ -1197,7 +1267,28 @@ std::string labels_csv(const SweepResult<T>& res) {
   return out;
 }
 
+// The per-thread batched handle sweep_grid<T> keeps for its next call.
+struct SimDel {
+  void operator()(rdcnn_sim_t h) const { rdcnn_sim_destroy(h); }
+};
+struct SweepCache {
+  std::array<int, 6> key{};
+  std::unique_ptr<rdcnn_sim, SimDel> h;
+};
+template <class T>
+SweepCache& sweep_cache() {
+  static thread_local SweepCache c;
+  return c;
+}
+
 }  // namespace detail_sweep
+
+/// Frees the calling thread's cached sweep handles (fp32 and fp64), e.g.
+/// before cudaDeviceReset or when a worker thread is done sweeping.
+inline void release_sweep_cache() {
+  detail_sweep::sweep_cache<float>().h.reset();
+  detail_sweep::sweep_cache<double>().h.reset();
+}
 
 /// sweep_grid (sweep.hpp:249-326): |x|*|y| cells, one shared seed unless
 /// per_cell_seed, blow-ups recorded per cell (never fatal), all cells as the
@@ -1243,14 +1334,9 @@ SweepResult<T> sweep_grid(const SweepSpec& spec) {
   // The batched handle is kept (per thread) for the next sweep of the same
   // shape: creating and destroying one allocates and frees the whole batch
   // and its snapshot frames, which the driver made cost up to seconds.
-  struct Del {
-    void operator()(rdcnn_sim_t h) const { rdcnn_sim_destroy(h); }
-  };
-  struct Cached {
-    std::array<int, 6> key{};
-    std::unique_ptr<rdcnn_sim, Del> h;
-  };
-  static thread_local Cached cached;
+  // release_sweep_cache() frees it.  The cache is filled only once the
+  // handle is fully configured, so a failed configuration is not reused.
+  detail_sweep::SweepCache& cached = detail_sweep::sweep_cache<T>();
   const std::array<int, 6> key{rows, cols, B, be.device, be.mode, be.levels};
   if (!cached.h || cached.key != key) {
     cached.h.reset();
@@ -1264,10 +1350,12 @@ SweepResult<T> sweep_grid(const SweepSpec& spec) {
     }
     if (rc == RDCNN_ECUDA && std::strstr(rdcnn_last_error(), "out of memory")) throw std::bad_alloc();
     detail::check(rc, "rdcnn_sim_create (sweep batch)");
-    cached.h.reset(raw);
+    std::unique_ptr<rdcnn_sim, detail_sweep::SimDel> fresh(raw);
+    const int trc = rdcnn_sim_set_tuning(raw, sizeof(T) == 8 ? std::min(be.levels, 4) : be.levels, 0);
+    if (trc == RDCNN_EINVAL) throw std::invalid_argument(rdcnn_last_error());
+    detail::check(trc, "rdcnn_sim_set_tuning");
+    cached.h = std::move(fresh);
     cached.key = key;
-    detail::check(rdcnn_sim_set_tuning(raw, sizeof(T) == 8 ? std::min(be.levels, 4) : be.levels, 0),
-                  "rdcnn_sim_set_tuning");
   }
   rdcnn_sim* const h_raw = cached.h.get();
   struct View {  // the calls below take h.get()

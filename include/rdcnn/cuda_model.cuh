@@ -64,17 +64,29 @@ __global__ void model_step_kernel(const T* __restrict__ u, const T* __restrict__
   if (local) atomicOr(bad, 1u);
 }
 
-// Device scratch of the calling thread (one per element type), grown on demand.
+// Device scratch of the calling thread (one per element type), grown on
+// demand and re-allocated when the calling thread moves to another device.
 template <class T>
 struct Scratch {
   T* d = nullptr;
   unsigned* bad = nullptr;
   size_t cells = 0;
-  ~Scratch() {
+  int device = -1;
+  void release() {
+    if (device >= 0) cudaSetDevice(device);
     if (d) cudaFree(d);
     if (bad) cudaFree(bad);
+    d = nullptr;
+    bad = nullptr;
+    cells = 0;
   }
-  void ensure(size_t n) {
+  ~Scratch() { release(); }
+  void ensure(size_t n, int dev) {
+    if (dev != device) {
+      release();
+      device = dev;
+    }
+    if (cudaSetDevice(dev) != cudaSuccess) throw std::runtime_error("cuda_model: cudaSetDevice");
     if (n <= cells) return;
     if (d) cudaFree(d);
     d = nullptr;
@@ -84,11 +96,12 @@ struct Scratch {
   }
 };
 
+// One step of model m on CUDA device `device` (Backend::device).
 template <class M, class T>
-bool step_device(T* front_u, T* front_v, T* back_u, T* back_v, int rows, int cols, const M& m) {
+bool step_device(T* front_u, T* front_v, T* back_u, T* back_v, int rows, int cols, const M& m, int device = 0) {
   static thread_local Scratch<T> s;
   const size_t n = (size_t)rows * cols;
-  s.ensure(n);
+  s.ensure(n, device);
   T *du = s.d, *dv = s.d + n, *dun = s.d + 2 * n, *dvn = s.d + 3 * n;
   auto ok = [](cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string("cuda_model: ") + what + ": " + cudaGetErrorString(e));

@@ -220,13 +220,22 @@ int rdcnn_slab_attach_peers(rdcnn_sim_t sim, int rank, int world,
 int rdcnn_slab_step_fused(rdcnn_sim_t sim, int k, void* stream);
 
 /* Exact blow-up iteration for slab runs (engine.hpp:79 BlowUpError(iter+1)).
- * With the checkpoint on, every rdcnn_slab_advance first copies its input
- * buffer (ghost rows included) aside; rdcnn_slab_restore puts it back as the
- * front buffer.  The ranks then agree on the first bad block (min over
- * ranks), restore, re-advance to that block's first iteration and step one
- * level at a time until any rank flags -- see slab.py SlabStepper.advance. */
+ * With the checkpoint on, the first rdcnn_slab_advance after the state was
+ * set (upload/init), and then one advance every 2048 iterations
+ * (RDCNN_CKPT_INTERVAL), keeps its input aside: the fused peer ring tees it
+ * from the first block's own level-0 reads, the NCCL ring copies it.
+ * rdcnn_slab_checkpoint_age gives the iterations from the checkpoint to the
+ * start of the last advance; rdcnn_slab_restore makes the checkpoint the
+ * front buffer again.  The ranks then agree on the first bad block (min over
+ * ranks), restore, re-advance age + that block's first iteration - 1 steps
+ * and step one level at a time until any rank flags -- see slab.py
+ * SlabStepper.advance.  (Freezing every rank at the first flag instead
+ * cannot work: a rank's neighbours learn of it one block later, ranks at
+ * distance d only d blocks later, by when they have overwritten the state
+ * the replay needs.) */
 int rdcnn_slab_checkpoint_enable(rdcnn_sim_t sim, int on);
 int rdcnn_slab_restore(rdcnn_sim_t sim);
+int rdcnn_slab_checkpoint_age(rdcnn_sim_t sim, long* age);
 
 /* ---- in-process multi-device ring ------------------------------------------
  * One global_rows x cols torus split into n row slabs in ONE process, slab r

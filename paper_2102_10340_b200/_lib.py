@@ -92,6 +92,7 @@ SIGNATURES = {
     "rdcnn_slab_step_fused": (c_int, [c_void_p, c_int, c_void_p]),
     "rdcnn_slab_checkpoint_enable": (c_int, [c_void_p, c_int]),
     "rdcnn_slab_restore": (c_int, [c_void_p]),
+    "rdcnn_slab_checkpoint_age": (c_int, [c_void_p, POINTER(c_long)]),
     "rdcnn_ring_create": (c_int, [c_int, c_int, POINTER(c_int), c_int, c_int, c_int, POINTER(c_void_p)]),
     "rdcnn_ring_destroy": (None, [c_void_p]),
     "rdcnn_ring_slab": (c_int, [c_void_p, c_int, POINTER(c_void_p), POINTER(c_int), POINTER(c_int),

@@ -564,7 +564,9 @@ struct rdcnn_sim {
   unsigned* peer_words[2] = {};     // [prev, next]
   int peer_rows[2] = {0, 0};
   unsigned p2p_seq = 0;             // blocks run since attach (equal on every rank)
-  void* ckpt = nullptr;             // slab: copy of the last advance's input buffer (ghosts included)
+  void* ckpt = nullptr;             // slab: a recent advance's input buffer (ghosts included)
+  long ckpt_age = -1;               // iterations from the checkpointed state to now (-1: none)
+  long ckpt_age_at_call = 0;        // ... to the start of the last advance
   std::vector<void*> ipc_opened;    // cudaIpcCloseMemHandle on destroy
   void* frames = nullptr;   // snapshot store: n_frames x batch u-planes
   int n_frames = 0;
@@ -736,6 +738,18 @@ void free_all(rdcnn_sim* s) {
 void drop_graphs(rdcnn_sim* s) {
   for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
   s->graphs.clear();
+}
+
+// Iterations between exact-blow-up checkpoints of slab advances (the first
+// advance after the state is set always takes one).  RDCNN_CKPT_INTERVAL
+// overrides (tests use 1 and small values).
+long ckpt_interval() {
+  static const long v = [] {
+    const char* e = std::getenv("RDCNN_CKPT_INTERVAL");
+    const long x = e ? std::atol(e) : 0;
+    return x > 0 ? x : 2048L;
+  }();
+  return v;
 }
 
 // Sequence of block depths an advance of `steps` uses: floor(steps/Kmax)
@@ -1250,6 +1264,7 @@ int advance_impl(rdcnn_sim* s, long steps, long* first_bad) {
 
 int copy_state(rdcnn_sim* s, void* u, void* v, bool upload) {
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  if (upload) s->ckpt_age = -1;  // the checkpoint no longer precedes the state
   const size_t e = (size_t)s->elem;
   char* du = static_cast<char*>(s->buf[s->cur]);
   char* dv = du + (s->slab ? (size_t)s->plane_off * e : (size_t)s->rows * s->cols * s->batch * e);
@@ -1315,6 +1330,7 @@ int init_impl(rdcnn_sim* s, int typ, uint64_t seed, int global_rows, int row_off
       s->slab ? 1 : s->batch, s->rows, s->cols, global_rows, row_offset, typ, seed);
   RDCNN_CUDA_TRY(cudaGetLastError());
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  s->ckpt_age = -1;  // the checkpoint no longer precedes the state
   return RDCNN_OK;
 }
 
@@ -1346,13 +1362,17 @@ int set_params_impl(rdcnn_sim* s, const ParamsT<T>* p, int n) {
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   RDCNN_CUDA_TRY(cudaMemcpyAsync(s->d_params, p, sizeof(ParamsT<T>) * (size_t)n, cudaMemcpyHostToDevice, s->stream));
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  // Captured launches carry the shared gene (and the arithmetic instance it
+  // selects) by value: they survive only an identical shared gene.
+  const bool same = n == 1 && s->params_stride == 0 &&
+                    std::memcmp(&s->shared_params<T>(), p, sizeof(ParamsT<T>)) == 0;
   s->params_stride = (n == 1) ? 0 : 1;
   s->div2_ok = div2_gate<T>(p, n);
   if (n == 1) {
     if constexpr (sizeof(T) == 4) s->h_params_f = *p;
     else s->h_params_d = *p;
   }
-  drop_graphs(s);  // captured launches carry the shared gene by value
+  if (!same) drop_graphs(s);
   return RDCNN_OK;
 }
 
@@ -2034,16 +2054,21 @@ int rdcnn_slab_advance(rdcnn_sim_t s, long steps, long* first_bad) {
   s->slab_tag = 0;
   RDCNN_CUDA_TRY(cudaMemsetAsync(s->d_flags, 0, sizeof(unsigned), s->stream));
   const Schedule sched = make_schedule(steps, s->max_levels);
-  // The input of this advance, for an exact blow-up replay: the fused peer
+  // A state that precedes this advance, for an exact blow-up replay
+  // (rdcnn_slab_checkpoint_age): refreshed on the first advance after the
+  // state was set and then every ckpt_interval() iterations.  The fused peer
   // ring tees it from its first block's level-0 reads (no extra pass over
   // HBM); the NCCL ring copies it.
-  if (s->ckpt && !s->p2p)
+  const bool take = s->ckpt && steps > 0 && (s->ckpt_age < 0 || s->ckpt_age >= ckpt_interval());
+  if (take) s->ckpt_age = 0;
+  s->ckpt_age_at_call = s->ckpt_age;
+  if (take && !s->p2p)
     RDCNN_CUDA_TRY(cudaMemcpyAsync(s->ckpt, s->buf[s->cur], s->buf_elems * s->elem, cudaMemcpyDeviceToDevice,
                                    s->stream));
   RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
   for (long n = 0; n < sched.count() && s->p2p; ++n)
     RDCNN_TRY(peer_block(s, sched.depth(n), (unsigned)(n + 1), s->stream,
-                         n == 0 ? static_cast<float*>(s->ckpt) : nullptr));
+                         n == 0 && take ? static_cast<float*>(s->ckpt) : nullptr));
   for (long n = 0; n < sched.count() && !s->p2p; ++n) {
     const int k = sched.depth(n);
     RDCNN_TRY(slab_step_impl<float>(s, k, s->stream, true));
@@ -2056,6 +2081,7 @@ int rdcnn_slab_advance(rdcnn_sim_t s, long steps, long* first_bad) {
     s->cur ^= 1;
   }
   RDCNN_CUDA_TRY(cudaEventRecord(s->ev1, s->stream));
+  if (s->ckpt_age >= 0) s->ckpt_age += steps;
   unsigned tag = 0;
   RDCNN_CUDA_TRY(cudaMemcpyAsync(s->h_flags, s->d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, s->stream));
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
@@ -2089,9 +2115,17 @@ int rdcnn_slab_restore(rdcnn_sim_t s) {
   if (!s->ckpt) return fail(RDCNN_EINVAL, "no checkpoint (rdcnn_slab_checkpoint_enable)");
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   RDCNN_CUDA_TRY(cudaDeviceSynchronize());
+  if (s->ckpt_age < 0) return fail(RDCNN_EINVAL, "the checkpoint does not precede the current state");
   RDCNN_CUDA_TRY(cudaMemcpyAsync(s->buf[s->cur], s->ckpt, s->buf_elems * s->elem, cudaMemcpyDeviceToDevice,
                                  s->stream));
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  s->ckpt_age = 0;
+  return RDCNN_OK;
+}
+
+int rdcnn_slab_checkpoint_age(rdcnn_sim_t s, long* age) {
+  if (!s || !s->slab || !age) return fail(RDCNN_EINVAL, "not a slab handle");
+  *age = s->ckpt_age_at_call;
   return RDCNN_OK;
 }
 

@@ -37,6 +37,7 @@ struct rdcnn_ring {
   std::vector<cudaEvent_t> ev0, ev1;         // per distinct device
   double last_ms = 0;
   long launches = 0;
+  long ckpt_age = -1;          // iterations from the slabs' checkpoint to now (-1: none)
 };
 
 namespace {
@@ -113,6 +114,7 @@ int ring_run(rdcnn_ring* R, long steps, bool tee, std::vector<unsigned>& tags, d
 }
 
 int ring_restore(rdcnn_ring* R) {
+  R->ckpt_age = 0;
   for (rdcnn_sim* s : R->slabs) {
     RDCNN_CUDA_TRY(cudaSetDevice(s->device));
     RDCNN_CUDA_TRY(cudaMemcpyAsync(s->buf[s->cur], s->ckpt, s->buf_elems * s->elem, cudaMemcpyDeviceToDevice,
@@ -267,6 +269,7 @@ int rdcnn_ring_init(rdcnn_ring_t R, int typ, uint64_t seed) {
   if (!R) return fail(RDCNN_EINVAL, "null ring");
   for (int r = 0; r < R->n; ++r)
     RDCNN_TRY(rdcnn_slab_init(R->slabs[(size_t)r], typ, seed, R->global_rows, R->offset[(size_t)r]));
+  R->ckpt_age = -1;
   return ring_ready(R);
 }
 
@@ -276,6 +279,7 @@ int rdcnn_ring_upload(rdcnn_ring_t R, const float* u, const float* v) {
     const size_t o = (size_t)R->offset[(size_t)r] * (size_t)R->cols;
     RDCNN_TRY(rdcnn_sim_upload(R->slabs[(size_t)r], u + o, v + o));
   }
+  R->ckpt_age = -1;
   return ring_ready(R);
 }
 
@@ -295,8 +299,14 @@ int rdcnn_ring_advance(rdcnn_ring_t R, long steps, long* first_bad) {
   R->launches = 0;
   std::vector<unsigned> tags;
   double ms = 0;
-  RDCNN_TRY(ring_run(R, steps, R->exact, tags, &ms));
+  // The slabs' checkpoint: teed by the first block of the first advance
+  // after the state was set, then every ckpt_interval() iterations.
+  const bool take = R->exact && steps > 0 && (R->ckpt_age < 0 || R->ckpt_age >= ckpt_interval());
+  if (take) R->ckpt_age = 0;
+  const long age = R->ckpt_age;  // iterations from the checkpoint to this call's input
+  RDCNN_TRY(ring_run(R, steps, take, tags, &ms));
   R->last_ms = ms;
+  if (R->ckpt_age >= 0) R->ckpt_age += steps;
   const unsigned t = first_tag(tags);
   if (t == 0) return RDCNN_OK;
   const Schedule sched = make_schedule(steps, R->max_levels);
@@ -305,10 +315,11 @@ int rdcnn_ring_advance(rdcnn_ring_t R, long steps, long* first_bad) {
     if (first_bad) *first_bad = block_first;
     return fail(RDCNN_EBLOWUP, "blow-up: non-finite state in block %u (iterations from %ld)", t, block_first);
   }
-  // Exact iteration: every slab restores this advance's input (teed by its
-  // first block), re-advances to the bad block, then one level at a time.
+  // Exact iteration: every slab restores the checkpoint (`age` iterations
+  // before this call's input), re-advances to the bad block, then one level
+  // at a time.
   RDCNN_TRY(ring_restore(R));
-  const long pre = block_first - 1;
+  const long pre = age + block_first - 1;
   if (pre > 0) {
     RDCNN_TRY(ring_run(R, pre, false, tags, nullptr));
     if (first_tag(tags) != 0) return fail(RDCNN_ECUDA, "blow-up before the first flagged block on replay");
@@ -316,8 +327,9 @@ int rdcnn_ring_advance(rdcnn_ring_t R, long steps, long* first_bad) {
   for (int m = 1; m <= sched.depth((long)t - 1); ++m) {
     RDCNN_TRY(ring_run(R, 1, false, tags, nullptr));
     if (first_tag(tags) != 0) {
-      if (first_bad) *first_bad = pre + m;
-      return fail(RDCNN_EBLOWUP, "blow-up: non-finite state after iteration %ld", pre + m);
+      R->ckpt_age = pre + m;
+      if (first_bad) *first_bad = block_first - 1 + m;
+      return fail(RDCNN_EBLOWUP, "blow-up: non-finite state after iteration %ld", block_first - 1 + m);
     }
   }
   return fail(RDCNN_ECUDA, "blow-up flagged in block %u was not reproduced by the replay", t);

@@ -85,6 +85,19 @@ def params_from_gene(g: Gene, precision: str = "single"):
     return out
 
 
+def gene_batch(genes, precision: str = "single"):
+    """Batches (sweeps): the kernel-order vectors of many genes narrowed in
+    one numpy pass, round-to-nearest like make_params<float>
+    (model.hpp:24-32), as a ctypes array of ParamsF32 (ParamsF64 for
+    double) sharing the numpy buffer -- what rdcnn_sim_set_params takes."""
+    kind = ParamsF64 if precision == "double" else ParamsF32
+    vec = np.array([g.to_vector() for g in genes], np.float64)
+    arr = np.ascontiguousarray(vec if precision == "double" else vec.astype(np.float32))
+    out = (kind * len(genes)).from_buffer(arr)
+    out._keep = arr  # the ctypes view must keep its buffer alive
+    return out
+
+
 class GridState:
     """The paired u/v layers of a rows x cols toroidal lattice (grid.hpp:31-53)."""
 
@@ -150,13 +163,18 @@ class Backend:
     mode: str = "strict"
     device: int = 0
     levels: int = 4
+    # Two or more entries: row slabs of the lattice on these devices (the
+    # in-process fused peer ring, slab.Ring; fp32).  The multi-GPU
+    # counterpart of the reference's row-band parallelism (kernels.hpp:153-174).
+    devices: Optional[List[int]] = None
 
     def exact_order(self) -> bool:
         return self.mode == "strict"
 
 
 def make_backend(name: str = "cuda", tile_rows: int = 64, tile_cols: int = 64, threads: int = 0,
-                 mode: str = "strict", device: int = 0, levels: int = 4) -> Backend:
+                 mode: str = "strict", device: int = 0, levels: int = 4,
+                 devices: Optional[List[int]] = None) -> Backend:
     """backend.hpp:44-50 plus the ``cuda`` kind; unknown names raise ValueError."""
     if tile_rows < 1 or tile_cols < 1:
         raise ValueError("tile dimensions must be >= 1")
@@ -171,7 +189,8 @@ def make_backend(name: str = "cuda", tile_rows: int = 64, tile_cols: int = 64, t
         raise ValueError(f"unknown mode: {mode} (expected strict|fast)")
     if levels not in (1, 2, 4, 8):
         raise ValueError("levels must be 1, 2, 4 or 8")
-    return Backend(name, tile_rows, tile_cols, threads, mode, device, levels)
+    return Backend(name, tile_rows, tile_cols, threads, mode, device, levels,
+                   list(devices) if devices else None)
 
 
 # ---------------------------------------------------------------------------
@@ -241,11 +260,8 @@ class Simulator:
         genes = [genes] if isinstance(genes, (Gene, ParamsF32, ParamsF64)) else list(genes)
         fn = self._lib.rdcnn_sim_set_params_f64 if self._f64 else self._lib.rdcnn_sim_set_params
         if len(genes) > 1 and all(isinstance(g, Gene) for g in genes):
-            # Batches (sweeps): the kernel-order vectors narrowed in one pass,
-            # round-to-nearest like make_params<float> (model.hpp:24-32).
-            vec = np.array([g.to_vector() for g in genes], np.float64)
-            arr = np.ascontiguousarray(vec if self._f64 else vec.astype(np.float32))
-            check(fn(self._h, ctypes.cast(arr.ctypes.data, ctypes.POINTER(kind)), len(genes)))
+            arr = gene_batch(genes, self.precision)
+            check(fn(self._h, arr, len(genes)))
             return
         arr = (kind * len(genes))()
         for k, g in enumerate(genes):
@@ -387,6 +403,9 @@ class Pipeline:
         jobs = list(jobs)
         bad = np.zeros(len(jobs), np.int64)
         d = len(self.sims)
+        # Per job: the advance's device time (CUDA events on its handle), so
+        # callers can split end-to-end time into device and copy time.
+        self.last_device_ms = np.zeros(len(jobs), np.float64)
 
         def lane(k: int):
             sim = self.sims[k]
@@ -394,6 +413,7 @@ class Pipeline:
                 u_in, v_in, u_out, v_out = jobs[i]
                 sim.upload_ptr(u_in, v_in)
                 bad[i] = sim.advance(steps)[0]
+                self.last_device_ms[i] = sim.elapsed_ms()
                 sim.download_ptr(u_out, v_out)
 
         if d == 1:
@@ -430,8 +450,14 @@ class StepBuffers:
     def __init__(self, initial: GridState, backend: Optional[Backend] = None):
         be = backend or Backend()
         self.backend = be
-        self.sim = Simulator(initial.rows, initial.cols, 1, be.device, be.mode, be.levels,
-                             precision=initial.precision)
+        if be.devices and len(be.devices) > 1:
+            if initial.precision != "single":
+                raise ValueError("multi-device row slabs run fp32 lattices only")
+            from .slab import Ring
+            self.sim = Ring(initial.rows, initial.cols, be.devices, ghost=be.levels, mode=be.mode)
+        else:
+            self.sim = Simulator(initial.rows, initial.cols, 1, be.device, be.mode, be.levels,
+                                 precision=initial.precision)
         self.sim.upload(initial.u, initial.v)
         self._rows, self._cols = initial.rows, initial.cols
         self._gene_key = None

@@ -446,17 +446,20 @@ class SlabStepper:
         return 0 if (op == "min" and v == big) else v
 
     def _replay_exact(self, first_block_iter: int) -> int:
-        """Every rank: restore this advance's input, re-run to the first bad
+        """Every rank: restore the checkpoint (``age`` iterations before this
+        advance's input; the same on every rank), re-run to the first bad
         block, then one level at a time until any rank flags.  Leaves the
         post-blow-up state (as run_timed does, engine.hpp:103-104) and returns
-        the exact 1-based iteration."""
+        the exact 1-based iteration within this advance."""
+        age = ctypes.c_long()
+        check(self._lib.rdcnn_slab_checkpoint_age(self._h, ctypes.byref(age)))
         check(self._lib.rdcnn_slab_restore(self._h))
-        pre = first_block_iter - 1
+        pre = age.value + first_block_iter - 1
         if pre and self._agree(self._advance_native(pre), "min"):
             raise RuntimeError("blow-up before the first flagged block on replay")
         for m in range(1, self.ghost + 1):
             if self._agree(1 if self._advance_native(1) else 0, "max"):
-                return pre + m
+                return first_block_iter - 1 + m
         raise RuntimeError(f"blow-up flagged in the block at iteration {first_block_iter} "
                            "was not reproduced by the replay")
 

@@ -513,6 +513,69 @@ int run_sweep_file(const char* path, bool f64) {
   return spec.keep_buffers ? check_cells(res) : 0;
 }
 
+// Backend::devices: the lattice split into row slabs (rdcnn_ring_*), all on
+// device 0 here (the pool gives one GPU; the slabs' edge warps read each
+// other's rows through the peer path a multi-GPU box takes over NVLink).
+// The reference's criterion-1 KAT and BlowUpError iterations must not move.
+void multi_device_ring() {
+  for (int n : {2, 4}) {
+    RunConfig cfg = config(256, 1000, 1);
+    cfg.backend.devices.assign(size_t(n), 0);
+    auto out = run(cfg, Gene{}, init_center_square<float>(256, 256, 42));
+    CHECK(checksum_hex(checksum(out.final_state)) == "1026befcb693b1e5");
+  }
+  // test_engine.cpp:82-108 on two slabs of 8 rows, and a 4-slab 32x32 blow-up
+  // against the single-device iteration and post-blow-up state.
+  Gene g;
+  g.dt = 100;
+  Backend two = kCuda;
+  two.devices = {0, 0};
+  long it = 0;
+  RunConfig cfg = config(16, 1000, 1);
+  cfg.backend = two;
+  CHECK(throws_blowup([&] { run(cfg, g, init_center_square<float>(16, 16, 42)); }, &it));
+  CHECK(it == 4);
+  Backend four = kCuda;
+  four.devices = {0, 0, 0, 0};
+  for (int amp : {0, 1}) {
+    auto s0 = init_full_random<float>(64, 48, 5);
+    if (amp) s0.at_u(16, 7) = 7.935965061187744f;  // seeded on the slab 0 / slab 1 edge
+    Gene gg;
+    if (!amp) gg.dt = 2.5;
+    StepBuffers<float> single(s0), ring(s0);
+    long i1 = 0, i2 = 0;
+    const bool b1 = throws_blowup([&] { run_timed(single, gg, kCuda, 200); }, &i1);
+    const bool b2 = throws_blowup([&] { run_timed(ring, gg, four, 200); }, &i2);
+    CHECK(b1 == b2 && i1 == i2);
+    bool same = true;
+    for (size_t k = 0; k < single.front.u.size(); ++k) {
+      const float a = single.front.u[k], b = ring.front.u[k];
+      same &= (std::isfinite(a) == std::isfinite(b)) && (!std::isfinite(a) || a == b);
+    }
+    CHECK(same);
+    std::printf("ring blow-up case %d: single %s at %ld, 4 slabs at %ld\n", amp, b1 ? "blew up" : "finite", i1, i2);
+  }
+  // device_for follows the backend: the same buffers move between one device
+  // and four slabs and back, and the state carries over bit for bit.
+  auto s = init_full_random<float>(64, 64, 77);
+  StepBuffers<float> a(s), b(s);
+  for (int k = 0; k < 30; ++k) step(a, Gene{}, kCuda);
+  run_timed(b, Gene{}, kCuda, 10);
+  run_timed(b, Gene{}, four, 10);
+  run_timed(b, Gene{}, kCuda, 10);
+  CHECK(a.front == b.front);
+  // fp64 lattices stay on one device.
+  bool f64_rejected = false;
+  try {
+    StepBuffers<double> d(init_full_random<double>(32, 32, 1));
+    run_timed(d, Gene{}, four, 4);
+  } catch (const std::invalid_argument&) {
+    f64_rejected = true;
+  }
+  CHECK(f64_rejected);
+  release_sweep_cache();
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -538,6 +601,7 @@ int main(int argc, char** argv) {
   bench_emitters();
   bench_suite_cuda();
   acceptance_regimes_and_floor();
+  multi_device_ring();
   std::printf("cpp api: %d checks passed, %d failed\n", g_pass, g_fail);
   return g_fail;
 }

@@ -147,8 +147,18 @@ def test_batch_gene_narrowing_equals_c_abi():
                       c=float(rng.normal()), Du=float(abs(rng.normal())), Dv=float(abs(rng.normal())),
                       dt=float(abs(rng.normal()) * 0.1)) for _ in range(500)]
     genes += [fhn.Gene(Du=x) for x in np.linspace(0.02, 0.70, 64)]
-    vec = np.array([g.to_vector() for g in genes]).astype(np.float32)
+    from paper_2102_10340_b200.engine import ParamsF64, gene_batch
+
     fields = [f for f, _ in ParamsF32._fields_]
     ref = np.array([[getattr(params_from_gene(g), f) for f in fields] for g in genes], np.float32)
     assert fields == ["dt", "a", "b", "eps", "c", "du", "dv"]
-    assert np.array_equal(vec.view(np.uint32), ref.view(np.uint32))
+    # The helper Simulator.set_params passes to rdcnn_sim_set_params: a ctypes
+    # ParamsF32 array over the numpy buffer, read back struct by struct.
+    batch = gene_batch(genes)
+    assert len(batch) == len(genes) and isinstance(batch[0], ParamsF32)
+    got = np.array([[getattr(batch[k], f) for f in fields] for k in range(len(genes))], np.float32)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    b64 = gene_batch(genes, "double")
+    assert isinstance(b64[0], ParamsF64)
+    got64 = np.array([[getattr(b64[k], f) for f in fields] for k in range(len(genes))])
+    assert np.array_equal(got64, np.array([g.to_vector() for g in genes]))

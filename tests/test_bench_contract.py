@@ -39,6 +39,45 @@ def test_reference_arm_uses_every_host_core():
     assert d["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
 
 
+def test_reference_arm_prints_our_arms_config():
+    """Both arms describe the same workload (config) so the driver compares
+    like with like; the reference's bounded sample is recorded beside it."""
+    d = run_bench("--impl", "reference", "--size", "64", "--steps", "2", "--warmup", "1")
+    c = d["config"]
+    assert c["iterations_per_step"] == 10000 and c["rows"] == 64 and c["parallelism"] == "single"
+    assert c["workload"].startswith("cfg2") and c["levels_per_launch"] == 4 and c["mode"] == "strict"
+    cb = d["cpu_baseline"]
+    assert cb["iterations_per_step_sampled"] >= 1 and ".." in cb["iterations_timed"]
+    sys.path.insert(0, ROOT)
+    import argparse
+
+    import bench
+    args = argparse.Namespace(workload="cfg2", size=64, iters_per_step=None, levels=4, mode="strict",
+                              slab=False, ring=False, devices=None, transport="auto")
+    wl = bench.Workload(args, 1)
+    assert bench.config_dict(wl, args, 1, *bench.predicted_layout(wl, args, 1)) == c
+
+
+def test_reference_arm_ring_mode_config():
+    """--devices without torchrun: the reference arm runs the same global
+    lattice (weak scaling: one 64-row slab per entry) and says so."""
+    d = run_bench("--impl", "reference", "--size", "64", "--steps", "1", "--warmup", "1", "--devices", "0,0")
+    assert d["config"]["rows"] == 128 and d["config"]["parallelism"] == "slab2"
+    assert d["config"]["transport"] == "p2p"
+
+
+@pytest.mark.gpu
+def test_our_arm_ring_mode():
+    """Single-process multi-GPU mode (rdcnn_ring_*), here two slabs on the
+    one device: the line records the slabs, devices and launches."""
+    d = run_bench("--devices", "0,0", "--size", "256", "--steps", "2", "--warmup", "3", "--iters-per-step", "40",
+                  "--no-cpu-baseline", "--e2e-steps", "1")
+    assert d["n_gpus"] == 1 and d["slabs"] == 2 and d["devices"] == [0, 0]
+    assert d["config"]["parallelism"] == "slab2" and d["config"]["rows"] == 512
+    assert d["gpu_launches"] == 2 * 2 * 40 // 4 and d["value"] > 0
+    assert d["e2e"]["device_ms_per_step"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 2 * 4 * 512 * 256
+
+
 @pytest.mark.gpu
 def test_our_arm_contract():
     d = run_bench("--size", "512", "--steps", "3", "--warmup", "3", "--iters-per-step", "40",
@@ -48,6 +87,9 @@ def test_our_arm_contract():
     assert d["e2e"]["h2d_bytes_per_step"] == 2 * 4 * 512 * 512 and d["e2e"]["value"] > 0
     assert d["gpu_launches"] > 0 and "sm_mhz" in d["clocks"]
     assert d["config"]["workload"].startswith("cfg2")
+    fp = d["roofline"]["fp32"]
+    assert 0 < fp["frac_at_max_clock"] <= fp["frac"] + 1e-9
+    assert d["e2e"]["device_ms_per_step"] > 0 and "copy_and_host_ms_per_step" in d["e2e"]
     # BASELINE.md §1 publishes PyCUDA/P100 at N=512 (7581 Mcells/s): vs_baseline is value / that
     assert d["vs_baseline"] == pytest.approx(d["value"] / 7581.0, rel=1e-3) and "P100" in d["vs_baseline_basis"]
 

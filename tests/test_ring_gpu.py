@@ -209,3 +209,53 @@ def test_cfg5_sized_ring_blowup_crossing_slabs():
     fu, fv = np.isfinite(pu), np.isfinite(pv)
     assert np.array_equal(fu, np.isfinite(ru)) and np.array_equal(fv, np.isfinite(rv))
     assert np.array_equal(bits(ru)[fu], bits(pu)[fu]) and np.array_equal(bits(rv)[fv], bits(pv)[fv])
+
+
+def test_engine_run_with_devices_backend():
+    """engine.run / run_timed with Backend(devices=[...]): the reference's
+    criterion-1 KAT (test_output.txt:8) and blow-up iteration
+    (test_engine.cpp:95) on row slabs."""
+    cfg = fhn.RunConfig(init_mode=1, nn=256, nm=256, iter_max=1000, nssp=1, seed=42,
+                        backend=fhn.make_backend("cuda", devices=[0, 0, 0]))
+    out = fhn.run(cfg, fhn.Gene(), fhn.init_center_square(256, 256, 42))
+    assert fhn.checksum_hex(fhn.checksum(out.final_state)) == "1026befcb693b1e5"
+    bufs = fhn.StepBuffers(fhn.init_center_square(16, 16, 42), fhn.make_backend("cuda", devices=[0, 0]))
+    with pytest.raises(fhn.BlowUpError) as e:
+        fhn.run_timed(bufs, fhn.Gene(dt=100), bufs.backend, 1000)
+    assert e.value.iteration == 4
+
+
+@pytest.mark.parametrize("driver", ["ring2", "ring1", "slabstepper"])
+def test_blowup_replay_from_an_older_checkpoint(orc, driver):
+    """A lattice that blows up late (iteration 3032 of a near-unstable gene,
+    found with the oracle) advanced in calls of 100 iterations: the
+    checkpoint is refreshed only every 2048 iterations, so the exact replay
+    restarts from a state up to 2000 iterations before the failing call and
+    must still report the oracle's iteration (engine.hpp:79)."""
+    g7 = [0.2468, -0.3, 1.3, -0.1, 1.0, 0.06, 1.0]
+    u0, v0 = orc.init(2, 32, 48, 11)
+    ou, ov, obad = orc.run(32, 48, u0, v0, 4000, g7)
+    assert obad == 3032
+    if driver == "slabstepper":
+        from paper_2102_10340_b200.slab import SlabStepper
+        h = SlabStepper(32, 48, rank=0, world=1, ghost=4, device=0, transport="p2p")
+        h.set_params(gene7(g7))
+        h.upload(u0, v0)
+        h.fill_ghosts()
+        adv = h.advance
+    else:
+        h = Ring(32, 48, [0, 0] if driver == "ring2" else [0], ghost=4)
+        h.set_params(gene7(g7))
+        h.upload(u0, v0)
+        adv = lambda k: int(h.advance(k)[0])  # noqa: E731
+    done, bad = 0, 0
+    while not bad:
+        bad = adv(100)
+        if not bad:
+            done += 100
+    u, v = h.download()
+    h.close()
+    assert done + bad == obad
+    fu, fv = np.isfinite(ou), np.isfinite(ov)
+    assert np.array_equal(fu, np.isfinite(u)) and np.array_equal(fv, np.isfinite(v))
+    assert np.array_equal(bits(u)[fu], bits(ou)[fu]) and np.array_equal(bits(v)[fv], bits(ov)[fv])
