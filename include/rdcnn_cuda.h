@@ -48,7 +48,11 @@ enum rdcnn_status {
 
 enum rdcnn_mode {
   RDCNN_STRICT = 0, /* default: reference op order, IEEE RN, no FMA, no FTZ */
-  RDCNN_FAST = 1    /* opt-in: FMA-contracted; tolerance-checked, not bit-exact */
+  RDCNN_FAST = 1    /* opt-in: FMA-contracted, not bit-exact; checked at the
+                       reference tolerance after 10 steps (test_kernels.cpp:159-172)
+                       and statistically to 10^4 steps (regime labels of the full
+                       cfg4 sweep identical, cfg2 growth curve within 6.4e-5:
+                       profiles/fast_mode_r02.json, tests/test_fast_mode_gpu.py) */
 };
 
 /* Gene narrowed to fp32 in kernel order (gene_to_vector, gene.hpp:39-41). */

@@ -190,8 +190,8 @@ def _take_handle(key) -> Simulator:
     with _handles_lock:
         sim = _handles.pop(key, None)
     if sim is None:
-        rows, cols, batch, device, levels, prec = key
-        sim = Simulator(rows, cols, batch=batch, device=device, levels=levels, precision=prec)
+        rows, cols, batch, device, levels, prec, mode = key
+        sim = Simulator(rows, cols, batch=batch, device=device, levels=levels, precision=prec, mode=mode)
     return sim
 
 
@@ -222,7 +222,9 @@ def _run_cells(cells: List[SweepCell], idx0: int, spec: SweepSpec, base: RunConf
     if B == 0:
         return
     prec = base.precision
-    key = (rows, cols, B, device, levels, prec)
+    # base_config.backend.mode: strict (bit-exact, default) or the opt-in fast
+    # arithmetic (validated statistically, tools/fast_mode_validation.py).
+    key = (rows, cols, B, device, levels, prec, base.backend.mode)
     sim = _take_handle(key)
     sim.set_params([c.gene for c in cells])
     # initial states (init.hpp:67-82); the shared-seed default runs on the device
