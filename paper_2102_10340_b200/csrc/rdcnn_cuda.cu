@@ -26,6 +26,7 @@
 
 #include "analysis.cuh"
 #include "fhn_cluster.cuh"
+#include "fhn_rowring.cuh"
 #include "fhn_stencil.cuh"
 #include "rdcnn_cuda.h"
 
@@ -651,9 +652,197 @@ int seg_for(const rdcnn_sim* s, int k, int row_begin, int row_end) {
   return s->tuned_seg[k_index(k)];
 }
 
+// ---- row-ring path (fhn_rowring.cuh): a cluster spans a whole torus row ----
+// Periodic fp32 lattices whose width is 128*M*C columns (M warps per CTA, C
+// CTAs per cluster) can run their K=4 blocks with no halo lanes.  Measured
+// slower than the wavefront kernel (4096^2: 744k vs 894k), so it runs only
+// with RDCNN_ROWRING=1; RDCNN_RR_M pins M.
+struct RowRingTable {
+  using Fn = void (*)(StepArgsT<float>);
+  Fn fn[4][3][2] = {};             // [M: -,4,8,16][arith][per_grid]
+  int max_clusters[4][3][2][17] = {};  // by C (0: not yet queried)
+};
+
+template <int MI, int FI>
+void fill_rr(RowRingTable& t) {
+  t.fn[MI][FI][0] = &rdcnn_dev::fhn_rowring_kernel<4, 2 << MI, FI, false>;
+  t.fn[MI][FI][1] = &rdcnn_dev::fhn_rowring_kernel<4, 2 << MI, FI, true>;
+}
+template <int MI>
+void fill_rr_m(RowRingTable& t) {
+  fill_rr<MI, 0>(t);
+  fill_rr<MI, 1>(t);
+  fill_rr<MI, 2>(t);
+}
+
+std::mutex g_rr_mu;
+RowRingTable& rr_table() {
+  static RowRingTable t = [] {
+    RowRingTable x;
+    fill_rr_m<1>(x);
+    fill_rr_m<2>(x);
+    fill_rr_m<3>(x);
+    return x;
+  }();
+  return t;
+}
+
+// RDCNN_ROWRING=1: use it where it fits; =2: also fail any K=4 launch that
+// cannot take it (tests prove the path ran).
+int rowring_setting() {
+  static const int v = [] {
+    const char* e = std::getenv("RDCNN_ROWRING");
+    return e && (e[0] == '1' || e[0] == '2') ? e[0] - '0' : 0;
+  }();
+  return v;
+}
+bool rowring_enabled() { return rowring_setting() > 0; }
+
+int rowring_forced_m() {
+  static const int m = [] {
+    const char* e = std::getenv("RDCNN_RR_M");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+
+struct RRPlan {
+  int M = 0, C = 0, seg_rows = 0, n_segs = 0;
+  long long clusters = 0;
+  size_t smem = 0;
+  bool full = false;
+  RowRingTable::Fn fn = nullptr;
+};
+
+int rr_mi(int m) { return m == 2 ? 0 : m == 4 ? 1 : m == 8 ? 2 : 3; }
+
+// Chooses M, C and the segment plan; false when the launch does not fit the
+// row-ring path (the wavefront kernel runs it).
+bool rowring_plan(rdcnn_sim* s, int k, int arith, bool per_grid, int batch, int row_begin, int row_end,
+                  int seg_override, RRPlan& p) {
+  if (!rowring_enabled() || s->slab || s->elem != 4 || k != 4 || s->cols % 128 != 0) return false;
+  const int wr = s->cols / 128;  // warps per row = M*C
+  static const int kPref[] = {16, 8, 4};
+  const int forced = rowring_forced_m();
+  int M = 0;
+  for (int m : kPref) {
+    if (forced && m != forced) continue;
+    if (m <= wr && wr % m == 0 && wr / m <= 16) {
+      M = m;
+      break;
+    }
+  }
+  if (M == 0) return false;
+  const int C = wr / M;
+  RowRingTable& t = rr_table();
+  const int mi = rr_mi(M);
+  p.fn = t.fn[mi][arith][per_grid];
+  if (!p.fn) return false;
+  p.M = M;
+  p.C = C;
+  p.smem = (size_t)rdcnn_dev::rowring_smem_bytes(M, k);
+  int nc;
+  {
+    std::lock_guard<std::mutex> lock(g_rr_mu);
+    int& slot = t.max_clusters[mi][arith][per_grid][C];
+    if (slot == 0) {
+      if (cudaFuncSetAttribute(p.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess) {
+        cudaGetLastError();
+        slot = -1;
+      } else {
+        if (C > 8) cudaFuncSetAttribute(p.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)C);
+        cfg.blockDim = dim3(32u * (unsigned)M);
+        cfg.dynamicSmemBytes = p.smem;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, p.fn, &cfg) != cudaSuccess || n < 1) {
+          cudaGetLastError();
+          n = -1;
+        }
+        slot = n;
+      }
+    }
+    nc = slot;
+  }
+  if (nc < 1) return false;
+  const int nrows = row_end - row_begin;
+  if (nrows <= 0) return false;
+  int h;
+  if (seg_override > 0) {
+    h = seg_override;
+  } else {
+    // As make_plan: one wave of clusters, segments of at least 8K rows
+    // unless the lattice cannot fill the chip anyway.
+    const long long segs = std::max<long long>(1, nc / std::max(batch, 1));
+    h = (int)std::max<long long>(1, (nrows + segs - 1) / segs);
+    const int h_long = std::max(16, 8 * k);
+    const long long cl_long = (long long)batch * ((nrows + h_long - 1) / h_long);
+    h = std::max(h, std::min(nrows, cl_long >= nc / 2 ? h_long : std::max(4, 2 * k)));
+  }
+  h = std::min(h, nrows);
+  p.seg_rows = h;
+  p.n_segs = (nrows + h - 1) / h;
+  p.clusters = (long long)p.n_segs * batch;
+  if (seg_override <= 0 && p.clusters > nc && p.clusters < 2LL * nc && nc / batch >= 1) {
+    const long long segs = nc / batch;
+    p.seg_rows = (int)((nrows + segs - 1) / segs);
+    p.n_segs = (nrows + p.seg_rows - 1) / p.seg_rows;
+    p.clusters = (long long)p.n_segs * batch;
+  }
+  p.full = 4 * p.clusters >= 3LL * nc;
+  return true;
+}
+
+cudaError_t launch_rowring(const RRPlan& p, StepArgsT<float> a, cudaStream_t st) {
+  a.seg_rows = p.seg_rows;
+  a.n_segs = p.n_segs;
+  a.n_bands = p.C;
+  a.band_groups = 32 * p.M;
+  a.halo_groups = 0;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)p.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  int na = 1;
+  if (pdl_enabled() && p.full) {
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    na = 2;
+  }
+  cfg.gridDim = dim3((unsigned)(p.clusters * p.C));
+  cfg.blockDim = dim3(32u * (unsigned)p.M);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = (unsigned)na;
+  return cudaLaunchKernelEx(&cfg, p.fn, a);
+}
+
 template <class T>
 cudaError_t launch_range(rdcnn_sim* s, int k, StepArgsT<T> a, int row_begin, int row_end,
                          cudaStream_t st) {
+  if constexpr (sizeof(T) == 4) {
+    RRPlan rp;
+    if (a.trace == nullptr &&
+        rowring_plan(s, k, arith_for<T>(s), a.params_stride != 0, a.batch, row_begin, row_end,
+                     seg_for(s, k, row_begin, row_end), rp)) {
+      a.row_begin = row_begin;
+      a.row_end = row_end;
+      ++s->launches;
+      return launch_rowring(rp, a, st);
+    }
+    if (rowring_setting() == 2 && k == 4 && a.trace == nullptr) return cudaErrorNotSupported;
+  }
   const int w = width_for<T>(s);
   const int arith = arith_for<T>(s);
   const bool per_grid = a.params_stride != 0;

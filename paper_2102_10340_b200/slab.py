@@ -213,15 +213,17 @@ class SlabStepper:
         ``exchange`` (the gloo-testable path).
 
         ``transport`` (native only): ``"p2p"`` fuses the halo exchange into
-        the step kernel -- edge rows are stored straight into the neighbours'
-        ghost rows over peer memory (CUDA IPC) and signalled with release
-        stores, one launch per block; ``"nccl"`` runs boundary kernel ->
+        the step kernel -- the edge warps pull the rows beyond the slab
+        straight from the neighbours' input buffers over peer memory (CUDA
+        IPC), after acquiring their ready words, and publish their own with
+        release stores; one launch per block, no ghost-row copies; ``"nccl"`` runs boundary kernel ->
         NCCL send/recv on a comm stream || interior kernel; ``"auto"``
         (default) is p2p unless some rank cannot map its neighbours' memory,
         then NCCL on every rank (``self.transport`` says which).  ``attach=False``
         leaves the ring to the caller (in-process rings, see ``attach_peers``).
-        ``exact_blowup`` keeps a device copy of each advance's input so a
-        blow-up is reported at its exact iteration (see ``advance``)."""
+        ``exact_blowup`` keeps a recent checkpoint of the slab (teed by the
+        first block's kernel, refreshed every 2048 iterations) so a blow-up
+        is replayed to its exact iteration (see ``advance``)."""
         if global_rows % world:
             raise ValueError(f"global rows {global_rows} not divisible by world size {world}")
         self._lib = load()
