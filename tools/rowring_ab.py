@@ -1,10 +1,9 @@
-"""A/B of the row-ring kernel (fhn_rowring.cuh) against the wavefront kernel:
-device Mcell-updates/s and the device checksum of the same run, per variant.
+"""A/B of kernel paths chosen from the environment (one process per
+variant): device Mcell-updates/s and the device checksum of the same run.
 
-Each variant runs in its own process (the path is chosen from the
-environment once per process):
-  RDCNN_ROWRING=0              wavefront kernel (halo lanes)
-  RDCNN_ROWRING=1 RDCNN_RR_M=m row-ring, m warps per CTA
+  --m 0,8,16          RDCNN_ROWRING=0 (wavefront) vs the row-ring kernel with M warps per CTA
+  --variants "wf:RDCNN_RESIDENT=0;res2:RDCNN_RESIDENT=2,RDCNN_RES_K=2"
+                      arbitrary named environments (the first is the checksum reference)
 
   python tools/rowring_ab.py --shapes 4096x4096,8192x8192 --iters 20000 --m 0,4,8,16
 """
@@ -59,7 +58,22 @@ def main():
     ap.add_argument("--mode", default="strict")
     ap.add_argument("--m", default="0,8")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--variants", default=None)
     a = ap.parse_args()
+    if a.variants:
+        vs = []
+        for item in a.variants.split(";"):
+            name, _, envs = item.partition(":")
+            vs.append((name, dict(kv.split("=", 1) for kv in envs.split(",") if kv)))
+        for shape in a.shapes.split(","):
+            rows, cols = (int(x) for x in shape.split("x"))
+            base = None
+            for name, env in vs:
+                r = run(env, rows, cols, a.batch, a.iters, a.typ, a.mode, a.reps)
+                base = base or r
+                print(f"{shape} {a.mode} {name}: {json.dumps(r)} same_as_first={r.get('checksum') == base.get('checksum')}",
+                      flush=True)
+        return
     for shape in a.shapes.split(","):
         rows, cols = (int(x) for x in shape.split("x"))
         base = None
