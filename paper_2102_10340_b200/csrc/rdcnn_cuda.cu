@@ -26,7 +26,6 @@
 
 #include "analysis.cuh"
 #include "fhn_cluster.cuh"
-#include "fhn_resident.cuh"
 #include "fhn_rowring.cuh"
 #include "fhn_stencil.cuh"
 #include "rdcnn_cuda.h"
@@ -550,8 +549,6 @@ struct rdcnn_sim {
   int seg_force = 0;                // set while an autotune candidate runs
   int cluster_mode = 0;       // persistent cluster path: 0 auto, 1 required, -1 off
   long long* d_first_bad = nullptr;  // cluster path result word
-  void* res_buf = nullptr;           // resident path: exchange slots + flags + blow-up word
-  size_t res_bytes = 0;
   std::map<std::pair<long, int>, cudaGraphExec_t> graphs;  // captured advances by (steps, start buffer)
   int sm_count = 148;
   unsigned slab_tag = 0;
@@ -915,7 +912,6 @@ void free_all(rdcnn_sim* s) {
   for (void* p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   if (s->p2p_words) cudaFree(s->p2p_words);
   if (s->d_first_bad) cudaFree(s->d_first_bad);
-  if (s->res_buf) cudaFree(s->res_buf);
   for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
   s->graphs.clear();
   if (s->ckpt) cudaFree(s->ckpt);
@@ -1439,135 +1435,6 @@ int cluster_advance_tuned(rdcnn_sim* s, const std::vector<ClusterPlan>& plans, l
   return rc;
 }
 
-// ---- resident path (fhn_resident.cuh): mid-size lattices in shared memory ----
-// One cooperative launch per advance; each CTA keeps R rows (+ K halo rows
-// each side) of the torus in shared memory.  RDCNN_RESIDENT=1 uses it where
-// it fits, =2 also fails advances that cannot take it (tests), =0 never;
-// RDCNN_RES_K pins the levels per exchange (1, 2 or 4).
-int resident_setting() {
-  static const int v = [] {
-    const char* e = std::getenv("RDCNN_RESIDENT");
-    return e && (e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 0;
-  }();
-  return v;
-}
-
-struct ResidentPlan {
-  int R = 0, P = 0, K = 2;
-  size_t smem = 0;
-};
-
-using ResidentFn = void (*)(rdcnn_dev::ResidentArgs);
-
-ResidentFn resident_fn(int k, int arith) {
-  using namespace rdcnn_dev;
-  static const ResidentFn t[3][3] = {
-      {&fhn_resident_kernel<1, 0>, &fhn_resident_kernel<1, 1>, &fhn_resident_kernel<1, 2>},
-      {&fhn_resident_kernel<2, 0>, &fhn_resident_kernel<2, 1>, &fhn_resident_kernel<2, 2>},
-      {&fhn_resident_kernel<4, 0>, &fhn_resident_kernel<4, 1>, &fhn_resident_kernel<4, 2>}};
-  return t[k == 1 ? 0 : k == 2 ? 1 : 2][arith];
-}
-
-bool resident_plan(rdcnn_sim* s, ResidentPlan& pl) {
-  if (resident_setting() == 0 || s->slab || s->batch != 1 || s->elem != 4 || s->params_stride != 0) return false;
-  const int G = s->cols / 4;
-  if (s->cols % 4 != 0 || G < 32 || G > rdcnn_dev::kResidentThreads) return false;
-  int K = 2;
-  if (const char* e = std::getenv("RDCNN_RES_K")) K = std::atoi(e);
-  if (K != 1 && K != 2 && K != 4) K = 2;
-  int R = std::max(K, (s->rows + s->sm_count - 1) / s->sm_count);
-  for (;; ++R) {
-    const int P = (s->rows + R - 1) / R;
-    if (s->rows - (P - 1) * R >= K || P == 1) break;
-  }
-  const int P = (s->rows + R - 1) / R;
-  if (s->rows < 2 * K || (P == 1 && s->rows < K)) return false;
-  const size_t smem = rdcnn_dev::resident_smem_bytes(R, K, s->cols);
-  if (smem > 224 * 1024) return false;
-  pl.R = R;
-  pl.P = P;
-  pl.K = K;
-  pl.smem = smem;
-  return true;
-}
-
-int resident_advance(rdcnn_sim* s, const ResidentPlan& pl, long steps, long* first_bad, bool* fell_back) {
-  *fell_back = false;
-  const size_t xfloats = (size_t)pl.P * 2 * 2 * pl.K * 2 * (size_t)s->cols;
-  const size_t need = xfloats * sizeof(float) + sizeof(unsigned) * ((size_t)pl.P + 1);
-  if (s->res_bytes < need) {
-    if (s->res_buf) cudaFree(s->res_buf);
-    s->res_buf = nullptr;
-    s->res_bytes = 0;
-    RDCNN_CUDA_TRY(cudaMalloc(&s->res_buf, need));
-    s->res_bytes = need;
-  }
-  rdcnn_dev::ResidentArgs a{};
-  a.u_in = s->u_ptr<float>(s->cur);
-  a.v_in = s->v_ptr<float>(s->cur);
-  a.u_out = s->u_ptr<float>(s->cur ^ 1);
-  a.v_out = s->v_ptr<float>(s->cur ^ 1);
-  a.rows = s->rows;
-  a.cols = s->cols;
-  a.R = pl.R;
-  a.P = pl.P;
-  a.steps = steps;
-  a.p = s->h_params_f;
-  a.xbuf = static_cast<float*>(s->res_buf);
-  a.flags = reinterpret_cast<unsigned*>(static_cast<float*>(s->res_buf) + xfloats);
-  a.bad = a.flags + pl.P;
-  ResidentFn fn = resident_fn(pl.K, arith_for<float>(s));
-  {
-    static std::mutex mu;
-    std::lock_guard<std::mutex> lock(mu);
-    RDCNN_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-  }
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.gridDim = dim3((unsigned)pl.P);
-  cfg.blockDim = dim3((unsigned)rdcnn_dev::kResidentThreads);
-  cfg.dynamicSmemBytes = pl.smem;
-  cfg.stream = s->stream;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  RDCNN_CUDA_TRY(cudaMemsetAsync(a.flags, 0, sizeof(unsigned) * ((size_t)pl.P + 1), s->stream));
-  RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
-  {
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
-    if (e != cudaSuccess) {
-      // The grid could not be made co-resident right now (SMs held by
-      // another context): the wavefront path takes over, state untouched.
-      cudaGetLastError();
-      if (resident_setting() < 2) {
-        *fell_back = true;
-        return RDCNN_OK;
-      }
-      return fail(RDCNN_ECUDA, "resident launch failed: %s", cudaGetErrorString(e));
-    }
-  }
-  RDCNN_CUDA_TRY(cudaEventRecord(s->ev1, s->stream));
-  unsigned bad = 0;
-  RDCNN_CUDA_TRY(cudaMemcpyAsync(&bad, a.bad, sizeof bad, cudaMemcpyDeviceToHost, s->stream));
-  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
-  float ms = 0;
-  RDCNN_CUDA_TRY(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
-  if (bad) {
-    // Blow-up: the input (buffer cur) is untouched; the wavefront path
-    // re-runs the advance and finds the exact iteration.
-    const int rc = advance_launches<float>(s, steps, first_bad);
-    s->last_ms += ms;
-    s->launches += 1;
-    return rc;
-  }
-  s->last_ms = ms;
-  s->launches = 1;
-  s->cur ^= 1;
-  if (first_bad) first_bad[0] = 0;
-  return RDCNN_OK;
-}
-
 template <class T>
 int advance_impl(rdcnn_sim* s, long steps, long* first_bad) {
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
@@ -1580,15 +1447,6 @@ int advance_impl(rdcnn_sim* s, long steps, long* first_bad) {
     }
     if (s->cluster_mode > 0) return fail(RDCNN_EINVAL, "persistent cluster path required but %dx%d (batch %d) does not fit it",
                                          s->rows, s->cols, s->batch);
-    ResidentPlan rp;
-    if (steps > 0 && resident_plan(s, rp)) {
-      bool fell_back = false;
-      const int rc = resident_advance(s, rp, steps, first_bad, &fell_back);
-      if (!fell_back) return rc;
-    } else if (steps > 0 && resident_setting() == 2) {
-      return fail(RDCNN_EINVAL, "resident path required but %dx%d (batch %d) does not fit it", s->rows, s->cols,
-                  s->batch);
-    }
   }
   return advance_launches<T>(s, steps, first_bad);
 }
