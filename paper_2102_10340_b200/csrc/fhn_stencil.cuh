@@ -93,6 +93,11 @@ struct StepArgsT {
   // (trace_stride 5, kPeer instances).
   unsigned long long* trace;
   int trace_stride;
+  // TMA tensor-map staging (RDCNN_BULK=2 builds): a 3-D map {cols, rows x
+  // batch, 2 planes} of this launch's input buffer with a {128, 1, 2} box --
+  // one band row of both planes -- built by the host (cuTensorMapEncodeTiled).
+  int tma_ok;
+  alignas(64) unsigned char tmap[128];
 };
 
 // Per-warp profile of one block (kPeer traces).
@@ -435,6 +440,19 @@ __device__ __forceinline__ void bulk_wait(uint32_t mbar, uint32_t parity) {
       : "memory");
 }
 
+// One band row of both planes by the TMA engine from the tensor map (UTMALDG):
+// box {128 columns, 1 row, 2 planes} at column x, stacked row y.
+__device__ __forceinline__ void tma_stage_row(uint32_t dst, const void* tmap, int x, int y, uint32_t mbar) {
+  if (elect_one()) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 1024;\n" ::"r"(mbar) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(0), "r"(mbar)
+        : "memory");
+  }
+  __syncwarp();
+}
+
 // ---- peer ring synchronisation (kPeer) --------------------------------------
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   unsigned v;
@@ -624,6 +642,11 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
   uint32_t bytes_a = 32u * kLaneBytes, bytes_b = 0;
   ptrdiff_t d_b = 0;
   const T* ub = nullptr;  // uniform running source row (lane 0's group)
+  // Tensor-map staging (RDCNN_BULK=2): bands that do not wrap the torus
+  // column edge take one UTMALDG per row; the edge bands keep the two-piece
+  // 1-D bulk copies.  y is the stacked row (grid g's row r at g*rows + r).
+  bool use_tma = false;
+  int tma_x = 0, tma_y = 0;
   if constexpr (kBulk) {
     const int gl0 = band * a.band_groups - a.halo_groups;  // lane 0's column group
     const int grp0 = wrap_index(gl0, G);
@@ -634,6 +657,9 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
     bytes_b = 32u * kLaneBytes - bytes_a;
     d_b = -(ptrdiff_t)grp0 * W;  // group 0 relative to lane 0's group
     ub = u_in_b + (size_t)g * (size_t)a.grid_stride + (size_t)grp0 * W + (size_t)r_first * pitch;
+    use_tma = RDCNN_BULK == 2 && a.tma_ok && bytes_b == 0 && a.periodic;
+    tma_x = grp0 * W;
+    tma_y = g * a.rows + r_first;
     if (elect_one()) {
 #pragma unroll
       for (int q = 0; q < kStage; ++q)
@@ -644,9 +670,15 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
   }
   auto stage = [&](uint32_t slot, uint32_t mb) {  // slot: the lane-0 (base) address
     if constexpr (kBulk) {
-      bulk_stage_row<T>(slot, ub, vdelta, bytes_a, d_b, bytes_b, mb);
-      ub += pitch;
-      if (rows_left == 1) ub -= span;  // same wrap point as su (src_next)
+      if (use_tma) {
+        tma_stage_row(slot, a.tmap, tma_x, tma_y, mb);
+        ++tma_y;
+        if (rows_left == 1) tma_y -= a.rows;  // same wrap point as su (src_next)
+      } else {
+        bulk_stage_row<T>(slot, ub, vdelta, bytes_a, d_b, bytes_b, mb);
+        ub += pitch;
+        if (rows_left == 1) ub -= span;  // same wrap point as su (src_next)
+      }
     } else {
       stage_row<W, T>(slot + lane * kLaneStride, su, su + vdelta, 0);
     }
@@ -825,7 +857,7 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
 template <int K, int W, class T, int kArith, bool kPerGrid, bool kPeer = false, bool kWrap = false,
           bool kTee = false>
 __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T, W>::value)
-    fhn_wavefront_kernel(const StepArgsT<T> a) {
+    fhn_wavefront_kernel(const __grid_constant__ StepArgsT<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = kWarpsPerCta == 1 ? 0 : int(threadIdx.x >> 5);

@@ -5,7 +5,9 @@
 //        -fmad=false -prec-div=true -ftz=false -shared -Xcompiler -fPIC
 // (see __graft_entry__.build()).  Strict arithmetic relies on -ftz=false
 // (reference keeps subnormals, SURVEY.md §7 "Denormals").
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -544,6 +546,8 @@ struct rdcnn_sim {
   long launches = 0;
   int max_levels = 4;
   int seg_rows = 0;
+  bool tma_ok = false;              // RDCNN_BULK=2 builds: tensor maps of both buffers
+  alignas(64) unsigned char tmap[2][128];
   int tuned_seg[4] = {0, 0, 0, 0};  // autotuned segment height per K (0: not tuned)
   bool tuned[4] = {false, false, false, false};
   int seg_force = 0;                // set while an autotune candidate runs
@@ -640,6 +644,8 @@ StepArgsT<T> base_args(rdcnn_sim* s, int in_buf, int out_buf) {
   a.params = static_cast<const ParamsT<T>*>(s->d_params);
   a.params_stride = s->params_stride;
   a.flags = s->d_flags;
+  a.tma_ok = s->tma_ok ? 1 : 0;
+  if (s->tma_ok) std::memcpy(a.tmap, s->tmap[in_buf], sizeof a.tmap);
   return a;
 }
 
@@ -1479,6 +1485,37 @@ int copy_state(rdcnn_sim* s, void* u, void* v, bool upload) {
   return RDCNN_OK;
 }
 
+// Tensor maps of the two state buffers for TMA staging (RDCNN_BULK=2
+// builds): {cols, rows x batch, 2 planes} fp32 with a {128, 1, 2} box, i.e.
+// one 32-lane band row of both planes.  Periodic fp32 handles whose rows
+// hold at least one band; the driver entry point is resolved at run time.
+int make_tensor_maps(rdcnn_sim* s) {
+  if (s->slab || s->cols % 4 != 0 || s->cols < 128) return RDCNN_OK;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return fail(RDCNN_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  for (int b = 0; b < 2; ++b) {
+    const cuuint64_t dims[3] = {(cuuint64_t)s->cols, (cuuint64_t)s->rows * (cuuint64_t)s->batch, 2};
+    const cuuint64_t strides[2] = {(cuuint64_t)s->pitch * 4,
+                                   (cuuint64_t)((char*)s->v_ptr<float>(b) - (char*)s->u_ptr<float>(b))};
+    const cuuint32_t box[3] = {128, 1, 2};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMap* m = reinterpret_cast<CUtensorMap*>(s->tmap[b]);
+    const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, s->u_ptr<float>(b), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(RDCNN_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  }
+  s->tma_ok = true;
+  return RDCNN_OK;
+}
+
 int create_impl(int rows, int cols, int batch, int device, int mode, int elem, rdcnn_sim_t* out) {
   if (!out) return fail(RDCNN_EINVAL, "null output handle");
   *out = nullptr;
@@ -1500,6 +1537,7 @@ int create_impl(int rows, int cols, int batch, int device, int mode, int elem, r
   s->buf_elems = (size_t)rows * cols * batch * 2;
   s->max_levels = 4;
   int rc = alloc_common(s);
+  if (rc == RDCNN_OK && RDCNN_BULK == 2 && elem == 4) rc = make_tensor_maps(s);
   if (rc != RDCNN_OK) {
     std::string msg = g_last_error;
     free_all(s);
