@@ -387,7 +387,9 @@ __device__ __forceinline__ void read_staged(uint32_t src, Row<W, T>& r) {
 // (two pieces where the band wraps around the torus edge), so lane 0 stages
 // it with cp.async.bulk (the TMA engine) and the completion is counted on a
 // per-slot mbarrier; every lane waits on the barrier instead of its own
-// cp.async group.  Built with -DRDCNN_BULK=1 only: measured 6 % SLOWER than
+// cp.async group.  -DRDCNN_BULK=2 stages the bands that do not wrap with one
+// tensor-map copy (UTMALDG, both planes) per row instead: 8 % slower
+// (4096^2 822k vs 893k).  Built with -DRDCNN_BULK=1 only: measured 6 % SLOWER than
 // per-lane cp.async (4096^2: 785k vs 833k; batched 128^2: 876k vs 932k) --
 // the elected copy, expect_tx and per-slot waits cost more issue slots than
 // two LDGSTS per lane in an issue-bound kernel (profiles/README.md).
