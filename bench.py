@@ -264,6 +264,16 @@ class ClockSampler:
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+        # nvidia-smi takes a few hundred ms to start: wait (before the timed
+        # region opens) until it has written its first sample, so that short
+        # regions (cfg1) are sampled too.
+        t_end = time.time() + 3.0
+        while self.proc is not None and time.time() < t_end and self.proc.poll() is None:
+            if os.path.getsize(self.path) > 0:
+                break
+            time.sleep(0.02)
+        with open(self.path) as f:
+            self.skip = len(f.readlines())  # samples taken before the region: not counted
         return self
 
     def __exit__(self, *exc):
@@ -280,29 +290,35 @@ class ClockSampler:
         sm, mx, pw, lim, reasons = [], [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         with open(self.path) as f:
-            for line in f:
-                p = [x.strip() for x in line.split(",")]
-                if len(p) < 9:
-                    continue
-                try:
-                    sm.append(float(p[1]))
-                    mx.append(float(p[2]))
-                except ValueError:
-                    continue
-                try:
-                    pw.append(float(p[3]))
-                    lim.append(float(p[9]))
-                except (ValueError, IndexError):
-                    pass
-                for name, val in zip(names, p[5:9]):
-                    if val.lower() == "active":
-                        reasons.add(name)
+            lines = f.readlines()
+        # The region's samples; a region shorter than the 100 ms period falls
+        # back to the last sample before it (and says so).
+        in_region = lines[getattr(self, "skip", 0):]
+        pre_region = not in_region
+        for line in in_region or lines[-1:]:
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx.append(float(p[2]))
+            except ValueError:
+                continue
+            try:
+                pw.append(float(p[3]))
+                lim.append(float(p[9]))
+            except (ValueError, IndexError):
+                pass
+            for name, val in zip(names, p[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
         os.unlink(self.path)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
                 "samples": len(sm),
                 "power_w": round(statistics.median(pw), 1) if pw else None,
-                "power_limit_w": max(lim) if lim else None}
+                "power_limit_w": max(lim) if lim else None,
+                **({"pre_region_sample": True} if pre_region and sm else {})}
 
 
 def ncu_traffic():
