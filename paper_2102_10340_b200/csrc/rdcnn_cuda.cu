@@ -1778,23 +1778,47 @@ int normalize_impl(rdcnn_sim* s, const void* src_dev, double lo, double hi, uint
 
 // checksum / fnv1a (grid.hpp:100-126) of every grid of a batch on the device:
 // one thread per grid, FNV-1a 64 over the raw bytes of its u plane then its v
-// plane -- sequential within a grid, independent across grids.
+// plane -- sequential within a grid, independent across grids.  The hash is
+// a dependent chain (XOR, multiply) per byte, so the loads are software-
+// pipelined kDepth x 16 bytes ahead: the next chunk is in flight while the
+// current one is hashed (the 4096-grid cfg4 digest: 85 ms -> a few ms).
+constexpr int kFnvDepth = 8;
+
+__device__ __forceinline__ unsigned long long fnv_word(unsigned long long h, unsigned w) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) h = (h ^ ((w >> (8 * k)) & 0xFFu)) * 0x100000001b3ull;
+  return h;
+}
+
 __global__ void fnv_batch_kernel(const unsigned char* __restrict__ u, const unsigned char* __restrict__ v,
                                  size_t plane_bytes, size_t grid_stride_bytes, int batch,
                                  unsigned long long* __restrict__ out) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= batch) return;
   unsigned long long h = 0xcbf29ce484222325ull;
+  const size_t n16 = plane_bytes / 16;  // the caller guarantees plane_bytes % 16 == 0
   for (const unsigned char* plane : {u, v}) {
-    const unsigned char* p = plane + (size_t)g * grid_stride_bytes;
-    size_t i = 0;
-    for (; i + 16 <= plane_bytes; i += 16) {
-      const uint4 w = __ldg(reinterpret_cast<const uint4*>(p + i));
-      for (unsigned word : {w.x, w.y, w.z, w.w})
+    const uint4* p = reinterpret_cast<const uint4*>(plane + (size_t)g * grid_stride_bytes);
+    uint4 cur[kFnvDepth];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) h = (h ^ ((word >> (8 * k)) & 0xFFu)) * 0x100000001b3ull;
+    for (int k = 0; k < kFnvDepth; ++k) cur[k] = (size_t)k < n16 ? __ldcs(p + k) : make_uint4(0, 0, 0, 0);
+    for (size_t i = 0; i < n16; i += kFnvDepth) {
+      uint4 nxt[kFnvDepth];
+#pragma unroll
+      for (int k = 0; k < kFnvDepth; ++k)
+        nxt[k] = i + kFnvDepth + k < n16 ? __ldcs(p + i + kFnvDepth + k) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int k = 0; k < kFnvDepth; ++k) {
+        if (i + k < n16) {
+          h = fnv_word(h, cur[k].x);
+          h = fnv_word(h, cur[k].y);
+          h = fnv_word(h, cur[k].z);
+          h = fnv_word(h, cur[k].w);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kFnvDepth; ++k) cur[k] = nxt[k];
     }
-    for (; i < plane_bytes; ++i) h = (h ^ p[i]) * 0x100000001b3ull;
   }
   out[g] = h;
 }
