@@ -1,5 +1,5 @@
 // fhn_rowring.cuh -- the K-level wavefront with NO halo lanes: one thread-
-// block cluster covers a whole torus row (DESIGN.md §3b).
+// block cluster covers a whole torus row (DESIGN.md §3c).
 //
 // The wavefront kernel (fhn_stencil.cuh) gives every warp its own 32-lane
 // column band; the outermost lane on each side is halo (its columns go stale
@@ -12,19 +12,20 @@
 //   * all warps of the cluster share one row segment and march down it in
 //     the same skewed wavefront (same tick sequence);
 //   * level-0 rows are staged by cp.async into a CTA-wide row buffer (the
-//     CTA's 32*M column groups plus one halo group each side, staged by the
-//     CTA's first/last lane from the wrapped neighbouring columns), so every
-//     lane reads its left/right level-0 neighbours from shared memory;
+//     CTA's 32*M column groups plus one pad entry each side, filled with the
+//     ring neighbours' edge columns), so every lane reads its left/right
+//     level-0 neighbours from shared memory;
 //   * levels 1..K-1: every lane publishes the first and last column (u, v)
 //     of each row it produces as one STS.128 into that row's edge slot and
 //     reads its neighbours' 8-byte halves when that row is the center row of
 //     the level above (two ticks later): one STS.128 + two LDS.64 replace
 //     the four SHFLs per row of the wavefront kernel, and warp boundaries
 //     cost nothing extra;
-//   * the CTA's first/last lane also sends its edge half into the ring
-//     neighbour CTA's pad entry by st.async, counting the bytes on the
-//     receiver's mbarrier (complete_tx): DSMEM over the cluster, no fences;
-//     the ring wraps the torus column edge;
+//   * once per tick the CTA's first/last lane sends its edge entries (and
+//     the next staged row's two edge values) into the ring neighbour CTA's
+//     pad entries by st.async, counting the bytes on the receiver's mbarrier
+//     (complete_tx): DSMEM over the cluster, no fences; the ring wraps the
+//     torus column edge (a one-CTA ring writes its own pads directly);
 //   * one mbarrier per tick slot (ring of 3: slot = tick % 3, a compile-time
 //     offset in the 3-unrolled tick loop) completes when all 32*M threads of
 //     the CTA have arrived (release: after this tick's stores, reads and the
@@ -81,17 +82,6 @@ __device__ __forceinline__ void sts_v4u(uint32_t addr, float a, float b, float c
 __device__ __forceinline__ void lds_v2(uint32_t addr, float& a, float& b) {
   asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n" : "=f"(a), "=f"(b) : "r"(addr) : "memory");
 }
-// st.async of one 16-byte edge entry into a cluster peer's shared memory,
-// issued only where `on` (a predicate, not a branch: the loop stays
-// convergent).
-__device__ __forceinline__ void stas_v4_if(uint32_t addr, float a, float b, float c, float d, uint32_t mbar,
-                                           bool on) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.u32 p, %6, 0;\n"
-      "@p st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];\n}\n" ::"r"(addr),
-      "f"(a), "f"(b), "f"(c), "f"(d), "r"(mbar), "r"((unsigned)on)
-      : "memory");
-}
 // Every thread arrives; `bytes` (non-zero in one thread) is the tick's
 // expected DSMEM transaction count.
 __device__ __forceinline__ void mbar_arrive_tx(uint32_t mbar, unsigned bytes) {
@@ -102,6 +92,14 @@ __device__ __forceinline__ void stas_v4(uint32_t addr, const Row<4, float>& r, u
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];\n"
                ::"r"(addr), "f"(r.u[0]), "f"(r.v[0]), "f"(r.u[3]), "f"(r.v[3]), "r"(mbar)
                : "memory");
+}
+__device__ __forceinline__ void sts_row_edges(uint32_t addr, const Row<4, float>& r) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "f"(r.u[0]), "f"(r.v[0]), "f"(r.u[3]),
+               "f"(r.v[3])
+               : "memory");
+}
+__device__ __forceinline__ void sts_f32(uint32_t addr, float x) {
+  asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(addr), "f"(x) : "memory");
 }
 __device__ __forceinline__ void stas_f32(uint32_t addr, float x, uint32_t mbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(addr),
@@ -118,12 +116,6 @@ __device__ __forceinline__ void mbar_wait_cta(uint32_t mbar, unsigned parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
       "@!P bra WAITR_%=;\n"
       "}\n" ::"r"(mbar), "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void cp_async16_if(uint32_t dst, const void* src, bool on) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.u32 p, %2, 0;\n@p cp.async.cg.shared.global [%0], [%1], 16;\n}\n" ::"r"(dst),
-      "l"(src), "r"((unsigned)on)
       : "memory");
 }
 __device__ __forceinline__ void lds_v4f(uint32_t addr, float (&x)[4]) {
@@ -354,24 +346,41 @@ __global__ void __launch_bounds__(32 * M, 16 / M) fhn_rowring_kernel(const StepA
     const bool s0 = j + 1 < n_load;
     if (halo_lane) {
       // Ring neighbour sends: the level rows produced this tick, then the
-      // next staged row's two edge values.
+      // next staged row's two edge values.  A one-CTA ring (C == 1) wraps
+      // onto itself: plain shared stores, released by the arrival below
+      // (st.async needs a cluster of at least two CTAs).
       const uint32_t mb = mbar0 + kMb + rem;
-      if (l1) stas_v4(e_own + kW + rem - 16u * (uint32_t)(li + 1) + e_pad, win[0][ph], mb);
-#pragma unroll
-      for (int t = 2; t < K; ++t)
-        if (j >= 3 * t - 1 && j - (h + 2 * K - 1) < t)
-          stas_v4(ebase + kW + (uint32_t)(t - 1) * kRow + rem + e_pad, win[t - 1][ph], mb);
+      float eu = 0.0f, ev = 0.0f;
       if (s0) {
-        float eu, ev;
         lds(nxt + s_own + v_off, eu);
         lds(nxt + kRow + s_own + v_off, ev);
-        stas_f32(nxt + e_pad + v_off + rem, eu, mb);
-        stas_f32(nxt + kRow + e_pad + v_off + rem, ev, mb);
+      }
+      if (C > 1) {
+        if (l1) stas_v4(ebase + kW + rem + e_pad, win[0][ph], mb);
+#pragma unroll
+        for (int t = 2; t < K; ++t)
+          if (j >= 3 * t - 1 && j - (h + 2 * K - 1) < t)
+            stas_v4(ebase + kW + (uint32_t)(t - 1) * kRow + rem + e_pad, win[t - 1][ph], mb);
+        if (s0) {
+          stas_f32(nxt + e_pad + v_off + rem, eu, mb);
+          stas_f32(nxt + kRow + e_pad + v_off + rem, ev, mb);
+        }
+      } else {
+        if (l1) sts_row_edges(ebase + kW + e_pad, win[0][ph]);
+#pragma unroll
+        for (int t = 2; t < K; ++t)
+          if (j >= 3 * t - 1 && j - (h + 2 * K - 1) < t)
+            sts_row_edges(ebase + kW + (uint32_t)(t - 1) * kRow + e_pad, win[t - 1][ph]);
+        if (s0) {
+          sts_f32(nxt + e_pad + v_off, eu);
+          sts_f32(nxt + kRow + e_pad + v_off, ev);
+        }
       }
     }
     // Done with this tick's stores, reads and row j+1's copy: arrive (thread
     // 0 also expects both ring neighbours' bytes for this tick).
-    mbar_arrive_tx(mbar0 + kMb, threadIdx.x == 0 ? 2u * (16u * sends + (s0 ? 8u : 0u)) : 0u);
+    const unsigned tx = C > 1 ? 2u * (16u * sends + (s0 ? 8u : 0u)) : 0u;
+    mbar_arrive_tx(mbar0 + kMb, threadIdx.x == 0 ? tx : 0u);
   };
 
   for (int j0 = 0; j0 < nt; j0 += 3) {
