@@ -162,3 +162,24 @@ def test_batch_gene_narrowing_equals_c_abi():
     assert isinstance(b64[0], ParamsF64)
     got64 = np.array([[getattr(b64[k], f) for f in fields] for k in range(len(genes))])
     assert np.array_equal(got64, np.array([g.to_vector() for g in genes]))
+
+
+# The C++ drop-in headers mirror the reference's: each one compiles on its
+# own (its include graph is complete), as a reference translation unit that
+# includes only, say, rdcnn/kernels.hpp expects.
+HEADERS = ["gene", "grid", "rng", "model", "backend", "config", "init", "kernels", "engine", "bench", "sweep",
+           "cuda_api"]
+
+
+@pytest.mark.parametrize("name", HEADERS)
+def test_cpp_header_compiles_standalone(tmp_path, name):
+    import shutil
+    import subprocess
+    cxx = shutil.which("g++")
+    if cxx is None:
+        pytest.skip("no g++")
+    src = tmp_path / f"t_{name}.cpp"
+    src.write_text(f'#include "rdcnn/{name}.hpp"\nint main() {{ return 0; }}\n')
+    r = subprocess.run([cxx, "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), str(src)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
