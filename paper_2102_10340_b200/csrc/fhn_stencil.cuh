@@ -98,11 +98,6 @@ struct StepArgsT {
   // one band row of both planes -- built by the host (cuTensorMapEncodeTiled).
   int tma_ok;
   alignas(64) unsigned char tmap[128];
-  // Skewed (parallelogram) segments (kPara instances, periodic): per warp,
-  // its bottom two rows of levels 1..K-1 for the segment below, and a word
-  // raised to 1 when they are written (the consumer resets it to 0).
-  T* xbuf;
-  unsigned* xflag;
 };
 
 // Per-warp profile of one block (kPeer traces).
@@ -460,16 +455,6 @@ __device__ __forceinline__ void tma_stage_row(uint32_t dst, const void* tmap, in
   __syncwarp();
 }
 
-// GPU-scope release/acquire words (kPara segment exchange).
-__device__ __forceinline__ void st_release_gpu_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
 // ---- peer ring synchronisation (kPeer) --------------------------------------
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   unsigned v;
@@ -528,23 +513,13 @@ struct MinBlocks {
 // returns whether a stored value was non-finite (folded over the warp).
 // (A persistent variant that looped over blocks, each warp waiting only for
 // its 8 neighbours, measured 2.5 % slower than launches + PDL: profiles/.)
-template <int K, int W, class T, int kArith, bool kPerGrid, bool kPeer, bool kWrap, bool kTee, bool kPara = false>
+template <int K, int W, class T, int kArith, bool kPerGrid, bool kPeer, bool kWrap, bool kTee>
 __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned char* smem_raw, int lane, int wib,
                                                 int g, int band, int seg, unsigned frozen,
                                                 const T* __restrict__ u_in_b, const T* __restrict__ v_in_b,
                                                 T* __restrict__ u_out_b, T* __restrict__ v_out_b,
                                                 BlockStats& stats) {
   static_assert(!kTee || (kPeer && RDCNN_L0REG), "the checkpoint tee is a slab (kPeer) feature");
-  // kPara: skewed segments ("parallelogram segments").  Level t
-  // covers rows [r0-K+t, r0+h-K+t) -- h rows at every level, none
-  // recomputed.  Its bottom rows at level t need two level-(t-1) rows below
-  // its range: the top two rows of the segment below at that level, which
-  // that warp computes in its first ticks and publishes (xbuf, xflag); this
-  // warp reads them only at the end of its (top-down) sweep.  The trapezoid
-  // (kPara false) instead recomputes K-t extra rows at each end of every
-  // level (the 2K-row segment start-up).
-  static_assert(!kPara || (!kPeer && !kTee && RDCNN_L0REG && !BulkStage<W, T>::value && K >= 2),
-                "skewed segments: periodic K >= 2 instances with the register level-0 ring");
   // Shared gene: read straight from the kernel-parameter bank.  Per-grid
   // genes (sweeps) come from global memory once per warp.
   const ParamsT<T> p = kPerGrid ? a.params[g] : a.shared;
@@ -569,7 +544,7 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
 
   const int r0 = a.row_begin + seg * a.seg_rows;
   const int h = min(a.seg_rows, a.row_end - r0);
-  const int n_load = kPara ? h + 2 : h + 2 * K;  // level-0 rows x_0 .. x_{n_load-1}
+  const int n_load = h + 2 * K;       // level-0 rows x_0 .. x_{n_load-1}
   const int nt = h + 3 * K - 1;       // ticks until level K has produced h rows
 
   // Fused exchange: a warp reads the previous (next) rank's last (first)
@@ -647,49 +622,6 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
     }
   };
   T* du = uout + (size_t)(a.periodic ? r0 : r0 + a.ghost) * pitch;
-  // kPara exchange: this warp's slots and the slots/word of the warp that
-  // owns the same band one segment down (the torus wraps the last segment to
-  // segment 0).  Computed where used (a few ticks per launch), not kept live.
-  constexpr int kXWarp = (K > 1 ? K - 1 : 1) * 2 * 2 * 32 * W;  // [level][row][plane][lane][W]
-  auto warp_me = [&]() {
-    return (long long)g * ((long long)a.n_segs * a.n_bands) + (long long)seg * a.n_bands + band;
-  };
-  auto warp_up = [&]() {  // the segment BELOW, whose top rows this one needs
-    return (long long)g * ((long long)a.n_segs * a.n_bands) + (long long)(seg + 1 == a.n_segs ? 0 : seg + 1) * a.n_bands +
-           band;
-  };
-  auto fmine = [&]() { return a.xflag + warp_me(); };
-  auto fup = [&]() { return a.xflag + warp_up(); };
-  // Level t' (1..K-1) row `r` (0: the bottom row, 1: the one above) of a warp's slots.
-  auto xoff = [](int lvl, int r, int plane) { return ((((lvl - 1) * 2 + r) * 2 + plane) * 32) * W; };
-  auto publish = [&](const Row<W, T>& x, int lvl, int r) {
-    T* xmine = a.xbuf + warp_me() * kXWarp + lane * W;
-    if constexpr (W == 4 && sizeof(T) == 4) {
-      __stcg(reinterpret_cast<float4*>(xmine + xoff(lvl, r, 0)), make_float4(x.u[0], x.u[1], x.u[2], x.u[3]));
-      __stcg(reinterpret_cast<float4*>(xmine + xoff(lvl, r, 1)), make_float4(x.v[0], x.v[1], x.v[2], x.v[3]));
-    } else {
-#pragma unroll
-      for (int k = 0; k < W; ++k) {
-        __stcg(xmine + xoff(lvl, r, 0) + k, x.u[k]);
-        __stcg(xmine + xoff(lvl, r, 1) + k, x.v[k]);
-      }
-    }
-  };
-  auto fetch = [&](Row<W, T>& x, int lvl, int r) {
-    const T* xup = a.xbuf + warp_up() * kXWarp + lane * W;
-    if constexpr (W == 4 && sizeof(T) == 4) {
-      const float4 a4 = __ldcg(reinterpret_cast<const float4*>(xup + xoff(lvl, r, 0)));
-      const float4 b4 = __ldcg(reinterpret_cast<const float4*>(xup + xoff(lvl, r, 1)));
-      x.u[0] = a4.x; x.u[1] = a4.y; x.u[2] = a4.z; x.u[3] = a4.w;
-      x.v[0] = b4.x; x.v[1] = b4.y; x.v[2] = b4.z; x.v[3] = b4.w;
-    } else {
-#pragma unroll
-      for (int k = 0; k < W; ++k) {
-        x.u[k] = __ldcg(xup + xoff(lvl, r, 0) + k);
-        x.v[k] = __ldcg(xup + xoff(lvl, r, 1) + k);
-      }
-    }
-  };
   const ptrdiff_t vout_delta = vout - uout;
   // Checkpoint tee: the owned rows r0 .. r0+h-1 (level-0 rows of ticks
   // K .. K+h-1) go to the same place in a.tee_u.
@@ -782,19 +714,15 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
 
   // One tick.  PH = j % 3 (compile-time ring slot); kSteady = every level is
   // active in this tick, so the validity tests disappear.
-  auto tick = [&](auto ph_c, auto steady_c, auto edge_c, int j) {
+  auto tick = [&](auto ph_c, auto steady_c, int j) {
     constexpr int ph = decltype(ph_c)::value;
     constexpr bool kSteady = decltype(steady_c)::value;
-    // kEdge: this tick may publish or fetch skewed-segment rows (the first
-    // 3K and last few ticks); the middle ticks run a body without that code.
-    constexpr bool kEdge = kPara && decltype(edge_c)::value;
     // Levels K..2, top-down: level t reads the level-(t-1) rows of ticks
     // j-3, j-2, j-1 (slots ph, ph+1, ph+2 mod 3), then level t-1 overwrites
     // slot ph with its tick-j row.
 #pragma unroll
     for (int t = K; t >= 2; --t) {
-      // Active ticks: trapezoid [3t-1, h+2K+t-2]; skewed [3t-1, h+3t-2].
-      if (kSteady || (j >= 3 * t - 1 && (kPara ? j < h + 3 * t - 1 : j - (h + 2 * K - 1) < t))) {
+      if (kSteady || (j >= 3 * t - 1 && j - (h + 2 * K - 1) < t)) {
         const Row<W, T>& up = win[t - 2][ph];
         const Row<W, T>& ce = win[t - 2][(ph + 1) % 3];
         const Row<W, T>& dn = win[t - 2][(ph + 2) % 3];
@@ -861,43 +789,6 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
         level_row<W, T, kArith, kWrap>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
       }
     }
-    if constexpr (kEdge) {
-      // Publications (ticks 3..3(K-1), multiples of 3): at tick 3t both top
-      // rows of level t are in registers -- the one of tick 3t-1 (row 0,
-      // slot 2) and this tick's (row 1, slot 0).  Then raise the word.
-      if constexpr (ph == 0) {
-        if (j <= 3 * (K - 1)) {
-#pragma unroll
-          for (int tt = 1; tt < K; ++tt) {
-            if (j == 3 * tt) {
-              publish(win[tt - 1][2], tt, 0);
-              publish(win[tt - 1][0], tt, 1);
-            }
-          }
-          if (j == 3 * (K - 1)) {
-            __threadfence();
-            __syncwarp();
-            if (lane == 0) st_release_gpu_u32(fmine(), 1u);
-          }
-        }
-      }
-      // Fetches (ticks h+2 .. h+3(K-1)): the two level-t rows below this
-      // segment -- the segment below's top rows -- go where level t's rows of
-      // those ticks would be (level t+1 already read that slot this tick).
-      // Wait once for the segment below; finally reset its word for the next
-      // launch (this warp is its only reader).
-      if (j >= h + 2) {
-        if (j == h + 2) {
-          while (ld_acquire_gpu_u32(fup()) != 1u) __nanosleep(64);
-        }
-#pragma unroll
-        for (int tt = 1; tt < K; ++tt) {
-          if (j == h + 3 * tt - 1) fetch(win[tt - 1][ph], tt, 0);
-          if (j == h + 3 * tt) fetch(win[tt - 1][ph], tt, 1);
-        }
-        if (j == h + 3 * (K - 1) && lane == 0) *(volatile unsigned*)fup() = 0u;
-      }
-    }
   };
 
   // Steady ticks: every level active, j in [3K-1, n_load).
@@ -908,15 +799,13 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
   constexpr bool kSplit = K >= 8;
   for (int j0 = 0; j0 < nt; j0 += 3) {
     if (kSplit && j0 >= steady_lo && j0 + 3 <= steady_hi) {
-      tick(Int<0>{}, Bool<true>{}, Bool<false>{}, j0);
-      tick(Int<1>{}, Bool<true>{}, Bool<false>{}, j0 + 1);
-      tick(Int<2>{}, Bool<true>{}, Bool<false>{}, j0 + 2);
+      tick(Int<0>{}, Bool<true>{}, j0);
+      tick(Int<1>{}, Bool<true>{}, j0 + 1);
+      tick(Int<2>{}, Bool<true>{}, j0 + 2);
     } else {
-      // Skewed segments publish/fetch from the same body (a second body for
-      // those ticks doubled the loop's instruction footprint: I-cache misses).
-      tick(Int<0>{}, Bool<false>{}, Bool<true>{}, j0);
-      if (j0 + 1 < nt) tick(Int<1>{}, Bool<false>{}, Bool<true>{}, j0 + 1);
-      if (j0 + 2 < nt) tick(Int<2>{}, Bool<false>{}, Bool<true>{}, j0 + 2);
+      tick(Int<0>{}, Bool<false>{}, j0);
+      if (j0 + 1 < nt) tick(Int<1>{}, Bool<false>{}, j0 + 1);
+      if (j0 + 2 < nt) tick(Int<2>{}, Bool<false>{}, j0 + 2);
     }
     const uint32_t t_half = half_now;
     half_now = half_other;
@@ -968,7 +857,7 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
 // stage those rows straight from the neighbour's input buffer (peer memory)
 // and publish completion -- the halo exchange is fused into the step.
 template <int K, int W, class T, int kArith, bool kPerGrid, bool kPeer = false, bool kWrap = false,
-          bool kTee = false, bool kPara = false>
+          bool kTee = false>
 __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T, W>::value)
     fhn_wavefront_kernel(const __grid_constant__ StepArgsT<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -982,9 +871,7 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T, W>::value)
   const int g = int(warp_id / per_grid);
   const int rem = int(warp_id - (long long)g * per_grid);
   const int band = rem % a.n_bands;
-  // Skewed segments wait for the segment below: number them bottom-up so
-  // that, with CTAs dispatched in blockIdx order, that neighbour starts first.
-  const int seg = kPara ? a.n_segs - 1 - rem / a.n_bands : rem / a.n_bands;
+  const int seg = rem / a.n_bands;
 
   // A grid that already blew up in an earlier launch of this advance stays
   // frozen (no stores), so the input of its first bad launch survives for
@@ -1000,7 +887,7 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T, W>::value)
   const unsigned frozen = fl != 0u && fl != a.tag;
 
   BlockStats stats;
-  const bool bad = wavefront_block<K, W, T, kArith, kPerGrid, kPeer, kWrap, kTee, kPara>(
+  const bool bad = wavefront_block<K, W, T, kArith, kPerGrid, kPeer, kWrap, kTee>(
       a, smem_raw, lane, wib, g, band, seg, frozen, a.u_in, a.v_in, a.u_out, a.v_out, stats);
 
   if (bad && lane == 0 && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);

@@ -95,8 +95,6 @@ struct KernelTable {
   using Fn = void (*)(StepArgsT<T>);
   Fn fn[2][4][3][2][2] = {};        // [wide][k][arith][per_grid][wrap]
   int resident[2][4][3][2][2] = {};
-  Fn para[3][2][2] = {};            // skewed segments, fp32 wide K=4: [arith][per_grid][wrap]
-  int para_resident[3][2][2] = {};
 };
 
 template <class T, int W, int KI, int FI, int PI>
@@ -127,35 +125,15 @@ void fill_w(KernelTable<T>& t) {
   fill_k<T, W, 3>(t);
 }
 
-template <int FI, int PI>
-void fill_para(KernelTable<float>& t) {
-  t.para[FI][PI][0] = &rdcnn_dev::fhn_wavefront_kernel<4, Traits<float>::kWide, float, FI, PI == 1, false, false, false, true>;
-  t.para[FI][PI][1] = &rdcnn_dev::fhn_wavefront_kernel<4, Traits<float>::kWide, float, FI, PI == 1, false, true, false, true>;
-}
-
 template <class T>
 KernelTable<T>& table() {
   static KernelTable<T> t = [] {
     KernelTable<T> x;
     fill_w<T, 1>(x);
     fill_w<T, Traits<T>::kWide>(x);
-    if constexpr (sizeof(T) == 4 && !rdcnn_dev::BulkStage<Traits<float>::kWide, float>::value) {
-      fill_para<0, 0>(x); fill_para<0, 1>(x); fill_para<1, 0>(x); fill_para<1, 1>(x); fill_para<2, 0>(x); fill_para<2, 1>(x);
-    }
     return x;
   }();
   return t;
-}
-
-// Skewed (parallelogram) segments for periodic fp32 K=4 launches: no
-// segment start-up recomputation (fhn_stencil.cuh kPara).  RDCNN_PARA=0
-// turns them off.
-bool para_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("RDCNN_PARA");
-    return !(e && e[0] == '0');
-  }();
-  return on;
 }
 
 // Dynamic shared memory of one CTA (the level-0 staging rings).
@@ -269,10 +247,10 @@ int peer_resident_blocks(int k, int w, int arith, bool wrap, bool tee) {
 
 template <class T>
 cudaError_t launch_stencil(int k, int w, int arith, bool per_grid, bool wrap, const StepArgsT<T>& a,
-                           long long warps, cudaStream_t s, bool full, bool para = false) {
+                           long long warps, cudaStream_t s, bool full) {
   if (warps <= 0) return cudaSuccess;
   if (k != 1 && k != 2 && k != 4 && k != 8) return cudaErrorInvalidValue;
-  auto fn = para ? table<T>().para[arith][per_grid][wrap] : table<T>().fn[w > 1][k_index(k)][arith][per_grid][wrap];
+  auto fn = table<T>().fn[w > 1][k_index(k)][arith][per_grid][wrap];
   if (!fn) return cudaErrorInvalidValue;
   const long long blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
   return launch_pdl(fn, (unsigned)blocks, smem_for<T>(w), s, a, full);
@@ -568,8 +546,6 @@ struct rdcnn_sim {
   long launches = 0;
   int max_levels = 4;
   int seg_rows = 0;
-  void* xbuf = nullptr;             // kPara segment exchange: rows + words
-  size_t xbuf_bytes = 0;
   bool tma_ok = false;              // RDCNN_BULK=2 builds: tensor maps of both buffers
   alignas(64) unsigned char tmap[2][128];
   int tuned_seg[4] = {0, 0, 0, 0};  // autotuned segment height per K (0: not tuned)
@@ -888,32 +864,8 @@ cudaError_t launch_range(rdcnn_sim* s, int k, StepArgsT<T> a, int row_begin, int
   a.band_groups = p.band_groups;
   a.halo_groups = p.halo;
   ++s->launches;
-  // Skewed segments need every segment (the last one included) to be at
-  // least 3K rows, so each warp publishes its rows before it waits.
-  bool para = false;
-  if constexpr (sizeof(T) == 4) {
-    const int h_last = (row_end - row_begin) - (p.n_segs - 1) * p.seg_rows;
-    para = k == 4 && w > 1 && !s->slab && a.trace == nullptr && para_enabled() && row_begin == 0 &&
-           row_end == s->rows && p.seg_rows >= 3 * k && h_last >= 3 * k && table<T>().para[arith][per_grid][wrap];
-    if (para) {
-      const size_t xfloats = (size_t)p.warps * (size_t)(k - 1) * 2 * 2 * 32 * (size_t)w;
-      const size_t need = xfloats * sizeof(T) + sizeof(unsigned) * (size_t)p.warps;
-      if (s->xbuf_bytes < need) {
-        if (s->xbuf) cudaFree(s->xbuf);
-        s->xbuf = nullptr;
-        s->xbuf_bytes = 0;
-        cudaError_t e = cudaMalloc(&s->xbuf, need);
-        if (e != cudaSuccess) return e;
-        e = cudaMemsetAsync(s->xbuf, 0, need, st);  // every word 0: nothing published
-        if (e != cudaSuccess) return e;
-        s->xbuf_bytes = need;
-      }
-      a.xbuf = static_cast<T*>(s->xbuf);
-      a.xflag = reinterpret_cast<unsigned*>(static_cast<T*>(s->xbuf) + xfloats);
-    }
-  }
   return launch_stencil<T>(k, w, arith, per_grid, wrap, a, p.warps, st,
-                           4 * p.warps >= 3LL * rw * s->sm_count, para);
+                           4 * p.warps >= 3LL * rw * s->sm_count);
 }
 
 int alloc_common(rdcnn_sim* s) {
@@ -966,7 +918,6 @@ void free_all(rdcnn_sim* s) {
   for (void* p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   if (s->p2p_words) cudaFree(s->p2p_words);
   if (s->d_first_bad) cudaFree(s->d_first_bad);
-  if (s->xbuf) cudaFree(s->xbuf);
   for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
   s->graphs.clear();
   if (s->ckpt) cudaFree(s->ckpt);
