@@ -231,8 +231,10 @@ int rdcnn_slab_step_fused(rdcnn_sim_t sim, int k, void* stream);
  * rdcnn_slab_checkpoint_age gives the iterations from the checkpoint to the
  * start of the last advance; rdcnn_slab_restore makes the checkpoint the
  * front buffer again.  The ranks then agree on the first bad block (min over
- * ranks), restore, re-advance age + that block's first iteration - 1 steps
- * and step one level at a time until any rank flags -- see slab.py
+ * ranks), restore, synchronise (no rank may start the re-advance while a
+ * neighbour's buffer still holds the post-blow-up rows its peer reads would
+ * pull), re-advance age + that block's first iteration - 1 steps and step
+ * one level at a time until any rank flags -- see slab.py
  * SlabStepper.advance.  (Freezing every rank at the first flag instead
  * cannot work: a rank's neighbours learn of it one block later, ranks at
  * distance d only d blocks later, by when they have overwritten the state

@@ -456,6 +456,11 @@ class SlabStepper:
         age = ctypes.c_long()
         check(self._lib.rdcnn_slab_checkpoint_age(self._h, ctypes.byref(age)))
         check(self._lib.rdcnn_slab_restore(self._h))
+        # Every rank has restored before any rank's replay reads its
+        # neighbours' rows: their ready words still carry the last block of
+        # the advance, so without this a fast rank could pull a neighbour's
+        # post-blow-up rows (seen as a rare 3-process IPC failure).
+        self._agree(0, "max")
         pre = age.value + first_block_iter - 1
         if pre and self._agree(self._advance_native(pre), "min"):
             raise RuntimeError("blow-up before the first flagged block on replay")
