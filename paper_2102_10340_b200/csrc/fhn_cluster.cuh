@@ -160,7 +160,7 @@ __device__ __forceinline__ void read_row(uint32_t addr, float (&u)[W], float (&v
 
 // One row of one step: left/right by shuffles (the warp is the whole row, so
 // lane 31's right neighbour is lane 0: the torus column wrap).
-template <int W, bool kFast>
+template <int W, int kArith>
 __device__ __forceinline__ void cluster_row(const float (&uu)[W], const float (&vu)[W], const float (&uc)[W],
                                             const float (&vc)[W], const float (&ud)[W], const float (&vd)[W],
                                             float (&un)[W], float (&vn)[W], const ParamsT<float>& p,
@@ -175,7 +175,7 @@ __device__ __forceinline__ void cluster_row(const float (&uu)[W], const float (&
     const float u_r = k < W - 1 ? uc[k + 1] : ur;
     const float v_l = k > 0 ? vc[k - 1] : vl;
     const float v_r = k < W - 1 ? vc[k + 1] : vr;
-    fhn_cell<float, kFast ? kFastArith : kStrictArith>(uc[k], vc[k], u_r, u_l, ud[k], uu[k], v_r, v_l, vd[k], vu[k], p, neg_eps, un[k],
+    fhn_cell<float, kArith>(uc[k], vc[k], u_r, u_l, ud[k], uu[k], v_r, v_l, vd[k], vu[k], p, neg_eps, un[k],
                            vn[k]);
   }
 }
@@ -189,7 +189,7 @@ struct EdgePre {
   float su, sv, f1, f2;
 };
 
-template <bool kDnOwn>
+template <bool kDnOwn, int kArith>
 __device__ __forceinline__ void cell_pre(float uc, float vc, float ur, float ul, float vr, float vl, float ud,
                                          float vd, const ParamsT<float>& p, float neg_eps, EdgePre& e) {
   e.su = add_rn(ur, ul);
@@ -198,11 +198,12 @@ __device__ __forceinline__ void cell_pre(float uc, float vc, float ur, float ul,
     e.su = add_rn(e.su, ud);
     e.sv = add_rn(e.sv, vd);
   }
-  e.f1 = sub_rn(mul_rn(uc, sub_rn(p.c, div3_rn(mul_rn(uc, uc)))), vc);
+  const float uu3 = kArith >= kStrictDiv2 ? div3_rn2(mul_rn(uc, uc)) : div3_rn(mul_rn(uc, uc));
+  e.f1 = sub_rn(mul_rn(uc, sub_rn(p.c, uu3)), vc);
   e.f2 = mul_rn(neg_eps, add_rn(sub_rn(uc, mul_rn(p.b, vc)), p.a));
 }
 
-template <bool kDnOwn>
+template <bool kDnOwn, int kArith>
 __device__ __forceinline__ void cell_post(float uc, float vc, float ud, float vd, float uu, float vu,
                                           const EdgePre& e, const ParamsT<float>& p, float& un, float& vn) {
   float su = e.su, sv = e.sv;
@@ -213,11 +214,12 @@ __device__ __forceinline__ void cell_post(float uc, float vc, float ud, float vd
   const float lap_u = fma_rn(-4.0f, uc, add_rn(su, uu));  // as fhn_cell: exact when 4*uc is finite
   const float lap_v = sub_rn(add_rn(sv, vu), mul_rn(4.0f, vc));
   un = add_rn(uc, mul_rn(p.dt, add_rn(e.f1, mul_rn(p.du, lap_u))));
-  vn = add_rn(vc, mul_rn(p.dt, add_rn(e.f2, mul_rn(p.dv, lap_v))));
+  const float dv_lap = kArith == kStrictDiv2U ? lap_v : mul_rn(p.dv, lap_v);  // as fhn_cell
+  vn = add_rn(vc, mul_rn(p.dt, add_rn(e.f2, dv_lap)));
 }
 
 // Pre-wait half of one edge row: left/right by shuffles, as cluster_row.
-template <int W, bool kDnOwn>
+template <int W, bool kDnOwn, int kArith>
 __device__ __forceinline__ void edge_pre(const float (&uc)[W], const float (&vc)[W], const float (&ud)[W],
                                          const float (&vd)[W], EdgePre (&e)[W], const ParamsT<float>& p,
                                          float neg_eps, int lane_l, int lane_r) {
@@ -227,7 +229,7 @@ __device__ __forceinline__ void edge_pre(const float (&uc)[W], const float (&vc)
   const float vr = __shfl_sync(kFull, vc[0], lane_r);
 #pragma unroll
   for (int k = 0; k < W; ++k) {
-    cell_pre<kDnOwn>(uc[k], vc[k], k < W - 1 ? uc[k + 1] : ur, k > 0 ? uc[k - 1] : ul, k < W - 1 ? vc[k + 1] : vr,
+    cell_pre<kDnOwn, kArith>(uc[k], vc[k], k < W - 1 ? uc[k + 1] : ur, k > 0 ? uc[k - 1] : ul, k < W - 1 ? vc[k + 1] : vr,
                      k > 0 ? vc[k - 1] : vl, ud[k], vd[k], p, neg_eps, e[k]);
   }
 }
@@ -238,7 +240,9 @@ struct ClusterThreads {  // launch bound: 4-row warps keep ~200 registers
   static constexpr int value = RW >= 4 ? 256 : 512;
 };
 
-template <int W, int RW, bool kFast>
+// kArith: kStrictArith, kFastArith or kStrictDiv2U (the host maps
+// kStrictDiv2 to kStrictArith here: both are exact; fewer instances).
+template <int W, int RW, int kArith>
 __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kernel(const ClusterArgs a) {
   static_assert(W % 4 == 0, "W must be a multiple of 4 (float4 chunks)");
   constexpr uint32_t kRow = 2 * (W / 4) * 32 * 16;  // bytes of one exchange row (u, v)
@@ -322,33 +326,33 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
     float un[RW][W], vn[RW][W];
 #pragma unroll
     for (int r = 1; r < RW - 1; ++r)
-      cluster_row<W, kFast>(u[r - 1], v[r - 1], u[r], v[r], u[r + 1], v[r + 1], un[r], vn[r], p, neg_eps, lane_l,
+      cluster_row<W, kArith>(u[r - 1], v[r - 1], u[r], v[r], u[r + 1], v[r + 1], un[r], vn[r], p, neg_eps, lane_l,
                             lane_r);
     const unsigned phase = (unsigned)((done >> 1) & 1);
     // 2b. strict mode: the edge rows' own-row half before the wait
     EdgePre e_top[W], e_bot[W];
-    if constexpr (!kFast) {
+    if constexpr (kArith != kFastArith) {
       if constexpr (RW == 1) {
-        edge_pre<W, false>(u[0], v[0], u[0], v[0], e_top, p, neg_eps, lane_l, lane_r);
+        edge_pre<W, false, kArith>(u[0], v[0], u[0], v[0], e_top, p, neg_eps, lane_l, lane_r);
       } else {
-        edge_pre<W, true>(u[0], v[0], u[1], v[1], e_top, p, neg_eps, lane_l, lane_r);
-        edge_pre<W, false>(u[RW - 1], v[RW - 1], u[RW - 1], v[RW - 1], e_bot, p, neg_eps, lane_l, lane_r);
+        edge_pre<W, true, kArith>(u[0], v[0], u[1], v[1], e_top, p, neg_eps, lane_l, lane_r);
+        edge_pre<W, false, kArith>(u[RW - 1], v[RW - 1], u[RW - 1], v[RW - 1], e_bot, p, neg_eps, lane_l, lane_r);
       }
     }
     mbar_wait_parity_cta(lb, phase);
     if (cta_first || cta_last) mbar_wait_parity(mb, phase);
     // 3. edge rows with the neighbours' rows from shared memory
-    if constexpr (!kFast) {
+    if constexpr (kArith != kFastArith) {
       float ua[W], va[W], ub[W], vb[W];
       read_row<W>(above + par, ua, va);
       read_row<W>(below + par, ub, vb);
 #pragma unroll
       for (int k = 0; k < W; ++k) {
         if constexpr (RW == 1) {
-          cell_post<false>(u[0][k], v[0][k], ub[k], vb[k], ua[k], va[k], e_top[k], p, un[0][k], vn[0][k]);
+          cell_post<false, kArith>(u[0][k], v[0][k], ub[k], vb[k], ua[k], va[k], e_top[k], p, un[0][k], vn[0][k]);
         } else {
-          cell_post<true>(u[0][k], v[0][k], 0.0f, 0.0f, ua[k], va[k], e_top[k], p, un[0][k], vn[0][k]);
-          cell_post<false>(u[RW - 1][k], v[RW - 1][k], ub[k], vb[k], u[RW - 2][k], v[RW - 2][k], e_bot[k], p,
+          cell_post<true, kArith>(u[0][k], v[0][k], 0.0f, 0.0f, ua[k], va[k], e_top[k], p, un[0][k], vn[0][k]);
+          cell_post<false, kArith>(u[RW - 1][k], v[RW - 1][k], ub[k], vb[k], u[RW - 2][k], v[RW - 2][k], e_bot[k], p,
                            un[RW - 1][k], vn[RW - 1][k]);
         }
       }
@@ -357,10 +361,10 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
       read_row<W>(above + par, ua, va);
       read_row<W>(below + par, ub, vb);
       if constexpr (RW == 1) {
-        cluster_row<W, kFast>(ua, va, u[0], v[0], ub, vb, un[0], vn[0], p, neg_eps, lane_l, lane_r);
+        cluster_row<W, kArith>(ua, va, u[0], v[0], ub, vb, un[0], vn[0], p, neg_eps, lane_l, lane_r);
       } else {
-        cluster_row<W, kFast>(ua, va, u[0], v[0], u[1], v[1], un[0], vn[0], p, neg_eps, lane_l, lane_r);
-        cluster_row<W, kFast>(u[RW - 2], v[RW - 2], u[RW - 1], v[RW - 1], ub, vb, un[RW - 1], vn[RW - 1], p,
+        cluster_row<W, kArith>(ua, va, u[0], v[0], u[1], v[1], un[0], vn[0], p, neg_eps, lane_l, lane_r);
+        cluster_row<W, kArith>(u[RW - 2], v[RW - 2], u[RW - 1], v[RW - 1], ub, vb, un[RW - 1], vn[RW - 1], p,
                               neg_eps, lane_l, lane_r);
       }
     }

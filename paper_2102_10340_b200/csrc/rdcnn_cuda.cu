@@ -93,8 +93,8 @@ int k_index(int k) { return k == 1 ? 0 : k == 2 ? 1 : k == 4 ? 2 : 3; }
 template <class T>
 struct KernelTable {
   using Fn = void (*)(StepArgsT<T>);
-  Fn fn[2][4][3][2][2] = {};        // [wide][k][arith][per_grid][wrap]
-  int resident[2][4][3][2][2] = {};
+  Fn fn[2][4][4][2][2] = {};        // [wide][k][arith][per_grid][wrap]
+  int resident[2][4][4][2][2] = {};
 };
 
 template <class T, int W, int KI, int FI, int PI>
@@ -115,6 +115,8 @@ void fill_k(KernelTable<T>& t) {
   fill_one<T, W, KI, 1, 1>(t);
   fill_one<T, W, KI, 2, 0>(t);
   fill_one<T, W, KI, 2, 1>(t);
+  fill_one<T, W, KI, 3, 0>(t);
+  fill_one<T, W, KI, 3, 1>(t);
 }
 
 template <class T, int W>
@@ -202,8 +204,8 @@ cudaError_t launch_pdl(void (*fn)(Args), unsigned blocks, size_t smem, cudaStrea
 // Fused peer-exchange instances (fp32 slabs, shared gene): [wide][k][fast].
 struct PeerTable {
   using Fn = void (*)(StepArgsT<float>);
-  Fn fn[2][4][3][2][2] = {};  // [wide][k][arith][wrap][tee]
-  int resident[2][4][3][2][2] = {};
+  Fn fn[2][4][4][2][2] = {};  // [wide][k][arith][wrap][tee]
+  int resident[2][4][4][2][2] = {};
 };
 
 template <int W, int KI, int FI>
@@ -216,10 +218,10 @@ void fill_peer_one(PeerTable& t) {
 
 template <int W>
 void fill_peer_w(PeerTable& t) {
-  fill_peer_one<W, 0, 0>(t); fill_peer_one<W, 0, 1>(t); fill_peer_one<W, 0, 2>(t);
-  fill_peer_one<W, 1, 0>(t); fill_peer_one<W, 1, 1>(t); fill_peer_one<W, 1, 2>(t);
-  fill_peer_one<W, 2, 0>(t); fill_peer_one<W, 2, 1>(t); fill_peer_one<W, 2, 2>(t);
-  fill_peer_one<W, 3, 0>(t); fill_peer_one<W, 3, 1>(t); fill_peer_one<W, 3, 2>(t);
+  fill_peer_one<W, 0, 0>(t); fill_peer_one<W, 0, 1>(t); fill_peer_one<W, 0, 2>(t); fill_peer_one<W, 0, 3>(t);
+  fill_peer_one<W, 1, 0>(t); fill_peer_one<W, 1, 1>(t); fill_peer_one<W, 1, 2>(t); fill_peer_one<W, 1, 3>(t);
+  fill_peer_one<W, 2, 0>(t); fill_peer_one<W, 2, 1>(t); fill_peer_one<W, 2, 2>(t); fill_peer_one<W, 2, 3>(t);
+  fill_peer_one<W, 3, 0>(t); fill_peer_one<W, 3, 1>(t); fill_peer_one<W, 3, 2>(t); fill_peer_one<W, 3, 3>(t);
 }
 
 PeerTable& peer_table() {
@@ -537,6 +539,7 @@ struct rdcnn_sim {
   ParamsT<double> h_params_d{};
   int params_stride = 0;
   bool div2_ok = true;      // every gene has |c| >= 2^-90: the 2-op x/3 instance is exact
+  bool unit_dv = false;     // every gene has Dv == 1: the Dv*lap_v product is the identity
   int arith_override = -1;  // RDCNN_DIV3 / tests: force the 3-op (0) or 2-op (2) strict instance
   unsigned* d_flags = nullptr;  // batch words (+1 scratch for replays)
   unsigned* h_flags = nullptr;  // pinned mirror
@@ -607,14 +610,16 @@ int width_for(const rdcnn_sim* s) {
 }
 
 // Arithmetic instance of a launch: fast mode, or strict with the 2-op x/3
-// when every gene of the handle passes its gate (fhn_stencil.cuh div3_rn2),
-// else strict with the 3-op x/3.  fp64 always takes the 3-op strict path.
+// when every gene of the handle passes its gate (fhn_stencil.cuh div3_rn2)
+// -- and without the Dv*lap_v product when every gene also has Dv == 1
+// (kStrictDiv2U) -- else strict with the 3-op x/3.  fp64 always takes the
+// 3-op strict path.
 template <class T>
 int arith_for(const rdcnn_sim* s) {
   if (s->mode == RDCNN_FAST) return rdcnn_dev::kFastArith;
-  if (sizeof(T) != 4) return rdcnn_dev::kStrictArith;
-  if (s->arith_override >= 0) return s->arith_override == 2 && s->div2_ok ? rdcnn_dev::kStrictDiv2 : rdcnn_dev::kStrictArith;
-  return s->div2_ok ? rdcnn_dev::kStrictDiv2 : rdcnn_dev::kStrictArith;
+  if (sizeof(T) != 4 || !s->div2_ok || s->arith_override == 0) return rdcnn_dev::kStrictArith;
+  if (s->arith_override == 2 || !s->unit_dv) return rdcnn_dev::kStrictDiv2;
+  return rdcnn_dev::kStrictDiv2U;
 }
 
 // The gate of the 2-op x/3: |c| >= 2^-90 (false for NaN).
@@ -623,6 +628,14 @@ bool div2_gate(const ParamsT<T>* p, int n) {
   for (int i = 0; i < n; ++i)
     if (!(std::fabs((double)p[i].c) >= 0x1p-90)) return false;
   return true;
+}
+
+// The gate of kStrictDiv2U: Dv == 1 exactly (after narrowing) for every gene.
+template <class T>
+bool unit_dv_gate(const ParamsT<T>* p, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!(p[i].dv == T(1))) return false;
+  return n > 0;
 }
 
 template <class T>
@@ -840,7 +853,7 @@ cudaError_t launch_range(rdcnn_sim* s, int k, StepArgsT<T> a, int row_begin, int
   if constexpr (sizeof(T) == 4) {
     RRPlan rp;
     if (a.trace == nullptr &&
-        rowring_plan(s, k, arith_for<T>(s), a.params_stride != 0, a.batch, row_begin, row_end,
+        rowring_plan(s, k, std::min(arith_for<T>(s), int(rdcnn_dev::kStrictDiv2)), a.params_stride != 0, a.batch, row_begin, row_end,
                      seg_for(s, k, row_begin, row_end), rp)) {
       a.row_begin = row_begin;
       a.row_end = row_end;
@@ -872,8 +885,9 @@ int alloc_common(rdcnn_sim* s) {
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   s->sm_count = sm_count_for(s->device);
   // A/B and tests: RDCNN_DIV3=3 pins the 3-op x/3 strict instance, =2 the
-  // gated 2-op one (still subject to its gate); unset: automatic.
-  if (const char* e = std::getenv("RDCNN_DIV3")) s->arith_override = e[0] == '3' ? 0 : 2;
+  // gated 2-op one with the Dv*lap_v product kept (still subject to its
+  // gate); unset or anything else: automatic.
+  if (const char* e = std::getenv("RDCNN_DIV3")) s->arith_override = e[0] == '3' ? 0 : e[0] == '2' ? 2 : -1;
   RDCNN_CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   RDCNN_CUDA_TRY(cudaEventCreate(&s->ev0));
   RDCNN_CUDA_TRY(cudaEventCreate(&s->ev1));
@@ -896,6 +910,7 @@ int alloc_common(rdcnn_sim* s) {
   else
     RDCNN_CUDA_TRY(cudaMemcpyAsync(s->d_params, &s->h_params_d, sizeof s->h_params_d, cudaMemcpyHostToDevice, s->stream));
   s->params_stride = 0;
+  s->unit_dv = true;  // the default gene has Dv = 1
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
   return RDCNN_OK;
 }
@@ -1031,14 +1046,24 @@ struct ClusterPlan {
 
 using ClusterFn = void (*)(rdcnn_dev::ClusterArgs);
 
-template <int W, int RW>
-ClusterFn cluster_fn_wr(bool fast) {
-  return fast ? &rdcnn_dev::fhn_cluster_kernel<W, RW, true> : &rdcnn_dev::fhn_cluster_kernel<W, RW, false>;
+// Arithmetic instance of the cluster kernel: fast, strict with the 2-op x/3
+// and the unit-Dv product skipped when both gates hold, else the 3-op strict
+// instance (kStrictDiv2 alone is not instantiated here: fewer kernels).
+int cluster_arith(const rdcnn_sim* s) {
+  const int a = arith_for<float>(s);
+  return a == rdcnn_dev::kStrictDiv2 ? rdcnn_dev::kStrictArith : a;
 }
 
-ClusterFn cluster_fn(int w, int rw, bool fast) {
-  if (w == 4) return rw == 1 ? cluster_fn_wr<4, 1>(fast) : rw == 2 ? cluster_fn_wr<4, 2>(fast) : cluster_fn_wr<4, 4>(fast);
-  return rw == 1 ? cluster_fn_wr<8, 1>(fast) : rw == 2 ? cluster_fn_wr<8, 2>(fast) : cluster_fn_wr<8, 4>(fast);
+template <int W, int RW>
+ClusterFn cluster_fn_wr(int arith) {
+  return arith == rdcnn_dev::kFastArith      ? &rdcnn_dev::fhn_cluster_kernel<W, RW, rdcnn_dev::kFastArith>
+         : arith == rdcnn_dev::kStrictDiv2U ? &rdcnn_dev::fhn_cluster_kernel<W, RW, rdcnn_dev::kStrictDiv2U>
+                                            : &rdcnn_dev::fhn_cluster_kernel<W, RW, rdcnn_dev::kStrictArith>;
+}
+
+ClusterFn cluster_fn(int w, int rw, int arith) {
+  if (w == 4) return rw == 1 ? cluster_fn_wr<4, 1>(arith) : rw == 2 ? cluster_fn_wr<4, 2>(arith) : cluster_fn_wr<4, 4>(arith);
+  return rw == 1 ? cluster_fn_wr<8, 1>(arith) : rw == 2 ? cluster_fn_wr<8, 2>(arith) : cluster_fn_wr<8, 4>(arith);
 }
 
 int cluster_max_warps(int rw) { return (rw >= 4 ? 256 : 512) / 32; }
@@ -1062,7 +1087,7 @@ std::vector<ClusterPlan> cluster_plans(rdcnn_sim* s) {
   if (s->cols % 128 != 0) return plans;
   const int w = s->cols / 32;
   if (w != 4 && w != 8) return plans;
-  const bool fast = s->mode == RDCNN_FAST;
+  const int arith = cluster_arith(s);
   for (int rw : cluster_rw_order()) {
     int C = 0;
     for (int c = rdcnn_dev::kClusterMax; c >= 1; --c)
@@ -1078,12 +1103,12 @@ std::vector<ClusterPlan> cluster_plans(rdcnn_sim* s) {
     p.RW = rw;
     p.smem = (size_t)(w == 4 ? rdcnn_dev::cluster_smem_bytes<4>(p.R) : rdcnn_dev::cluster_smem_bytes<8>(p.R));
     if (p.smem > 200 * 1024) continue;
-    static int checked[2][5][2][rdcnn_dev::kClusterMax + 1] = {};  // 1 ok, -1 not launchable
+    static int checked[2][5][4][rdcnn_dev::kClusterMax + 1] = {};  // 1 ok, -1 not launchable
     static std::mutex checked_mu;  // handles may plan concurrently from several host threads
     std::lock_guard<std::mutex> lock(checked_mu);
-    int& ok = checked[w == 8][rw][fast][C];
+    int& ok = checked[w == 8][rw][arith][C];
     if (ok == 0) {
-      ClusterFn fn = cluster_fn(w, rw, fast);
+      ClusterFn fn = cluster_fn(w, rw, arith);
       ok = -1;
       if (cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
           cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) == cudaSuccess) {
@@ -1135,7 +1160,7 @@ int cluster_advance(rdcnn_sim* s, const ClusterPlan& pl, long steps, long* first
   cfg.stream = s->stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  ClusterFn fn = cluster_fn(pl.W, pl.RW, s->mode == RDCNN_FAST);
+  ClusterFn fn = cluster_fn(pl.W, pl.RW, cluster_arith(s));
   RDCNN_CUDA_TRY(cudaMemsetAsync(s->d_first_bad, 0xFF, sizeof(long long), s->stream));
   RDCNN_CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
   {
@@ -1595,6 +1620,7 @@ int set_params_impl(rdcnn_sim* s, const ParamsT<T>* p, int n) {
                     std::memcmp(&s->shared_params<T>(), p, sizeof(ParamsT<T>)) == 0;
   s->params_stride = (n == 1) ? 0 : 1;
   s->div2_ok = div2_gate<T>(p, n);
+  s->unit_dv = unit_dv_gate<T>(p, n);
   if (n == 1) {
     if constexpr (sizeof(T) == 4) s->h_params_f = *p;
     else s->h_params_d = *p;

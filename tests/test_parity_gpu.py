@@ -46,19 +46,22 @@ def test_div3_exhaustive_on_device():
     assert n.value == 0
 
 
-@pytest.mark.parametrize("c", [1.0, 0.0, 2.0 ** -100, 2.0 ** -89, -3.5])
-def test_div3_instances_agree_with_oracle(c, monkeypatch):
-    """Genes on both sides of the 2-op x/3 gate (|c| >= 2^-90): the strict
-    launch picks the 2-op or the 3-op instance, both equal the oracle bit for
-    bit; pinning the 3-op instance (RDCNN_DIV3=3) changes nothing."""
+@pytest.mark.parametrize("c,dv", [(1.0, 1.0), (1.0, 0.5), (0.0, 1.0), (2.0 ** -100, 1.0), (2.0 ** -89, 1.0),
+                                  (-3.5, 1.0), (-3.5, 0.0), (1.0, 1.0 + 2.0 ** -23)])
+def test_div3_instances_agree_with_oracle(c, dv, monkeypatch):
+    """Genes on both sides of the 2-op x/3 gate (|c| >= 2^-90) and of the
+    unit-Dv gate (Dv == 1): the strict launch picks the 3-op, 2-op or 2-op
+    unit-Dv instance; every one equals the oracle bit for bit, and pinning the
+    3-op (RDCNN_DIV3=3) or the 2-op instance with the Dv product kept
+    (RDCNN_DIV3=2) changes nothing."""
     from oracle.oracle import Oracle
-    gene = fhn.Gene(c=c, a=-0.05)
+    gene = fhn.Gene(c=c, a=-0.05, Dv=dv)
     orc = Oracle()
     u0, v0 = orc.init(2, 96, 128, 5)
     g7 = [gene.dt, gene.a, gene.b, gene.eps, gene.c, gene.Du, gene.Dv]
     ou, ov, obad = orc.run(96, 128, u0, v0, 40, g7)
     outs = []
-    for pin in (None, "3"):
+    for pin in (None, "2", "3"):
         if pin:
             monkeypatch.setenv("RDCNN_DIV3", pin)
         with fhn.Simulator(96, 128, device=0, levels=4) as sim:
