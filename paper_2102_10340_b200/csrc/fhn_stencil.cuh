@@ -97,11 +97,6 @@ struct StepArgsT {
   // batch, 2 planes} of this launch's input buffer with a {128, 1, 2} box --
   // one band row of both planes -- built by the host (cuTensorMapEncodeTiled).
   int tma_ok;
-  // -0.0, from the host: the product operand of the packed-pair arithmetic
-  // (RDCNN_PAIR builds), fma(a, b, -0) == RN(a*b) for every a, b.  A
-  // kernel parameter, so ptxas cannot fold the fma back into a multiply it
-  // would then contract with the following add.
-  T neg_zero;
   alignas(64) unsigned char tmap[128];
 };
 
@@ -216,76 +211,6 @@ __device__ __forceinline__ void fhn_cell(T uc, T vc, T ur, T ul, T ud, T uu, T v
   }
 }
 
-// ---- Packed cell pairs (RDCNN_PAIR builds; kStrictDiv2U, fp32) -------------
-// sm_100 FFMA2/FADD2 run two fp32 lanes per instruction (same lane-op
-// throughput, half the issue slots; bit-exact IEEE RN, tools/check_f32x2.cu).
-// The kernel is issue-bound with the FMA pipe ~74 % busy, so the reaction
-// terms of two neighbouring cells (10 ops per cell, all elementwise) run
-// packed while the Laplacians and the final updates stay scalar.  Products
-// are fma(a, b, -0) with -0 from the kernel parameters: ptxas contracts a
-// packed multiply into a following packed add even under --fmad=false.
-#ifndef RDCNN_PAIR
-#define RDCNN_PAIR 0
-#endif
-template <int W, class T, int kArith>
-struct PairArith {
-  static constexpr bool value = RDCNN_PAIR && W % 2 == 0 && sizeof(T) == 4 && kArith == kStrictDiv2U;
-};
-using f32x2_t = unsigned long long;
-__device__ __forceinline__ f32x2_t pk2(float a, float b) {
-  f32x2_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ void upk2(f32x2_t r, float& a, float& b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-}
-__device__ __forceinline__ f32x2_t add2(f32x2_t a, f32x2_t b) {
-  f32x2_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f32x2_t sub2(f32x2_t a, f32x2_t b) {
-  f32x2_t d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f32x2_t fma2(f32x2_t a, f32x2_t b, f32x2_t c) {
-  f32x2_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-
-// Cells (k, k+1) of one row: fhn_cell<float, kStrictDiv2U> twice, with the
-// same operations in the same order (kernels.hpp:63-72, model.hpp:37-56).
-__device__ __forceinline__ void fhn_cell_pair(float uc0, float uc1, float vc0, float vc1, float ur1, float ul0,
-                                              float vr1, float vl0, float ud0, float ud1, float uu0, float uu1,
-                                              float vd0, float vd1, float vu0, float vu1, const ParamsT<float>& p,
-                                              float neg_eps, float nz, float& un0, float& un1, float& vn0,
-                                              float& vn1) {
-  // Laplacians, scalar: right + left + down + up - 4*c (cell 0's right is uc1,
-  // cell 1's left is uc0).
-  const float lu0 = fma_rn(-4.0f, uc0, add_rn(add_rn(add_rn(uc1, ul0), ud0), uu0));
-  const float lu1 = fma_rn(-4.0f, uc1, add_rn(add_rn(add_rn(ur1, uc0), ud1), uu1));
-  const float lv0 = sub_rn(add_rn(add_rn(add_rn(vc1, vl0), vd0), vu0), mul_rn(4.0f, vc0));
-  const float lv1 = sub_rn(add_rn(add_rn(add_rn(vr1, vc0), vd1), vu1), mul_rn(4.0f, vc1));
-  // Reaction terms, packed.
-  const f32x2_t NZ = pk2(nz, nz);
-  const f32x2_t U = pk2(uc0, uc1), V = pk2(vc0, vc1);
-  const f32x2_t X = fma2(U, U, NZ);                                              // u*u
-  const f32x2_t Q = fma2(X, pk2(__uint_as_float(0x3EAAAAABu), __uint_as_float(0x3EAAAAABu)),
-                         fma2(X, pk2(__uint_as_float(0xB22AAAABu), __uint_as_float(0xB22AAAABu)), NZ));  // div3_rn2
-  const f32x2_t F1 = sub2(fma2(U, sub2(pk2(p.c, p.c), Q), NZ), V);             // u*(c - q) - v
-  const f32x2_t F2 = fma2(pk2(neg_eps, neg_eps), add2(sub2(U, fma2(pk2(p.b, p.b), V, NZ)), pk2(p.a, p.a)), NZ);
-  float f10, f11, f20, f21;
-  upk2(F1, f10, f11);
-  upk2(F2, f20, f21);
-  un0 = add_rn(uc0, mul_rn(p.dt, add_rn(f10, mul_rn(p.du, lu0))));
-  un1 = add_rn(uc1, mul_rn(p.dt, add_rn(f11, mul_rn(p.du, lu1))));
-  vn0 = add_rn(vc0, mul_rn(p.dt, add_rn(f20, lv0)));
-  vn1 = add_rn(vc1, mul_rn(p.dt, add_rn(f21, lv1)));
-}
-
 template <int W, class T>
 struct Row {
   T u[W];
@@ -361,7 +286,7 @@ __device__ __forceinline__ void store_row(T* __restrict__ u, T* __restrict__ v, 
 template <int W, class T, int kArith, bool kWrap>
 __device__ __forceinline__ void level_row(const Row<W, T>& up, const Row<W, T>& c,
                                           const Row<W, T>& dn, Row<W, T>& out,
-                                          const ParamsT<T>& p, T neg_eps, T nz, int lane_l,
+                                          const ParamsT<T>& p, T neg_eps, int lane_l,
                                           int lane_r) {
   T ul, ur, vl, vr;
   if constexpr (kWrap) {
@@ -375,24 +300,14 @@ __device__ __forceinline__ void level_row(const Row<W, T>& up, const Row<W, T>& 
     vl = __shfl_up_sync(kFull, c.v[W - 1], 1);
     vr = __shfl_down_sync(kFull, c.v[0], 1);
   }
-  if constexpr (PairArith<W, T, kArith>::value) {
 #pragma unroll
-    for (int k = 0; k < W; k += 2) {
-      fhn_cell_pair(c.u[k], c.u[k + 1], c.v[k], c.v[k + 1], k < W - 2 ? c.u[k + 2] : ur,
-                    k > 0 ? c.u[k - 1] : ul, k < W - 2 ? c.v[k + 2] : vr, k > 0 ? c.v[k - 1] : vl,
-                    dn.u[k], dn.u[k + 1], up.u[k], up.u[k + 1], dn.v[k], dn.v[k + 1], up.v[k], up.v[k + 1],
-                    p, neg_eps, nz, out.u[k], out.u[k + 1], out.v[k], out.v[k + 1]);
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-      const T u_l = k > 0 ? c.u[k - 1] : ul;
-      const T u_r = k < W - 1 ? c.u[k + 1] : ur;
-      const T v_l = k > 0 ? c.v[k - 1] : vl;
-      const T v_r = k < W - 1 ? c.v[k + 1] : vr;
-      fhn_cell<T, kArith>(c.u[k], c.v[k], u_r, u_l, dn.u[k], up.u[k], v_r, v_l, dn.v[k], up.v[k],
-                         p, neg_eps, out.u[k], out.v[k]);
-    }
+  for (int k = 0; k < W; ++k) {
+    const T u_l = k > 0 ? c.u[k - 1] : ul;
+    const T u_r = k < W - 1 ? c.u[k + 1] : ur;
+    const T v_l = k > 0 ? c.v[k - 1] : vl;
+    const T v_r = k < W - 1 ? c.v[k + 1] : vr;
+    fhn_cell<T, kArith>(c.u[k], c.v[k], u_r, u_l, dn.u[k], up.u[k], v_r, v_l, dn.v[k], up.v[k],
+                       p, neg_eps, out.u[k], out.v[k]);
   }
 }
 
@@ -616,7 +531,6 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
   // genes (sweeps) come from global memory once per warp.
   const ParamsT<T> p = kPerGrid ? a.params[g] : a.shared;
   const T neg_eps = -p.eps;  // reference model.hpp:45 negates eps first
-  const T nz = a.neg_zero;
 
   const int G = a.cols / W;
   const int gl = band * a.band_groups - a.halo_groups + lane;
@@ -820,10 +734,10 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
         const Row<W, T>& ce = win[t - 2][(ph + 1) % 3];
         const Row<W, T>& dn = win[t - 2][(ph + 2) % 3];
         if (t < K) {
-          level_row<W, T, kArith, kWrap>(up, ce, dn, win[t - 1][ph], p, neg_eps, nz, lane_l, lane_r);
+          level_row<W, T, kArith, kWrap>(up, ce, dn, win[t - 1][ph], p, neg_eps, lane_l, lane_r);
         } else {
           Row<W, T> o;
-          level_row<W, T, kArith, kWrap>(up, ce, dn, o, p, neg_eps, nz, lane_l, lane_r);
+          level_row<W, T, kArith, kWrap>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
           // Folded on every lane (non-storing lanes are cleared at the end),
           // so the store is the only guarded instruction.
           fold_finite<W, T>(fin, o);
@@ -874,12 +788,12 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
 #endif
       if constexpr (K == 1) {
         Row<W, T> o;
-        level_row<W, T, kArith, kWrap>(up, ce, dn, o, p, neg_eps, nz, lane_l, lane_r);
+        level_row<W, T, kArith, kWrap>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
         fold_finite<W, T>(fin, o);
         if (store) store_row<W, T>(du, du + vout_delta, 0, o);
         du = reinterpret_cast<T*>(reinterpret_cast<char*>(du) + a.pitch_b);
       } else {
-        level_row<W, T, kArith, kWrap>(up, ce, dn, win[0][ph], p, neg_eps, nz, lane_l, lane_r);
+        level_row<W, T, kArith, kWrap>(up, ce, dn, win[0][ph], p, neg_eps, lane_l, lane_r);
       }
     }
   };

@@ -657,7 +657,6 @@ StepArgsT<T> base_args(rdcnn_sim* s, int in_buf, int out_buf) {
   a.params = static_cast<const ParamsT<T>*>(s->d_params);
   a.params_stride = s->params_stride;
   a.flags = s->d_flags;
-  a.neg_zero = T(-0.0);
   a.tma_ok = s->tma_ok ? 1 : 0;
   if (s->tma_ok) std::memcpy(a.tmap, s->tmap[in_buf], sizeof a.tmap);
   return a;
