@@ -278,10 +278,15 @@ def test_blowup_split_across_calls(oracle):
 # Batched sweeps (sweep.hpp:255-326): per-grid genes and blow-up
 # --------------------------------------------------------------------------
 
+@pytest.mark.parametrize("unit_dv", (False, True))
 @pytest.mark.parametrize("levels", (1, 4, 8))
-def test_batch_per_grid_genes(oracle, levels):
+def test_batch_per_grid_genes(oracle, levels, unit_dv):
+    """Per-grid genes in one batched launch; with every Dv == 1 the batch takes
+    the unit-Dv instance (kStrictDiv2U), otherwise the Dv product is kept."""
     rows, cols, iters = 40, 128, 57
-    genes = [fhn.Gene(Du=du, Dv=dv) for du, dv in [(0.02, 0.5), (0.3, 1.0), (0.5, 0.8), (0.7, 0.8)]]
+    pairs = ([(0.02, 1.0), (0.3, 1.0), (0.5, 1.0), (0.7, 1.0)] if unit_dv
+             else [(0.02, 0.5), (0.3, 1.0), (0.5, 0.8), (0.7, 0.8)])
+    genes = [fhn.Gene(Du=du, Dv=dv) for du, dv in pairs]
     genes.append(fhn.Gene(dt=100.0))        # blows up
     genes.append(fhn.Gene(a=-0.05))
     B = len(genes)
