@@ -580,6 +580,9 @@ struct rdcnn_sim {
   int n_frames = 0;
   double* d_stats = nullptr;        // 3*batch doubles (min, max, median) + batch thresholds
   long long* d_counts = nullptr;    // batch counts
+  unsigned long long* d_digest = nullptr;  // batch FNV digests (rdcnn_sim_checksums)
+  void* d_scratch = nullptr;        // per-call staging (image pixels, normalised frames), grown on demand
+  size_t scratch_bytes = 0;
 
   template <class T>
   T* u_ptr(int b) {
@@ -939,6 +942,8 @@ void free_all(rdcnn_sim* s) {
   if (s->frames) cudaFree(s->frames);
   if (s->d_stats) cudaFree(s->d_stats);
   if (s->d_counts) cudaFree(s->d_counts);
+  if (s->d_digest) cudaFree(s->d_digest);
+  if (s->d_scratch) cudaFree(s->d_scratch);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
 }
@@ -1586,6 +1591,22 @@ int init_impl(rdcnn_sim* s, int typ, uint64_t seed, int global_rows, int row_off
   return RDCNN_OK;
 }
 
+// Device staging kept with the handle (stream-ordered malloc/free per call
+// made short calls' wall time vary by two orders of magnitude).  The caller
+// synchronises the handle's stream before returning, so the next call may
+// reuse the bytes.
+int scratch(rdcnn_sim* s, size_t bytes, void** out) {
+  if (s->scratch_bytes < bytes) {
+    if (s->d_scratch) RDCNN_CUDA_TRY(cudaFree(s->d_scratch));
+    s->d_scratch = nullptr;
+    s->scratch_bytes = 0;
+    RDCNN_CUDA_TRY(cudaMalloc(&s->d_scratch, bytes));
+    s->scratch_bytes = bytes;
+  }
+  *out = s->d_scratch;
+  return RDCNN_OK;
+}
+
 template <class T>
 int image_impl(rdcnn_sim* s, const uint8_t* px, double ka) {
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
@@ -1593,18 +1614,17 @@ int image_impl(rdcnn_sim* s, const uint8_t* px, double ka) {
   const T k = (T)ka;
   for (int p = 0; p < 256; ++p) lut[p] = k * (T)(p / 255.0);  // init.hpp:58, image.hpp:283
   const size_t n = (size_t)s->rows * s->cols;
-  uint8_t* d_px = nullptr;
-  T* d_lut = nullptr;
-  RDCNN_CUDA_TRY(cudaMallocAsync(&d_px, n, s->stream));
-  RDCNN_CUDA_TRY(cudaMallocAsync(&d_lut, sizeof lut, s->stream));
+  void* buf = nullptr;
+  const size_t lut_off = (n + 255) / 256 * 256;
+  RDCNN_TRY(scratch(s, lut_off + sizeof lut, &buf));
+  uint8_t* d_px = static_cast<uint8_t*>(buf);
+  T* d_lut = reinterpret_cast<T*>(static_cast<uint8_t*>(buf) + lut_off);
   RDCNN_CUDA_TRY(cudaMemcpyAsync(d_px, px, n, cudaMemcpyHostToDevice, s->stream));
   RDCNN_CUDA_TRY(cudaMemcpyAsync(d_lut, lut, sizeof lut, cudaMemcpyHostToDevice, s->stream));
   image_kernel<T><<<4 * s->sm_count, 256, 0, s->stream>>>(s->u_ptr<T>(s->cur), s->v_ptr<T>(s->cur),
                                                            s->pitch, s->grid_stride, s->batch,
                                                            s->rows, s->cols, d_px, d_lut);
   RDCNN_CUDA_TRY(cudaGetLastError());
-  RDCNN_CUDA_TRY(cudaFreeAsync(d_px, s->stream));
-  RDCNN_CUDA_TRY(cudaFreeAsync(d_lut, s->stream));
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
   return RDCNN_OK;
 }
@@ -1792,12 +1812,12 @@ int frame_active_impl(rdcnn_sim* s, int slot, const double* med, const double* t
 template <class T>
 int normalize_impl(rdcnn_sim* s, const void* src_dev, double lo, double hi, uint8_t* out) {
   const long long n = (long long)s->rows * s->cols;
-  uint8_t* d_out = nullptr;
-  RDCNN_CUDA_TRY(cudaMallocAsync(&d_out, (size_t)n, s->stream));
+  void* buf = nullptr;
+  RDCNN_TRY(scratch(s, (size_t)n, &buf));
+  uint8_t* d_out = static_cast<uint8_t*>(buf);
   normalize_kernel<T><<<4 * s->sm_count, 256, 0, s->stream>>>(static_cast<const T*>(src_dev), n, lo, hi, d_out);
   RDCNN_CUDA_TRY(cudaGetLastError());
   RDCNN_CUDA_TRY(cudaMemcpyAsync(out, d_out, (size_t)n, cudaMemcpyDeviceToHost, s->stream));
-  RDCNN_CUDA_TRY(cudaFreeAsync(d_out, s->stream));
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
   return RDCNN_OK;
 }
@@ -2421,8 +2441,10 @@ int rdcnn_sim_checksums(rdcnn_sim_t s, uint64_t* out) {
     for (int g = 0; g < s->batch; ++g) out[g] = fnv_planes(hu.data() + g * plane, hv.data() + g * plane, plane);
     return RDCNN_OK;
   }
-  unsigned long long* d = nullptr;
-  RDCNN_CUDA_TRY(cudaMallocAsync(&d, sizeof(unsigned long long) * (size_t)s->batch, s->stream));
+  // The digest words live with the handle: a stream-ordered malloc/free per
+  // call made this call's wall time vary from 3 to 140 ms.
+  if (!s->d_digest) RDCNN_CUDA_TRY(cudaMalloc(&s->d_digest, sizeof(unsigned long long) * (size_t)s->batch));
+  unsigned long long* d = s->d_digest;
   const unsigned char* u = static_cast<const unsigned char*>(s->buf[s->cur]);
   const unsigned char* v = u + plane * s->batch;
   fnv_batch_kernel<<<(s->batch + 31) / 32, 32, 0, s->stream>>>(u, v, plane, (size_t)s->grid_stride * s->elem,
@@ -2430,7 +2452,6 @@ int rdcnn_sim_checksums(rdcnn_sim_t s, uint64_t* out) {
   RDCNN_CUDA_TRY(cudaGetLastError());
   RDCNN_CUDA_TRY(cudaMemcpyAsync(out, d, sizeof(unsigned long long) * (size_t)s->batch, cudaMemcpyDeviceToHost,
                                  s->stream));
-  RDCNN_CUDA_TRY(cudaFreeAsync(d, s->stream));
   RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
   return RDCNN_OK;
 }
