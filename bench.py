@@ -669,8 +669,9 @@ def bench_ours(args, rank, world, local_rank, ring_devices=None):
                         "lane-ops/s of FFMA/FADD on this part"),
         "frac_at_median_clock": round(fp32_achieved / fp32_peak_tops, 4),
         "median_clock_mhz": round(sm_mhz),
-        "note": (f"27 FP32 ops per cell-update (reference arithmetic); strict issues 26 (fused -4*u_c, gated 2-op "
-                 f"x/3, and the Dv*lap_v product skipped when Dv == 1; 27 with Dv != 1) "
+        "note": (f"27 FP32 ops per cell-update (reference arithmetic); strict issues 25 on periodic lattices "
+                 f"(fused -4*u_c and -4*v_c tails, gated 2-op x/3, Dv*lap_v skipped when Dv == 1; DESIGN.md "
+                 f"section 4) "
                  f"x cell-updates per {levels}-level launch / avg launch time ({avg_launch_s * 1e6:.1f} us over "
                  f"{blocks_per_rank} blocks, {launches} launches); traffic = ncu DRAM bytes of one launch; "
                  "instruction-level account in profiles/sass_r02_wavefront_k4_classes.txt"),

@@ -167,6 +167,21 @@ constexpr int kStrictDiv2 = 2;
 // model.hpp:55 is the identity and is skipped.  The reference's default gene
 // (gene.hpp:19) and every BASELINE workload have Dv = 1.
 constexpr int kStrictDiv2U = 3;
+// kStrictDiv2U with the v Laplacian's tail fused as on the u plane:
+// RN(s - RN(4*vc)) == fma(-4, vc, s) whenever 4*vc is finite, i.e. |vc| <
+// 2^126.  For |vc| >= 2^126 the reference's v+ is non-finite at that step
+// for EVERY gene (RN(4*vc) = +-inf; Dv*lap_v, f2 + ., dt*., vc + . stay
+// non-finite, dt = 0 included: 0*inf = NaN), while the fused form may stay
+// finite.  So this instance also folds the magnitude of every level's centre
+// v (the value that gets multiplied by 4) and flags the launch when one
+// reaches 2^126.  A flag then means exactly what it means for the other
+// instances: the reference blows up inside this block (at the first level
+// whose centre v is that large, or earlier) -- and without such a centre the
+// fused form computes the reference's values bit for bit, so the flag is
+// raised iff the reference blows up within the block.  The host's level
+// replay (K = 1 launches of this same instance) therefore finds the exact
+// iteration unchanged.  Periodic handles only.
+constexpr int kStrictDiv2UF = 4;
 
 // Round-to-nearest primitives that the compiler never contracts.
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
@@ -192,12 +207,13 @@ __device__ __forceinline__ void fhn_cell(T uc, T vc, T ur, T ul, T ud, T uu, T v
     // the fused form is bit-identical on every finite outcome.  The v plane
     // has no such guard and keeps the separate multiply.
     const T lap_u = fma_rn(T(-4), uc, add_rn(add_rn(add_rn(ur, ul), ud), uu));
-    const T lap_v = sub_rn(add_rn(add_rn(add_rn(vr, vl), vd), vu), mul_rn(T(4), vc));
+    const T lap_v = kArith == kStrictDiv2UF ? fma_rn(T(-4), vc, add_rn(add_rn(add_rn(vr, vl), vd), vu))
+                                            : sub_rn(add_rn(add_rn(add_rn(vr, vl), vd), vu), mul_rn(T(4), vc));
     const T uu3 = kArith >= kStrictDiv2 ? div3_rn2(mul_rn(uc, uc)) : div3_rn(mul_rn(uc, uc));
     const T f1 = sub_rn(mul_rn(uc, sub_rn(p.c, uu3)), vc);
     const T f2 = mul_rn(neg_eps, add_rn(sub_rn(uc, mul_rn(p.b, vc)), p.a));
     un = add_rn(uc, mul_rn(p.dt, add_rn(f1, mul_rn(p.du, lap_u))));
-    const T dv_lap = kArith == kStrictDiv2U ? lap_v : mul_rn(p.dv, lap_v);
+    const T dv_lap = kArith >= kStrictDiv2U ? lap_v : mul_rn(p.dv, lap_v);
     vn = add_rn(vc, mul_rn(p.dt, add_rn(f2, dv_lap)));
   } else {
     // Opt-in fast mode: same formula, FMA-contracted and reassociated.
@@ -254,6 +270,20 @@ template <int W, class T>
 __device__ __forceinline__ void fold_finite(Finite<T>& f, const Row<W, T>& r) {
 #pragma unroll
   for (int k = 0; k < W; ++k) f.add(r.u[k], r.v[k]);
+}
+
+// kStrictDiv2UF: the largest |v| among a level's centre cells (fp32 only).
+template <int W, class T, int kArith>
+__device__ __forceinline__ void fold_centre_v(Finite<T>& f, const Row<W, T>& c) {
+  if constexpr (kArith == kStrictDiv2UF) {
+#pragma unroll
+    for (int k = 0; k + 1 < W; k += 2) f.add(c.v[k], c.v[k + 1]);
+    if constexpr (W % 2 == 1) f.add(c.v[W - 1], c.v[W - 1]);
+  }
+}
+// Any |v| >= 2^126 (or non-finite) among the folded centres of the warp.
+__device__ __forceinline__ bool big_centre_in_warp(const Finite<float>& f) {
+  return __reduce_max_sync(kFull, __float_as_uint(f.m)) >= 0x7E800000u;
 }
 
 // 16-byte vector store when a lane's group is 16 bytes, else scalar stores.
@@ -708,6 +738,7 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
   Row<W, T> l0[3];
 #endif
   Finite<T> fin;
+  Finite<T> big;  // kStrictDiv2UF: centre |v| (fold_centre_v)
   const bool store = owner && frozen == 0u;
   // The 6-slot ring is two halves of 3: tick j lives in slot j % 6, i.e.
   // slot ph of the half the current 3-tick group uses; the prefetch of tick
@@ -733,6 +764,7 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
         const Row<W, T>& up = win[t - 2][ph];
         const Row<W, T>& ce = win[t - 2][(ph + 1) % 3];
         const Row<W, T>& dn = win[t - 2][(ph + 2) % 3];
+        fold_centre_v<W, T, kArith>(big, ce);
         if (t < K) {
           level_row<W, T, kArith, kWrap>(up, ce, dn, win[t - 1][ph], p, neg_eps, lane_l, lane_r);
         } else {
@@ -786,6 +818,7 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
       read_staged<W, T>(lane_off + (ph >= 1 ? half_now + (ph - 1) * kSlot : half_other + 2 * kSlot), ce);
       read_staged<W, T>(lane_off + half_now + ph * kSlot, dn);
 #endif
+      fold_centre_v<W, T, kArith>(big, ce);
       if constexpr (K == 1) {
         Row<W, T> o;
         level_row<W, T, kArith, kWrap>(up, ce, dn, o, p, neg_eps, lane_l, lane_r);
@@ -837,7 +870,13 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
     }
   }
 
-  if (!store) fin = Finite<T>{};  // halo lanes and frozen grids never flag
+  if (!store) {  // halo lanes and frozen grids never flag
+    fin = Finite<T>{};
+    big = Finite<T>{};
+  }
+  if constexpr (kArith == kStrictDiv2UF) {
+    if (big_centre_in_warp(big)) return true;
+  }
   return fin.bad_in_warp();
 }
 

@@ -93,8 +93,8 @@ int k_index(int k) { return k == 1 ? 0 : k == 2 ? 1 : k == 4 ? 2 : 3; }
 template <class T>
 struct KernelTable {
   using Fn = void (*)(StepArgsT<T>);
-  Fn fn[2][4][4][2][2] = {};        // [wide][k][arith][per_grid][wrap]
-  int resident[2][4][4][2][2] = {};
+  Fn fn[2][4][5][2][2] = {};        // [wide][k][arith][per_grid][wrap]
+  int resident[2][4][5][2][2] = {};
 };
 
 template <class T, int W, int KI, int FI, int PI>
@@ -117,6 +117,8 @@ void fill_k(KernelTable<T>& t) {
   fill_one<T, W, KI, 2, 1>(t);
   fill_one<T, W, KI, 3, 0>(t);
   fill_one<T, W, KI, 3, 1>(t);
+  fill_one<T, W, KI, 4, 0>(t);
+  fill_one<T, W, KI, 4, 1>(t);
 }
 
 template <class T, int W>
@@ -540,6 +542,7 @@ struct rdcnn_sim {
   int params_stride = 0;
   bool div2_ok = true;      // every gene has |c| >= 2^-90: the 2-op x/3 instance is exact
   bool unit_dv = false;     // every gene has Dv == 1: the Dv*lap_v product is the identity
+  bool replaying = false;   // replay_grid: the reference-order instance, so the post-blow-up state is its
   int arith_override = -1;  // RDCNN_DIV3 / tests: force the 3-op (0) or 2-op (2) strict instance
   unsigned* d_flags = nullptr;  // batch words (+1 scratch for replays)
   unsigned* h_flags = nullptr;  // pinned mirror
@@ -622,7 +625,10 @@ int arith_for(const rdcnn_sim* s) {
   if (s->mode == RDCNN_FAST) return rdcnn_dev::kFastArith;
   if (sizeof(T) != 4 || !s->div2_ok || s->arith_override == 0) return rdcnn_dev::kStrictArith;
   if (s->arith_override == 2 || !s->unit_dv) return rdcnn_dev::kStrictDiv2;
-  return rdcnn_dev::kStrictDiv2U;
+  // The fused v tail (kStrictDiv2UF) for periodic handles; slabs (their own
+  // replay protocol) and RDCNN_DIV3=u keep the separate 4*v_c product.
+  if (s->slab || s->replaying || s->arith_override == 3) return rdcnn_dev::kStrictDiv2U;
+  return rdcnn_dev::kStrictDiv2UF;
 }
 
 // The gate of the 2-op x/3: |c| >= 2^-90 (false for NaN).
@@ -890,7 +896,8 @@ int alloc_common(rdcnn_sim* s) {
   // A/B and tests: RDCNN_DIV3=3 pins the 3-op x/3 strict instance, =2 the
   // gated 2-op one with the Dv*lap_v product kept (still subject to its
   // gate); unset or anything else: automatic.
-  if (const char* e = std::getenv("RDCNN_DIV3")) s->arith_override = e[0] == '3' ? 0 : e[0] == '2' ? 2 : -1;
+  if (const char* e = std::getenv("RDCNN_DIV3"))
+    s->arith_override = e[0] == '3' ? 0 : e[0] == '2' ? 2 : e[0] == 'u' ? 3 : -1;
   RDCNN_CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   RDCNN_CUDA_TRY(cudaEventCreate(&s->ev0));
   RDCNN_CUDA_TRY(cudaEventCreate(&s->ev1));
@@ -1001,6 +1008,15 @@ Schedule make_schedule(long steps, int kmax) {
 // buffer `final_buf`.  Returns the 1-based level (1..k) in *level_out.
 template <class T>
 int replay_grid(rdcnn_sim* s, int g, int in_buf, int k, int final_buf, int* level_out) {
+  // Level by level with the reference-order instance (kStrictDiv2U, not the
+  // fused-v-tail one): the same first bad level either way (fhn_stencil.cuh
+  // kStrictDiv2UF), and the state it leaves is the reference's own
+  // post-blow-up state (non-finite exactly where the reference's is).
+  struct Guard {
+    rdcnn_sim* s;
+    ~Guard() { s->replaying = false; }
+  } guard{s};
+  s->replaying = true;
   unsigned* scratch = s->d_flags + s->batch;
   int a_buf = in_buf;
   const size_t off = (size_t)g * (size_t)s->grid_stride;
@@ -1056,7 +1072,9 @@ using ClusterFn = void (*)(rdcnn_dev::ClusterArgs);
 // instance (kStrictDiv2 alone is not instantiated here: fewer kernels).
 int cluster_arith(const rdcnn_sim* s) {
   const int a = arith_for<float>(s);
-  return a == rdcnn_dev::kStrictDiv2 ? rdcnn_dev::kStrictArith : a;
+  return a == rdcnn_dev::kStrictDiv2 ? rdcnn_dev::kStrictArith
+         : a == rdcnn_dev::kStrictDiv2UF ? rdcnn_dev::kStrictDiv2U  // per-step exact stop of its own
+                                         : a;
 }
 
 template <int W, int RW>

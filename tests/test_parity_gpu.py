@@ -823,3 +823,48 @@ def test_graph_replay_invalidated_by_new_params(oracle):
             u, v, _ = oracle.run(n, n, u, v, it, seven(g))
         du, dv = sim.download()
     assert np.array_equal(bits(du), bits(u)) and np.array_equal(bits(dv), bits(v))
+
+
+@pytest.mark.parametrize("levels", (1, 4, 8))
+@pytest.mark.parametrize("seed", (0, 1, 2))
+def test_fused_v_tail_large_centres(oracle, levels, seed, monkeypatch):
+    """The default strict instance for Dv == 1 fuses the v Laplacian's tail
+    (fma(-4, v_c, s), kStrictDiv2UF), which differs from the reference's
+    RN(s - RN(4*v_c)) only when |v_c| >= 2^126: there the reference's v+ is
+    non-finite while the fused value can stay finite (neighbour sums of the
+    same sign near FLT_MAX).  States with such centres planted (magnitudes on
+    both sides of 2^126, same-sign neighbours so the fused Laplacian stays
+    finite) must blow up at the reference's iteration with the reference's
+    post-blow-up finiteness mask, and match bit for bit when they do not."""
+    rows, cols, iters = 48, 128, 9
+    rng = np.random.default_rng(seed)
+    u0, v0 = oracle.init(2, rows, cols, 11 + seed)
+    u0 = u0.reshape(rows, cols).copy()
+    v0 = v0.reshape(rows, cols).copy()
+    mags = np.array([2.0 ** 126, np.nextafter(np.float32(2.0 ** 126), np.float32(0)), 1.5 * 2.0 ** 126,
+                     np.nextafter(np.float32(2.0 ** 127), np.float32(0)), 2.0 ** 125], np.float64)
+    for _ in range(4):
+        i, j = int(rng.integers(1, rows - 1)), int(rng.integers(1, cols - 1))
+        sgn = 1.0 if rng.random() < 0.5 else -1.0
+        v0[i, j] = np.float32(sgn * mags[rng.integers(len(mags))])
+        for di, dj in ((0, 1), (0, -1), (1, 0), (-1, 0)):
+            v0[i + di, j + dj] = np.float32(sgn * 2.0 ** 125 * (1.0 + rng.random()))
+        u0[i, j] = np.float32(0.0)
+    for gene in (fhn.Gene(a=-0.05), fhn.Gene(dt=0.0), fhn.Gene(Du=0.0, b=0.0)):
+        g7 = gene.to_vector()
+        ou, ov, obad = oracle.run(rows, cols, u0.reshape(-1), v0.reshape(-1), iters, g7)
+        for pin in (None, "u"):
+            if pin:
+                monkeypatch.setenv("RDCNN_DIV3", pin)
+            else:
+                monkeypatch.delenv("RDCNN_DIV3", raising=False)
+            with fhn.Simulator(rows, cols, levels=levels, persistent=-1) as sim:
+                sim.set_params(gene)
+                sim.upload(u0.reshape(-1), v0.reshape(-1))
+                bad = int(sim.advance(iters)[0])
+                u, v = sim.download()
+            assert bad == obad, (g7, pin)
+            fin = np.isfinite(ou) & np.isfinite(ov)
+            assert np.array_equal(np.isfinite(u) & np.isfinite(v), fin), (g7, pin)
+            assert np.array_equal(bits(u)[fin], bits(ou)[fin]), (g7, pin)
+            assert np.array_equal(bits(v)[fin], bits(ov)[fin]), (g7, pin)
