@@ -47,7 +47,11 @@ enum rdcnn_status {
 };
 
 enum rdcnn_mode {
-  RDCNN_STRICT = 0, /* default: reference op order, IEEE RN, no FMA, no FTZ */
+  RDCNN_STRICT = 0, /* default: the reference's results bit for bit (every finite
+                       value, the blow-up iteration).  fp32 launches use the
+                       exactly-equal substitutions the genes allow (fused -4*c
+                       tails, gated 2-op x/3, Dv == 1 product skipped; DESIGN.md
+                       section 4); RDCNN_DIV3=3|2|u pins simpler instances. */
   RDCNN_FAST = 1    /* opt-in: FMA-contracted, not bit-exact; checked at the
                        reference tolerance after 10 steps (test_kernels.cpp:159-172)
                        and statistically to 10^4 steps (regime labels of the full
