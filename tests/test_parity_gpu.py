@@ -868,3 +868,37 @@ def test_fused_v_tail_large_centres(oracle, levels, seed, monkeypatch):
             assert np.array_equal(np.isfinite(u) & np.isfinite(v), fin), (g7, pin)
             assert np.array_equal(bits(u)[fin], bits(ou)[fin]), (g7, pin)
             assert np.array_equal(bits(v)[fin], bits(ov)[fin]), (g7, pin)
+
+
+@pytest.mark.parametrize("rows,cols", [(40, 124), (37, 136), (64, 248), (48, 4096), (33, 152)])
+def test_column_strip_shapes_vs_oracle(oracle, rows, cols):
+    """K = 4 single lattices whose last 4-column band would own only a few
+    column groups run those columns as one-column-per-lane strip bands in the
+    same launch (kStrip; 124/136/248/4096 columns); 152 columns keep the plain
+    plan.  Bit-exact against the oracle, with a blow-up planted inside the
+    strip columns reported at the oracle's iteration."""
+    iters = 23
+    u0, v0 = oracle.init(2, rows, cols, 9)
+    g7 = fhn.Gene(a=-0.05).to_vector()
+    ou, ov, obad = oracle.run(rows, cols, u0, v0, iters, g7)
+    with fhn.Simulator(rows, cols, levels=4, persistent=-1) as sim:
+        sim.set_params(fhn.Gene(a=-0.05))
+        sim.upload(u0, v0)
+        bad = int(sim.advance(iters)[0])
+        u, v = sim.download()
+    assert bad == obad == 0
+    assert np.array_equal(bits(u), bits(ou)) and np.array_equal(bits(v), bits(ov))
+    # a blow-up seeded in the last columns (the strip's), at iteration > 1
+    u1, v1 = u0.reshape(rows, cols).copy(), v0.reshape(rows, cols).copy()
+    u1[rows // 2, cols - 3] = np.float32(3.0e12)
+    ou, ov, obad = oracle.run(rows, cols, u1.reshape(-1), v1.reshape(-1), iters, g7)
+    assert obad > 1
+    with fhn.Simulator(rows, cols, levels=4, persistent=-1) as sim:
+        sim.set_params(fhn.Gene(a=-0.05))
+        sim.upload(u1.reshape(-1), v1.reshape(-1))
+        bad = int(sim.advance(iters)[0])
+        u, v = sim.download()
+    assert bad == obad
+    fin = np.isfinite(ou) & np.isfinite(ov)
+    assert np.array_equal(np.isfinite(u) & np.isfinite(v), fin)
+    assert np.array_equal(bits(u)[fin], bits(ou)[fin]) and np.array_equal(bits(v)[fin], bits(ov)[fin])
