@@ -62,13 +62,6 @@ struct StepArgsT {
   int n_bands;
   int band_groups;        // useful W-groups per band
   int halo_groups;        // halo W-groups each side (0 = full-width wrap)
-  // Column strip (kStrip instances; single periodic lattices):
-  // when the last W-wide band would hold only a few useful groups, columns
-  // [s_col0, cols) go to one-column-per-lane bands (W = 1, halo K lanes)
-  // run by warps strip_warp0 .. strip_warp0 + n_segs*s_n_bands - 1 of the
-  // same launch; the W-wide bands own the columns below s_col0.
-  long long strip_warp0;
-  int s_n_bands, s_band_groups, s_halo_groups, s_col0;
   int batch;
   ParamsT<T> shared;      // the gene when every grid shares one (kernel-param
                           // space: the FP ops read it as constant-bank operands)
@@ -557,16 +550,12 @@ struct MinBlocks {
 // returns whether a stored value was non-finite (folded over the warp).
 // (A persistent variant that looped over blocks, each warp waiting only for
 // its 8 neighbours, measured 2.5 % slower than launches + PDL: profiles/.)
-// Band geometry: `band_groups` useful W-groups per band starting at group
-// `g0`, `halo_groups` halo groups each side; a lane owns its group iff it is
-// useful and below `g_end` (groups past it belong to other bands or wrap).
 template <int K, int W, class T, int kArith, bool kPerGrid, bool kPeer, bool kWrap, bool kTee>
 __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned char* smem_raw, int lane, int wib,
                                                 int g, int band, int seg, unsigned frozen,
                                                 const T* __restrict__ u_in_b, const T* __restrict__ v_in_b,
                                                 T* __restrict__ u_out_b, T* __restrict__ v_out_b,
-                                                BlockStats& stats, int band_groups, int halo_groups, int g0,
-                                                int g_end) {
+                                                BlockStats& stats) {
   static_assert(!kTee || (kPeer && RDCNN_L0REG), "the checkpoint tee is a slab (kPeer) feature");
   // Shared gene: read straight from the kernel-parameter bank.  Per-grid
   // genes (sweeps) come from global memory once per warp.
@@ -574,12 +563,12 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
   const T neg_eps = -p.eps;  // reference model.hpp:45 negates eps first
 
   const int G = a.cols / W;
-  const int gl = g0 + band * band_groups - halo_groups + lane;
+  const int gl = band * a.band_groups - a.halo_groups + lane;
   const int grp = wrap_index(gl, G);
-  // Store the band's useful lanes; gl >= g_end when a band overhangs a grid
-  // narrower than itself (the wrapped duplicates are not stored twice) or
-  // the columns a strip owns.
-  const bool owner = lane >= halo_groups && lane < halo_groups + band_groups && gl < g_end;
+  // Store the band's useful lanes; gl >= G only when a band overhangs a grid
+  // narrower than itself (the wrapped duplicates are not stored twice).
+  const bool owner =
+      lane >= a.halo_groups && lane < a.halo_groups + a.band_groups && gl < G;
   const int lane_l = (lane + 31) & 31;
   const int lane_r = (lane + 1) & 31;
 
@@ -698,7 +687,7 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
   bool use_tma = false;
   int tma_x = 0, tma_y = 0;
   if constexpr (kBulk) {
-    const int gl0 = g0 + band * band_groups - halo_groups;  // lane 0's column group
+    const int gl0 = band * a.band_groups - a.halo_groups;  // lane 0's column group
     const int grp0 = wrap_index(gl0, G);
     int na = 32;
     if (gl0 < 0) na = -gl0;
@@ -914,31 +903,21 @@ __device__ __forceinline__ bool wavefront_block(const StepArgsT<T>& a, unsigned 
 // stage those rows straight from the neighbour's input buffer (peer memory)
 // and publish completion -- the halo exchange is fused into the step.
 template <int K, int W, class T, int kArith, bool kPerGrid, bool kPeer = false, bool kWrap = false,
-          bool kTee = false, bool kStrip = false>
+          bool kTee = false>
 __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T, W>::value)
     fhn_wavefront_kernel(const __grid_constant__ StepArgsT<T> a) {
-  static_assert(!kStrip || (!kPeer && !kWrap && !kTee && W > 1), "column strips: periodic banded instances");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = kWarpsPerCta == 1 ? 0 : int(threadIdx.x >> 5);
   const long long warp_id = (long long)blockIdx.x * kWarpsPerCta + wib;
   const long long per_grid = (long long)a.n_segs * a.n_bands;
-  if (warp_id >= (kStrip ? a.strip_warp0 + (long long)a.n_segs * a.s_n_bands : per_grid * a.batch)) return;
+  if (warp_id >= per_grid * a.batch) return;
   unsigned long long t_start = 0;
   if (a.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-  const bool in_strip = kStrip && warp_id >= a.strip_warp0;  // strips: batch 1
-  int g, band, seg;
-  if (in_strip) {
-    const int rem = int(warp_id - a.strip_warp0);
-    g = 0;
-    band = rem % a.s_n_bands;
-    seg = rem / a.s_n_bands;
-  } else {
-    g = int(warp_id / per_grid);
-    const int rem = int(warp_id - (long long)g * per_grid);
-    band = rem % a.n_bands;
-    seg = rem / a.n_bands;
-  }
+  const int g = int(warp_id / per_grid);
+  const int rem = int(warp_id - (long long)g * per_grid);
+  const int band = rem % a.n_bands;
+  const int seg = rem / a.n_bands;
 
   // A grid that already blew up in an earlier launch of this advance stays
   // frozen (no stores), so the input of its first bad launch survives for
@@ -954,21 +933,8 @@ __global__ void __launch_bounds__(kCtaThreads, MinBlocks<K, T, W>::value)
   const unsigned frozen = fl != 0u && fl != a.tag;
 
   BlockStats stats;
-  bool bad;
-  if constexpr (kStrip) {
-    if (in_strip)
-      bad = wavefront_block<K, 1, T, kArith, kPerGrid, false, false, false>(
-          a, smem_raw, lane, wib, g, band, seg, frozen, a.u_in, a.v_in, a.u_out, a.v_out, stats, a.s_band_groups,
-          a.s_halo_groups, a.s_col0, a.cols);
-    else
-      bad = wavefront_block<K, W, T, kArith, kPerGrid, false, false, false>(
-          a, smem_raw, lane, wib, g, band, seg, frozen, a.u_in, a.v_in, a.u_out, a.v_out, stats, a.band_groups,
-          a.halo_groups, 0, a.s_col0 / W);
-  } else {
-    bad = wavefront_block<K, W, T, kArith, kPerGrid, kPeer, kWrap, kTee>(
-        a, smem_raw, lane, wib, g, band, seg, frozen, a.u_in, a.v_in, a.u_out, a.v_out, stats, a.band_groups,
-        a.halo_groups, 0, a.cols / W);
-  }
+  const bool bad = wavefront_block<K, W, T, kArith, kPerGrid, kPeer, kWrap, kTee>(
+      a, smem_raw, lane, wib, g, band, seg, frozen, a.u_in, a.v_in, a.u_out, a.v_out, stats);
 
   if (bad && lane == 0 && a.flags != nullptr) atomicCAS(a.flags + g, 0u, a.tag);
   if (a.trace != nullptr && lane == 0) {

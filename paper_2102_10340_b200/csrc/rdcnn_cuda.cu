@@ -95,7 +95,6 @@ struct KernelTable {
   using Fn = void (*)(StepArgsT<T>);
   Fn fn[2][4][5][2][2] = {};        // [wide][k][arith][per_grid][wrap]
   int resident[2][4][5][2][2] = {};
-  Fn strip[5][2] = {};              // column-strip instances, fp32 wide K=4: [arith][per_grid]
 };
 
 template <class T, int W, int KI, int FI, int PI>
@@ -122,11 +121,6 @@ void fill_k(KernelTable<T>& t) {
   fill_one<T, W, KI, 4, 1>(t);
 }
 
-template <int FI, int PI>
-void fill_strip(KernelTable<float>& t) {
-  t.strip[FI][PI] = &rdcnn_dev::fhn_wavefront_kernel<4, Traits<float>::kWide, float, FI, PI == 1, false, false, false, true>;
-}
-
 template <class T, int W>
 void fill_w(KernelTable<T>& t) {
   fill_k<T, W, 0>(t);
@@ -141,11 +135,6 @@ KernelTable<T>& table() {
     KernelTable<T> x;
     fill_w<T, 1>(x);
     fill_w<T, Traits<T>::kWide>(x);
-    if constexpr (sizeof(T) == 4) {
-      fill_strip<0, 0>(x); fill_strip<0, 1>(x); fill_strip<1, 0>(x); fill_strip<1, 1>(x);
-      fill_strip<2, 0>(x); fill_strip<2, 1>(x); fill_strip<3, 0>(x); fill_strip<3, 1>(x);
-      fill_strip<4, 0>(x); fill_strip<4, 1>(x);
-    }
     return x;
   }();
   return t;
@@ -174,15 +163,6 @@ int resident_blocks(int k, int w, int arith, bool per_grid, bool wrap) {
     __atomic_store_n(slot, r, __ATOMIC_RELAXED);
   }
   return r;
-}
-
-// Column strips (launch_range); RDCNN_STRIP=0 turns them off.
-bool strip_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("RDCNN_STRIP");
-    return !(e && e[0] == '0');
-  }();
-  return on;
 }
 
 // Programmatic dependent launch (PDL): consecutive stencil launches of an
@@ -271,10 +251,10 @@ int peer_resident_blocks(int k, int w, int arith, bool wrap, bool tee) {
 
 template <class T>
 cudaError_t launch_stencil(int k, int w, int arith, bool per_grid, bool wrap, const StepArgsT<T>& a,
-                           long long warps, cudaStream_t s, bool full, bool strip = false) {
+                           long long warps, cudaStream_t s, bool full) {
   if (warps <= 0) return cudaSuccess;
   if (k != 1 && k != 2 && k != 4 && k != 8) return cudaErrorInvalidValue;
-  auto fn = strip ? table<T>().strip[arith][per_grid] : table<T>().fn[w > 1][k_index(k)][arith][per_grid][wrap];
+  auto fn = table<T>().fn[w > 1][k_index(k)][arith][per_grid][wrap];
   if (!fn) return cudaErrorInvalidValue;
   const long long blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
   return launch_pdl(fn, (unsigned)blocks, smem_for<T>(w), s, a, full);
@@ -905,35 +885,9 @@ cudaError_t launch_range(rdcnn_sim* s, int k, StepArgsT<T> a, int row_begin, int
   a.n_bands = p.n_bands;
   a.band_groups = p.band_groups;
   a.halo_groups = p.halo;
-  long long warps = p.warps;
-  // Column strip: when the last W-wide band would own only a few column
-  // groups (4096 columns: 35 bands of 30 groups, the last one 4), those
-  // columns go to one-column-per-lane bands of the same launch instead --
-  // a W = 1 warp costs about a third of a W = 4 one.
-  bool strip = false;
-  if constexpr (sizeof(T) == 4) {
-    if (k == 4 && w == Traits<float>::kWide && !wrap && !s->slab && a.batch == 1 && strip_enabled() &&
-        table<T>().strip[arith][per_grid]) {
-      const int G = s->cols / w;
-      const int useful = 32 - 2 * p.halo;
-      const int nb = G / useful;
-      const int left = (G - nb * useful) * w;  // columns for the strip
-      if (nb >= 1 && left > 0 && left <= 32 - 2 * k) {
-        strip = true;
-        a.n_bands = nb;
-        a.band_groups = useful;
-        a.s_n_bands = 1;
-        a.s_band_groups = left;
-        a.s_halo_groups = k;
-        a.s_col0 = nb * useful * w;
-        a.strip_warp0 = (long long)p.n_segs * nb;
-        warps = a.strip_warp0 + (long long)p.n_segs * a.s_n_bands;
-      }
-    }
-  }
   ++s->launches;
-  return launch_stencil<T>(k, w, arith, per_grid, wrap, a, warps, st,
-                           4 * warps >= 3LL * rw * s->sm_count, strip);
+  return launch_stencil<T>(k, w, arith, per_grid, wrap, a, p.warps, st,
+                           4 * p.warps >= 3LL * rw * s->sm_count);
 }
 
 int alloc_common(rdcnn_sim* s) {
