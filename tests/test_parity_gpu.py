@@ -872,11 +872,11 @@ def test_fused_v_tail_large_centres(oracle, levels, seed, monkeypatch):
 
 @pytest.mark.parametrize("rows,cols", [(40, 124), (37, 136), (64, 248), (48, 4096), (33, 152)])
 def test_column_strip_shapes_vs_oracle(oracle, rows, cols):
-    """K = 4 single lattices whose last 4-column band would own only a few
-    column groups run those columns as one-column-per-lane strip bands in the
-    same launch (kStrip; 124/136/248/4096 columns); 152 columns keep the plain
-    plan.  Bit-exact against the oracle, with a blow-up planted inside the
-    strip columns reported at the oracle's iteration."""
+    """K = 4 single lattices whose last 4-column band owns only a few column
+    groups (124/136/248/4096 columns; 152 for contrast) -- the shapes of the
+    measured-and-rejected column-strip plan (profiles/README.md): bit-exact
+    against the oracle, with a blow-up planted in the last columns reported
+    at the oracle's iteration."""
     iters = 23
     u0, v0 = oracle.init(2, rows, cols, 9)
     g7 = fhn.Gene(a=-0.05).to_vector()
