@@ -20,6 +20,7 @@
 #include <new>
 #include <tuple>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <dlfcn.h>
@@ -1505,6 +1506,34 @@ int advance_impl(rdcnn_sim* s, long steps, long* first_bad) {
   return advance_launches<T>(s, steps, first_bad);
 }
 
+// Device-to-host copies into pageable memory that was never written (a
+// fresh numpy/malloc buffer) spend most of their time in the page faults of
+// the single copying thread: 268 MB took 55-66 ms against 13 ms into touched
+// pages (tools/download_timing.py).  Large pageable destinations are
+// therefore faulted in first by several threads (one store per page; the
+// copy overwrites every byte anyway).  Pinned destinations are left alone.
+void prefault_pageable(void* dst, size_t bytes) {
+  if (bytes < (32u << 20)) return;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, dst) == cudaSuccess && at.type != cudaMemoryTypeUnregistered) return;
+  cudaGetLastError();
+  const long page = sysconf(_SC_PAGESIZE) > 0 ? sysconf(_SC_PAGESIZE) : 4096;
+  const unsigned hw = std::thread::hardware_concurrency();
+  const unsigned nt = std::max(1u, std::min(16u, hw ? hw : 1u));
+  const size_t slice = (bytes / nt + (size_t)page - 1) / (size_t)page * (size_t)page;
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t) {
+    const size_t lo = (size_t)t * slice;
+    if (lo >= bytes) break;
+    const size_t hi = std::min(bytes, lo + slice);
+    th.emplace_back([=] {
+      volatile char* p = static_cast<char*>(dst);
+      for (size_t i = lo; i < hi; i += (size_t)page) p[i] = 0;
+    });
+  }
+  for (auto& t : th) t.join();
+}
+
 int copy_state(rdcnn_sim* s, void* u, void* v, bool upload) {
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   if (upload) s->ckpt_age = -1;  // the checkpoint no longer precedes the state
@@ -1514,6 +1543,10 @@ int copy_state(rdcnn_sim* s, void* u, void* v, bool upload) {
   if (!s->slab) {
     const size_t bytes = (size_t)s->rows * s->cols * s->batch * e;
     const cudaMemcpyKind kind = upload ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    if (!upload) {
+      prefault_pageable(u, bytes);
+      prefault_pageable(v, bytes);
+    }
     RDCNN_CUDA_TRY(cudaMemcpyAsync(upload ? (void*)du : u, upload ? u : (void*)du, bytes, kind, s->stream));
     RDCNN_CUDA_TRY(cudaMemcpyAsync(upload ? (void*)dv : v, upload ? v : (void*)dv, bytes, kind, s->stream));
   } else {
@@ -1525,6 +1558,8 @@ int copy_state(rdcnn_sim* s, void* u, void* v, bool upload) {
       RDCNN_CUDA_TRY(cudaMemcpy2DAsync(du + row0, dpitch, u, w, w, s->rows, cudaMemcpyHostToDevice, s->stream));
       RDCNN_CUDA_TRY(cudaMemcpy2DAsync(dv + row0, dpitch, v, w, w, s->rows, cudaMemcpyHostToDevice, s->stream));
     } else {
+      prefault_pageable(u, w * (size_t)s->rows);
+      prefault_pageable(v, w * (size_t)s->rows);
       RDCNN_CUDA_TRY(cudaMemcpy2DAsync(u, w, du + row0, dpitch, w, s->rows, cudaMemcpyDeviceToHost, s->stream));
       RDCNN_CUDA_TRY(cudaMemcpy2DAsync(v, w, dv + row0, dpitch, w, s->rows, cudaMemcpyDeviceToHost, s->stream));
     }
@@ -2512,7 +2547,10 @@ int rdcnn_sim_frame_download(rdcnn_sim_t s, int slot, void* u) {
   if (!u) return fail(RDCNN_EINVAL, "null argument");
   RDCNN_CUDA_TRY(cudaSetDevice(s->device));
   const size_t bytes = (size_t)s->batch * s->rows * s->cols * s->elem;
-  RDCNN_CUDA_TRY(cudaMemcpy(u, static_cast<char*>(s->frames) + (size_t)slot * bytes, bytes, cudaMemcpyDeviceToHost));
+  prefault_pageable(u, bytes);
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(u, static_cast<char*>(s->frames) + (size_t)slot * bytes, bytes, cudaMemcpyDeviceToHost,
+                                 s->stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
   return RDCNN_OK;
 }
 
