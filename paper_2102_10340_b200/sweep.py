@@ -160,6 +160,25 @@ def classify(frame_mins, frame_maxs, counts, cells: int, cc: ClassifierConfig, f
     return res
 
 
+def classify_batch(frame_mins, frame_maxs, counts, cells: int, cc: ClassifierConfig, final_range):
+    """classify() for every cell of a batch at once: arrays [frames, cells]
+    (and final_range [cells]) in, per-cell labels and final active fractions
+    out -- the same double-precision comparisons as classify(), elementwise
+    (tests/test_sweep_host.py checks them against it).  Cells must be finite
+    (blown-up cells are labelled before classification)."""
+    mins = np.asarray(frame_mins, np.float64)
+    maxs = np.asarray(frame_maxs, np.float64)
+    cnt = np.asarray(counts, np.int64)
+    fr = np.asarray(final_range, np.float64)
+    global_range = maxs.max(axis=0) - mins.min(axis=0)
+    homog = np.maximum(cc.homogeneity_floor, cc.homogeneity_rel * global_range)
+    c = cnt.astype(np.float64)
+    rising = np.all(c[1:] >= (1.0 - cc.dip_tolerance) * c[:-1], axis=0)
+    grew = cnt[-1] >= np.maximum(1, (cc.growth_factor * c[0]).astype(np.int64))
+    labels = np.where(fr < homog, "Homogeneous", np.where(rising & grew, "Growing", "Patterned"))
+    return labels, c[-1] / float(cells)
+
+
 def labels_csv(res: SweepResult) -> str:
     """sweep.hpp:227-247."""
     out = ["x_value,y_value,label,final_range,final_active_fraction,checksum\n"]
@@ -277,11 +296,13 @@ def _run_cells(cells: List[SweepCell], idx0: int, spec: SweepSpec, base: RunConf
     # slot holds exactly it, so only u comes back, and each cell gets a view.
     frames_u = [sim.frame_download(f).reshape(B, -1) for f in range(F)] if spec.keep_buffers else None
     fu = frames_u[-1] if frames_u is not None else sim.frame_download(F - 1).reshape(B, -1)
+    labels, fractions = classify_batch(mins, maxs, counts, rows * cols, spec.classifier, final_range)
+    counts_t = counts.T.tolist()
     for idx, c in enumerate(cells):
         if c.blew_up:
             continue
-        c.outcome = classify(mins[:, idx], maxs[:, idx], counts[:, idx], rows * cols, spec.classifier,
-                             float(final_range[idx]))
+        c.outcome = RegimeResult(label=str(labels[idx]), final_range=float(final_range[idx]),
+                                 final_active_fraction=float(fractions[idx]), activity_counts=counts_t[idx])
         c.digest = int(digests[idx])
         c.final_u = fu[idx]
         if frames_u is not None:
