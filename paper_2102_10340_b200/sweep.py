@@ -13,6 +13,7 @@ same inputs (tests/test_sweep_gpu.py).
 """
 from __future__ import annotations
 
+import copy
 import dataclasses
 import math
 import threading
@@ -333,12 +334,25 @@ def sweep_grid(spec: SweepSpec, image: Optional[np.ndarray] = None, device: int 
         base.nn, base.nm = int(image.shape[0]), int(image.shape[1])
     cells: List[SweepCell] = []
     fx, fy = GENE_FIELDS[spec.x_param], GENE_FIELDS[spec.y_param]
+    # gene_valid is a conjunction of per-field tests, so with two distinct
+    # swept fields every cell is valid iff every x and every y value is (with
+    # the base gene's other fields); otherwise the cell loop below finds and
+    # reports the first invalid cell in sweep order.
+    base = spec.base_gene
+    separable_ok = (fx != fy and
+                    all(gene_valid(dataclasses.replace(base, **{fx: float(x)})) for x in spec.x_values) and
+                    all(gene_valid(dataclasses.replace(base, **{fy: float(y)})) for y in spec.y_values))
     for y in spec.y_values:
         for x in spec.x_values:
-            g = dataclasses.replace(spec.base_gene, **{fx: float(x), fy: float(y)})
-            if not gene_valid(g):
-                raise ValueError(f"sweep cell gene invalid at {spec.x_param}={format_double(x)} "
-                                 f"{spec.y_param}={format_double(y)}")
+            if separable_ok:
+                g = copy.copy(base)
+                setattr(g, fx, float(x))
+                setattr(g, fy, float(y))
+            else:
+                g = dataclasses.replace(base, **{fx: float(x), fy: float(y)})
+                if not gene_valid(g):
+                    raise ValueError(f"sweep cell gene invalid at {spec.x_param}={format_double(x)} "
+                                     f"{spec.y_param}={format_double(y)}")
             cells.append(SweepCell(x_value=float(x), y_value=float(y), gene=g))
 
     if initial is not None:

@@ -40,3 +40,23 @@ def test_classify_batch_boundaries():
     counts = np.array([c for _, _, c in cols], np.float64).T.round().astype(np.int64)
     final_range = np.array([fr for fr, _, _ in cols])
     _check(mins, maxs, counts, cells, cc, final_range)
+
+
+def test_invalid_sweep_cell_reported_in_sweep_order():
+    """sweep.hpp: the first invalid cell (y outer, x inner) is named; the
+    separable fast path must not change which one."""
+    import pytest
+
+    from paper_2102_10340_b200.engine import RunConfig
+    from paper_2102_10340_b200.sweep import SweepSpec, sweep_grid
+
+    cfg = RunConfig()
+    cfg.nn = cfg.nm = 16
+    cfg.iter_max = 10
+    cfg.nssp = 1
+    spec = SweepSpec("du", [0.1, -0.2, 0.3], "dv", [0.5, -1.0], base_config=cfg)
+    with pytest.raises(ValueError, match=r"du=-0.2 dv=0.5"):
+        sweep_grid(spec)
+    spec = SweepSpec("du", [0.1, 0.2], "dv", [0.5, -1.0], base_config=cfg)
+    with pytest.raises(ValueError, match=r"du=0.1 dv=-1"):
+        sweep_grid(spec)
