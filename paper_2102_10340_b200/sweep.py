@@ -338,18 +338,18 @@ def sweep_grid(spec: SweepSpec, image: Optional[np.ndarray] = None, device: int 
     # swept fields every cell is valid iff every x and every y value is (with
     # the base gene's other fields); otherwise the cell loop below finds and
     # reports the first invalid cell in sweep order.
-    base = spec.base_gene
+    bg = spec.base_gene
     separable_ok = (fx != fy and
-                    all(gene_valid(dataclasses.replace(base, **{fx: float(x)})) for x in spec.x_values) and
-                    all(gene_valid(dataclasses.replace(base, **{fy: float(y)})) for y in spec.y_values))
+                    all(gene_valid(dataclasses.replace(bg, **{fx: float(x)})) for x in spec.x_values) and
+                    all(gene_valid(dataclasses.replace(bg, **{fy: float(y)})) for y in spec.y_values))
     for y in spec.y_values:
         for x in spec.x_values:
             if separable_ok:
-                g = copy.copy(base)
+                g = copy.copy(bg)
                 setattr(g, fx, float(x))
                 setattr(g, fy, float(y))
             else:
-                g = dataclasses.replace(base, **{fx: float(x), fy: float(y)})
+                g = dataclasses.replace(bg, **{fx: float(x), fy: float(y)})
                 if not gene_valid(g):
                     raise ValueError(f"sweep cell gene invalid at {spec.x_param}={format_double(x)} "
                                      f"{spec.y_param}={format_double(y)}")
