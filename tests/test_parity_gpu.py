@@ -902,3 +902,36 @@ def test_column_strip_shapes_vs_oracle(oracle, rows, cols):
     fin = np.isfinite(ou) & np.isfinite(ov)
     assert np.array_equal(np.isfinite(u) & np.isfinite(v), fin)
     assert np.array_equal(bits(u)[fin], bits(ou)[fin]) and np.array_equal(bits(v)[fin], bits(ov)[fin])
+
+
+@pytest.mark.parametrize("levels", (1, 4))
+def test_fused_v_tail_batch_one_grid_large_centre(oracle, levels):
+    """Batched per-grid genes (all Dv == 1: the fused-v-tail instance) with a
+    2^126 centre planted in one grid only: that grid blows up at iteration 1
+    with the reference's post-blow-up finiteness mask, the others stay
+    bit-identical to the oracle (per-grid flags and replay)."""
+    rows, cols, iters, B = 40, 128, 11, 3
+    genes = [fhn.Gene(Du=0.05), fhn.Gene(Du=0.07, a=-0.05), fhn.Gene(Du=0.3)]
+    u0, v0 = oracle.init(2, rows, cols, 5)
+    U = np.tile(u0, (B, 1))
+    V = np.tile(v0, (B, 1))
+    i, j = rows // 2, cols // 3
+    vv = V[1].reshape(rows, cols)
+    vv[i, j] = np.float32(2.0 ** 126)
+    for di, dj in ((0, 1), (0, -1), (1, 0), (-1, 0)):
+        vv[i + di, j + dj] = np.float32(1.5 * 2.0 ** 125)
+    with fhn.Simulator(rows, cols, batch=B, levels=levels) as sim:
+        sim.set_params(genes)
+        sim.upload(U.reshape(-1), V.reshape(-1))
+        bad = sim.advance(iters)
+        u, v = sim.download()
+    u = u.reshape(B, -1)
+    v = v.reshape(B, -1)
+    for k, g in enumerate(genes):
+        ou, ov, obad = oracle.run(rows, cols, U[k], V[k], iters, g.to_vector())
+        assert int(bad[k]) == obad, k
+        fin = np.isfinite(ou) & np.isfinite(ov)
+        assert np.array_equal(np.isfinite(u[k]) & np.isfinite(v[k]), fin), k
+        assert np.array_equal(bits(u[k])[fin], bits(ou)[fin]), k
+        assert np.array_equal(bits(v[k])[fin], bits(ov)[fin]), k
+    assert int(bad[1]) == 1 and int(bad[0]) == 0 and int(bad[2]) == 0
