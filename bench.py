@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--mode", default="strict", choices=("strict", "fast"))
     ap.add_argument("--e2e-steps", type=int, default=0,
                     help="lattices through the e2e pipeline (0: the workload's default)")
+    ap.add_argument("--e2e-states", action="store_true",
+                    help="cfg3: time the float state stream (upload u,v -> advance -> download u,v) instead of "
+                         "the image stream (pixels -> advance -> normalised edge map)")
     ap.add_argument("--e2e-depth", type=int, default=0,
                     help="lattices in flight in the e2e pipeline (0: the workload's default; 1: one after another)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -751,6 +754,52 @@ def bench_ours(args, rank, world, local_rank, ring_devices=None):
                "wall_ms_per_step": round(e2e_s * 1e3 / e2e_steps, 3),
                "device_ms_per_step": round(dev_ms / e2e_steps, 3),
                "copy_and_host_ms_per_step": round((e2e_s * 1e3 - dev_ms) / e2e_steps, 3)}
+    elif not use_slab and wl.typ == 3 and not args.e2e_states:
+        # Edge detection over a stream of images (the CeNN image-processing
+        # mode): per image its 8-bit pixels go up from pinned host memory, the
+        # device builds u = v = ka*x (init.hpp:58), advances S iterations and
+        # normalises the final u plane with its own min/max (frame.hpp:28-44)
+        # into the 8-bit edge map that comes back -- the reference CLI's
+        # image in, frames out.  Several images in flight on alternating
+        # handles, as for the state stream below.
+        cells = wl.rows_global * n
+        depth = max(1, min(args.e2e_depth or wl.e2e_depth, e2e_steps))
+        px = torch.from_numpy(np.ascontiguousarray(wl.pixels()).reshape(-1)).pin_memory()
+        outs = [torch.empty(cells, dtype=torch.uint8).pin_memory() for _ in range(depth)]
+        pipe = fhn.Pipeline(wl.rows_global, n, depth=depth, sims=[sim], device=local_rank, mode=args.mode,
+                            levels=args.levels, seg_rows=args.seg_rows)
+        pipe.set_params(gene)
+        for k, extra in enumerate(pipe.sims):  # first-use costs (graph capture, staging) stay out of the region
+            if k > 0:
+                extra.init_image_ptr(px.data_ptr(), 1.0)
+                extra.advance(S)
+            extra.frame_normalize_auto_ptr(outs[0].data_ptr())
+        jobs = [(px.data_ptr(), outs[i % depth].data_ptr()) for i in range(e2e_steps)]
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        bad = pipe.run_images(jobs, S, 1.0)
+        torch.cuda.synchronize()
+        te = torch.tensor([time.perf_counter() - t0], device=red_dev)
+        if dist is not None:  # replicas: max wall time over ranks
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        dev_ms = float(np.sum(pipe.last_device_ms))
+        pipe.close()
+        e2e_s = float(te.item())
+        e2e = {"value": round(cells * world * S * e2e_steps / e2e_s / 1e6, 2),
+               "unit": "Mcell-updates/s", "h2d_bytes_per_step": cells * world,
+               "d2h_bytes_per_step": (cells + 16) * world,
+               "path": (f"paper_2102_10340_b200.Pipeline(depth={depth}).run_images: per image "
+                        "rdcnn_sim_init_image (8-bit pixels, pinned host) -> rdcnn_sim_advance -> "
+                        "rdcnn_sim_frame_normalize_auto (final u plane -> 8-bit edge map + its min/max)"
+                        + (", images on alternating handles so copies overlap advances" if depth > 1 else "")
+                        + ("; per rank, max wall time over ranks" if world > 1 else "")),
+               "steps": e2e_steps, "lattices_in_flight": depth,
+               "wall_ms_per_step": round(e2e_s * 1e3 / e2e_steps, 3),
+               "device_ms_per_step": round(dev_ms / e2e_steps, 3)}
+        if bad.any():
+            raise RuntimeError("blow-up in the e2e image stream")
     elif not use_slab:
         # A stream of independent lattices through the public Pipeline API:
         # each one is uploaded from pinned host memory, advanced S iterations

@@ -314,6 +314,12 @@ int rdcnn_sim_frame_active(rdcnn_sim_t sim, int slot, const double* medians,
  * lround and clamping; 128 everywhere when hi <= lo. */
 int rdcnn_sim_frame_normalize(rdcnn_sim_t sim, int slot, int grid, double lo,
                               double hi, uint8_t* out);
+/* normalize_frame (frame.hpp:28-44): the same map with [lo, hi] = the
+ * plane's own min/max, found by a whole-device reduction (finite planes);
+ * *lo / *hi receive them (either may be NULL).  One call per processed image
+ * (edge detection: init_image -> advance -> this). */
+int rdcnn_sim_frame_normalize_auto(rdcnn_sim_t sim, int slot, int grid,
+                                   uint8_t* out, double* lo, double* hi);
 
 /* checksum (grid.hpp:100-126) of every grid of the current state, computed
  * on the device (one thread per grid: FNV-1a 64 over u's bytes then v's);

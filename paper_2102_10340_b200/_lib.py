@@ -115,6 +115,7 @@ SIGNATURES = {
     "rdcnn_sim_frame_stats": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "rdcnn_sim_frame_active": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "rdcnn_sim_frame_normalize": (c_int, [c_void_p, c_int, c_int, c_double, c_double, c_void_p]),
+    "rdcnn_sim_frame_normalize_auto": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "rdcnn_init_center_square_host": (c_int, [c_int, c_int, c_uint64, c_void_p, c_void_p]),
     "rdcnn_init_full_random_host": (c_int, [c_int, c_int, c_uint64, c_void_p, c_void_p]),
     "rdcnn_checksum_f32": (c_uint64, [c_void_p, c_void_p, c_size_t]),

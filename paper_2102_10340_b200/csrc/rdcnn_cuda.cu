@@ -1829,6 +1829,62 @@ __global__ void normalize_kernel(const T* __restrict__ x, long long n, double lo
   }
 }
 
+// Whole-device min/max of one plane for normalize_frame (frame.hpp:28-44):
+// values are exact in double, so the order of the reduction does not matter;
+// each block folds its grid-stride share with shuffles and one atomic pair on
+// order-preserving 64-bit keys of the doubles.
+__device__ __forceinline__ unsigned long long order_key(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ inline double key_value(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  double x;
+  std::memcpy(&x, &b, sizeof x);
+  return x;
+}
+
+template <class T>
+__global__ void minmax_kernel(const T* __restrict__ x, long long n, unsigned long long* __restrict__ keys) {
+  double mn = INFINITY, mx = -INFINITY;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double v = (double)x[i];
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(keys, order_key(mn));
+    atomicMax(keys + 1, order_key(mx));
+  }
+}
+
+template <class T>
+int normalize_impl(rdcnn_sim* s, const void* src_dev, double lo, double hi, uint8_t* out);
+
+template <class T>
+int normalize_auto_impl(rdcnn_sim* s, const void* src_dev, uint8_t* out, double* lo_out, double* hi_out) {
+  const long long n = (long long)s->rows * s->cols;
+  void* buf = nullptr;
+  const size_t key_off = ((size_t)n + 255) / 256 * 256;
+  RDCNN_TRY(scratch(s, key_off + 2 * sizeof(unsigned long long), &buf));
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(static_cast<char*>(buf) + key_off);
+  const unsigned long long init[2] = {~0ull, 0ull};
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(keys, init, sizeof init, cudaMemcpyHostToDevice, s->stream));
+  minmax_kernel<T><<<4 * s->sm_count, 256, 0, s->stream>>>(static_cast<const T*>(src_dev), n, keys);
+  RDCNN_CUDA_TRY(cudaGetLastError());
+  unsigned long long k[2];
+  RDCNN_CUDA_TRY(cudaMemcpyAsync(k, keys, sizeof k, cudaMemcpyDeviceToHost, s->stream));
+  RDCNN_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  const double lo = key_value(k[0]), hi = key_value(k[1]);
+  if (lo_out) *lo_out = lo;
+  if (hi_out) *hi_out = hi;
+  return normalize_impl<T>(s, src_dev, lo, hi, out);
+}
+
 template <class T>
 int frame_stats_impl(rdcnn_sim* s, int slot, double* mn, double* mx, double* med) {
   const long long n = (long long)s->rows * s->cols;
@@ -2585,6 +2641,23 @@ int rdcnn_sim_frame_normalize(rdcnn_sim_t s, int slot, int grid, double lo, doub
     src = static_cast<const char*>(s->frames) + ((size_t)slot * s->batch + grid) * plane;
   }
   return s->elem == 4 ? normalize_impl<float>(s, src, lo, hi, out) : normalize_impl<double>(s, src, lo, hi, out);
+}
+
+int rdcnn_sim_frame_normalize_auto(rdcnn_sim_t s, int slot, int grid, uint8_t* out, double* lo, double* hi) {
+  if (!s || !out) return fail(RDCNN_EINVAL, "null argument");
+  if (grid < 0 || grid >= s->batch) return fail(RDCNN_EINVAL, "grid %d outside the batch", grid);
+  RDCNN_CUDA_TRY(cudaSetDevice(s->device));
+  const size_t plane = (size_t)s->rows * s->cols * s->elem;
+  const void* src;
+  if (slot < 0) {
+    if (s->slab) return fail(RDCNN_EINVAL, "not a periodic handle");
+    src = static_cast<const char*>(s->buf[s->cur]) + (size_t)grid * plane;
+  } else {
+    RDCNN_TRY(frame_slot_ok(s, slot));
+    src = static_cast<const char*>(s->frames) + ((size_t)slot * s->batch + grid) * plane;
+  }
+  return s->elem == 4 ? normalize_auto_impl<float>(s, src, out, lo, hi)
+                      : normalize_auto_impl<double>(s, src, out, lo, hi);
 }
 
 // ---- host helpers ------------------------------------------------------------

@@ -361,6 +361,27 @@ class Simulator:
                                                   _ptr(out)))
         return out.reshape(self.rows, self.cols)
 
+    def frame_normalize_auto(self, slot: int = -1, grid: int = 0):
+        """normalize_frame (frame.hpp:28-44) on the device with the plane's own
+        min/max; returns (rows x cols uint8 image, lo, hi).  slot < 0 = the
+        current state."""
+        out = np.empty(self.rows * self.cols, np.uint8)
+        lo, hi = ctypes.c_double(), ctypes.c_double()
+        check(self._lib.rdcnn_sim_frame_normalize_auto(self._h, int(slot), int(grid), _ptr(out), ctypes.byref(lo),
+                                                       ctypes.byref(hi)))
+        return out.reshape(self.rows, self.cols), lo.value, hi.value
+
+    def frame_normalize_auto_ptr(self, out_ptr: int, slot: int = -1, grid: int = 0):
+        """As frame_normalize_auto into caller memory (rows*cols bytes)."""
+        lo, hi = ctypes.c_double(), ctypes.c_double()
+        check(self._lib.rdcnn_sim_frame_normalize_auto(self._h, int(slot), int(grid), ctypes.c_void_p(out_ptr),
+                                                       ctypes.byref(lo), ctypes.byref(hi)))
+        return lo.value, hi.value
+
+    def init_image_ptr(self, px_ptr: int, ka: float = 1.0):
+        """init_image from caller memory (rows*cols uint8 pixels, e.g. pinned)."""
+        check(self._lib.rdcnn_sim_init_image(self._h, ctypes.c_void_p(px_ptr), float(ka)))
+
     def device_state(self):
         u, v = ctypes.c_void_p(), ctypes.c_void_p()
         check(self._lib.rdcnn_sim_device_state(self._h, ctypes.byref(u), ctypes.byref(v)))
@@ -415,6 +436,36 @@ class Pipeline:
                 bad[i] = sim.advance(steps)[0]
                 self.last_device_ms[i] = sim.elapsed_ms()
                 sim.download_ptr(u_out, v_out)
+
+        if d == 1:
+            lane(0)
+        else:
+            with ThreadPoolExecutor(d) as ex:
+                for f in [ex.submit(lane, k) for k in range(min(d, len(jobs)))]:
+                    f.result()
+        return bad
+
+    def run_images(self, jobs, steps: int, ka: float = 1.0) -> np.ndarray:
+        """Edge detection over a stream of images (the reference's typ=3 run,
+        init.hpp:58 + frame.hpp:28-44): per job (pixels_ptr, out_ptr), both
+        rows*cols bytes of host memory -- init_image, ``steps`` iterations,
+        the final u plane normalised on the device into ``out``.  Returns
+        each job's first bad iteration (0 = stayed finite)."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        jobs = list(jobs)
+        bad = np.zeros(len(jobs), np.int64)
+        d = len(self.sims)
+        self.last_device_ms = np.zeros(len(jobs), np.float64)
+
+        def lane(k: int):
+            sim = self.sims[k]
+            for i in range(k, len(jobs), d):
+                px, out = jobs[i]
+                sim.init_image_ptr(px, ka)
+                bad[i] = sim.advance(steps)[0]
+                self.last_device_ms[i] = sim.elapsed_ms()
+                sim.frame_normalize_auto_ptr(out)
 
         if d == 1:
             lane(0)
