@@ -110,7 +110,14 @@ def test_our_arm_image_stream_e2e():
     d = run_bench("--workload", "cfg3", "--size", "512", "--steps", "2", "--warmup", "3",
                   "--iters-per-step", "20", "--no-cpu-baseline", "--e2e-steps", "4")
     assert d["e2e"]["lattices_in_flight"] == 3 and d["e2e"]["steps"] == 4 and d["e2e"]["value"] > 0
-    assert d["e2e"]["h2d_bytes_per_step"] == 2 * 4 * 512 * 512
+    # per image: its 8-bit pixels up, the normalised 8-bit edge map (+ its min/max) back
+    assert d["e2e"]["h2d_bytes_per_step"] == 512 * 512
+    assert d["e2e"]["d2h_bytes_per_step"] == 512 * 512 + 16
+    assert "run_images" in d["e2e"]["path"]
+    # the float-state stream on request: both planes each way
+    d = run_bench("--workload", "cfg3", "--size", "512", "--steps", "2", "--warmup", "3",
+                  "--iters-per-step", "20", "--no-cpu-baseline", "--e2e-steps", "4", "--e2e-states")
+    assert d["e2e"]["lattices_in_flight"] == 3 and d["e2e"]["h2d_bytes_per_step"] == 2 * 4 * 512 * 512
     d = run_bench("--size", "512", "--steps", "2", "--warmup", "3", "--iters-per-step", "40",
                   "--no-cpu-baseline", "--e2e-steps", "2")
     assert d["e2e"]["lattices_in_flight"] == 1
