@@ -186,7 +186,7 @@ __device__ __forceinline__ void cluster_row(const float (&uu)[W], const float (&
 // the wait; the rest after it.  Same operations in the same order
 // (kernels.hpp:63-72, model.hpp:37-56), so bit-identical to fhn_cell.
 struct EdgePre {
-  float su, sv, f1, f2;
+  float su, sv, f1, f2, m4v;  // m4v = RN(4 * vc) of the v Laplacian's tail
 };
 
 template <bool kDnOwn, int kArith>
@@ -201,6 +201,7 @@ __device__ __forceinline__ void cell_pre(float uc, float vc, float ur, float ul,
   const float uu3 = kArith >= kStrictDiv2 ? div3_rn2(mul_rn(uc, uc)) : div3_rn(mul_rn(uc, uc));
   e.f1 = sub_rn(mul_rn(uc, sub_rn(p.c, uu3)), vc);
   e.f2 = mul_rn(neg_eps, add_rn(sub_rn(uc, mul_rn(p.b, vc)), p.a));
+  e.m4v = mul_rn(4.0f, vc);
 }
 
 template <bool kDnOwn, int kArith>
@@ -212,7 +213,7 @@ __device__ __forceinline__ void cell_post(float uc, float vc, float ud, float vd
     sv = add_rn(sv, vd);
   }
   const float lap_u = fma_rn(-4.0f, uc, add_rn(su, uu));  // as fhn_cell: exact when 4*uc is finite
-  const float lap_v = sub_rn(add_rn(sv, vu), mul_rn(4.0f, vc));
+  const float lap_v = sub_rn(add_rn(sv, vu), e.m4v);
   un = add_rn(uc, mul_rn(p.dt, add_rn(e.f1, mul_rn(p.du, lap_u))));
   const float dv_lap = kArith == kStrictDiv2U ? lap_v : mul_rn(p.dv, lap_v);  // as fhn_cell
   vn = add_rn(vc, mul_rn(p.dt, add_rn(e.f2, dv_lap)));
@@ -328,6 +329,14 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
     for (int r = 1; r < RW - 1; ++r)
       cluster_row<W, kArith>(u[r - 1], v[r - 1], u[r], v[r], u[r + 1], v[r + 1], un[r], vn[r], p, neg_eps, lane_l,
                             lane_r);
+    // Their finiteness folds before the wait too: after it only the edge
+    // rows' work is on the step's critical path (the neighbours wait for
+    // those rows).  (Deferring the edge rows' fold to the next step's
+    // pre-wait phase measured 2 % slower: profiles/README.md.)
+#pragma unroll
+    for (int r = 1; r < RW - 1; ++r)
+#pragma unroll
+      for (int k = 0; k < W; ++k) fin.add(un[r][k], vn[r][k]);
     const unsigned phase = (unsigned)((done >> 1) & 1);
     // 2b. strict mode: the edge rows' own-row half before the wait
     EdgePre e_top[W], e_bot[W];
@@ -369,20 +378,26 @@ __global__ void __launch_bounds__(ClusterThreads<RW>::value, 1) fhn_cluster_kern
       }
     }
 #pragma unroll
+    for (int k = 0; k < W; ++k) {
+      fin.add(un[0][k], vn[0][k]);
+      if (RW > 1) fin.add(un[RW - 1][k], vn[RW - 1][k]);
+    }
+#pragma unroll
     for (int r = 0; r < RW; ++r)
 #pragma unroll
       for (int k = 0; k < W; ++k) {
         u[r][k] = un[r][k];
         v[r][k] = vn[r][k];
-        fin.add(un[r][k], vn[r][k]);
       }
     // Blow-up: record the first step whose output went non-finite (exact per
-    // warp; the minimum over warps is the lattice's).  The run continues --
-    // stopping would need every CTA to agree on the step -- and the host
-    // re-runs exactly that many steps from the untouched input.
-    if (!flagged && fin.bad_in_warp()) {
+    // lane; the minimum over lanes and warps is the lattice's).  Each lane
+    // tests its own running fold (no warp reduction on the step's critical
+    // path).  The run continues -- stopping would need every CTA to agree on
+    // the step -- and the host re-runs exactly that many steps from the
+    // untouched input.
+    if (!flagged && __float_as_uint(fin.m) >= 0x7F800000u) {
       flagged = true;
-      if (lane == 0) atomicMin(reinterpret_cast<unsigned long long*>(a.first_bad), (unsigned long long)(done + 1));
+      atomicMin(reinterpret_cast<unsigned long long*>(a.first_bad), (unsigned long long)(done + 1));
     }
   }
   cluster_barrier();
